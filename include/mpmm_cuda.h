@@ -1,0 +1,139 @@
+/*
+ * mpmm_cuda.h -- C ABI of libmpmm_cuda.so, the B200 (sm_100a) DD/QD GEMM
+ * library that replaces the reference's compiled kernel module.
+ *
+ * Conventions (all entry points)
+ * ------------------------------
+ * - Matrices are row-major views of DD (2 doubles) or QD (4 doubles)
+ *   elements, exactly the reference's C-contiguous float64 (rows, cols,
+ *   comps) arrays (reference pkg/src/mpmm/matrix.py:20,43-48).  Leading
+ *   dimensions (ld*) count ELEMENTS, not doubles.
+ * - `comps` is 2 (double-double) or 4 (quad-double).
+ * - Every function returns 0 on success or a nonzero MPMM_ERR_* code;
+ *   mpmm_last_error() then holds a message (thread-local).  No C++
+ *   exception crosses this boundary.  As in the reference, kernels never
+ *   fail on overflow/NaN; the caller checks (multiply.py:124-127), here via
+ *   the optional `nonfinite` device flag.
+ * - Ownership: the caller allocates and owns every buffer; the library
+ *   keeps no state between calls except the thread-local error text.
+ * - Reentrant: concurrent calls on disjoint outputs are safe
+ *   (multiply.py:99-112 relies on that for the reference kernels).
+ * - Results are bit-identical to the reference CPU kernels for |x| < 2^996
+ *   and no underflow of TwoProd error terms (reference eft.py:21-24).
+ */
+#ifndef MPMM_CUDA_H
+#define MPMM_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPMM_ABI_VERSION 1
+
+#define MPMM_OK 0
+#define MPMM_ERR_ARG 1    /* bad argument (shape, comps, algo, range)     */
+#define MPMM_ERR_CUDA 2   /* a CUDA runtime call failed                   */
+#define MPMM_ERR_NODEV 3  /* no CUDA device                               */
+
+#define MPMM_ALGO_SIMPLE 0
+#define MPMM_ALGO_BLOCK 1
+
+int mpmm_abi_version(void);
+const char *mpmm_last_error(void);
+/* Number of visible CUDA devices (0 without a GPU; never an error). */
+int mpmm_device_count(int *count);
+/* The CTA tile a reference block size n_min selects. */
+int mpmm_tile_for_nmin(int64_t n_min, int *tile, int *super_tiles);
+/* Launch geometry on the current device: CTA output tile, threads per CTA,
+ * resident CTAs per SM and the SM count -- the inputs of the wave-aware
+ * time predictor (predict.py; reference predict.py:37-50 assumes a CPU). */
+int mpmm_gemm_geometry(int comps, int algo, int64_t n_min, int *tile_m, int *tile_n,
+                       int *threads, int *ctas_per_sm, int *sm_count);
+
+/* ---------------------------------------------------------------------------
+ * Reference kernel-module protocol on HOST pointers
+ * (reference _kernels.pyx:36-452; consumed at multiply.py:140-145,
+ * :154-159, :195-200).  Each call copies its inputs to the current device,
+ * computes, copies the written rows back and synchronises.  a is (m,l),
+ * b is (l,n), c is (m,n), x/y/out are (rows,cols), all C-contiguous.
+ * ------------------------------------------------------------------------- */
+
+/* _kernels.pyx:36-100: rows [i0,i1) of c = a*b (accumulator from zero). */
+int mpmm_dd_simple_rows(const double *a, const double *b, double *c, int64_t m, int64_t l,
+                        int64_t n, int64_t i0, int64_t i1);
+/* _kernels.pyx:344-363 */
+int mpmm_qd_simple_rows(const double *a, const double *b, double *c, int64_t m, int64_t l,
+                        int64_t n, int64_t i0, int64_t i1);
+/* _kernels.pyx:103-186: cells [cell0,cell1) of the ceil(m/n_min) x
+ * ceil(n/n_min) block grid, flattened row-major, ACCUMULATED INTO c. */
+int mpmm_dd_block_cells(const double *a, const double *b, double *c, int64_t m, int64_t l,
+                        int64_t n, int64_t n_min, int64_t cell0, int64_t cell1);
+/* _kernels.pyx:366-404 */
+int mpmm_qd_block_cells(const double *a, const double *b, double *c, int64_t m, int64_t l,
+                        int64_t n, int64_t n_min, int64_t cell0, int64_t cell1);
+/* _kernels.pyx:207-230 / :407-452: rows [i0,i1) of out = x +/- y. */
+int mpmm_dd_ewise_add(const double *x, const double *y, double *out, int64_t rows,
+                      int64_t cols, int64_t i0, int64_t i1);
+int mpmm_dd_ewise_sub(const double *x, const double *y, double *out, int64_t rows,
+                      int64_t cols, int64_t i0, int64_t i1);
+int mpmm_qd_ewise_add(const double *x, const double *y, double *out, int64_t rows,
+                      int64_t cols, int64_t i0, int64_t i1);
+int mpmm_qd_ewise_sub(const double *x, const double *y, double *out, int64_t rows,
+                      int64_t cols, int64_t i0, int64_t i1);
+
+/* ---------------------------------------------------------------------------
+ * Device-resident entry points: all matrix pointers are DEVICE pointers on
+ * the current device, `stream` is a cudaStream_t (NULL = legacy default).
+ * Asynchronous: they enqueue work and return.
+ * ------------------------------------------------------------------------- */
+
+/* C = A*B (accumulate=0) or C += A*B (accumulate=1), m x n output,
+ * inner dimension l.  algo MPMM_ALGO_SIMPLE (reference matmul_simple,
+ * multiply.py:163-168) or MPMM_ALGO_BLOCK with block size n_min
+ * (matmul_block, multiply.py:171-182).  nonfinite: optional device int,
+ * OR-ed with 1 when an output component is not finite. */
+int mpmm_gemm_dev(int comps, int algo, int64_t n_min, int64_t m, int64_t l, int64_t n,
+                  const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
+                  int64_t ldc, int accumulate, int *nonfinite, void *stream);
+
+/* The reference's cell-range protocol on device pointers
+ * (_kernels.pyx:103-186 / :366-404): cells [cell0,cell1) accumulate into C. */
+int mpmm_block_cells_dev(int comps, int64_t n_min, int64_t cell0, int64_t cell1, int64_t m,
+                         int64_t l, int64_t n, const double *A, int64_t lda, const double *B,
+                         int64_t ldb, double *C, int64_t ldc, void *stream);
+
+/* O = ((X sy*Y) sz*Z) sw*W elementwise for nops = 1..3 chained reference
+ * ewise ops (signs +1/-1; Z/W unused below their nops).  Strassen's operand
+ * sums and quadrant combinations (multiply.py:313-337). */
+int mpmm_ewise_dev(int comps, int nops, int64_t rows, int64_t cols, const double *X,
+                   int64_t ldx, const double *Y, int64_t ldy, int sy, const double *Z,
+                   int64_t ldz, int sz, const double *W, int64_t ldw, int sw, double *O,
+                   int64_t ldo, void *stream);
+
+/* multiply.py:124-127 _check_finite on the device: *flag |= 1 if any
+ * component of the rows x cols view X is not finite. */
+int mpmm_nonfinite_dev(int comps, int64_t rows, int64_t cols, const double *X, int64_t ldx,
+                       int *flag, void *stream);
+
+/* FP64 roofline micro-benchmark: blocks x threads threads each run 8
+ * independent chains of `iters` DFMA (op 0) or DADD (op 1). */
+int mpmm_fp64_burn_dev(int op, int blocks, int threads, int64_t iters, double *scratch,
+                       void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Host-side verification helpers (reference matrix.py:207-294): Frobenius
+ * norm and relative difference evaluated sequentially in DD/QD arithmetic,
+ * exactly like the reference.  x, y: `count` elements of `comps` doubles.
+ * Return 0, 1 on overflow (reference RangeError), 2 on a negative square.
+ * ------------------------------------------------------------------------- */
+int mpmm_host_frobenius_norm(int comps, const double *x, int64_t count, double *out);
+int mpmm_host_frobenius_rel_diff(int comps, const double *x, const double *y, int64_t count,
+                                 double *out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPMM_CUDA_H */

@@ -1,0 +1,236 @@
+"""ctypes binding of ``libmpmm_cuda.so`` (C ABI: ``include/mpmm_cuda.h``).
+
+This module is the ``cuda`` kernel backend.  Its module-level ``NAME`` and
+eight range functions follow the reference's kernel-module protocol
+(``pkg/src/mpmm/backend.py:28-30``; signatures of ``_kernels.pyx:36-452``):
+numpy ``(rows, cols, comps)`` float64 C-contiguous arrays in, results
+written in place, nothing returned.  The ``*_dev`` wrappers take raw device
+pointers (``torch.Tensor.data_ptr()``) for the device-resident paths.
+
+There is no CPU fallback: if the library cannot be loaded, every entry
+point raises :class:`~paper_1710_01839_b200.errors.DeviceError`.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import DeviceError, ShapeError
+
+NAME = "cuda"
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmpmm_cuda.so")
+
+_lib = None
+_load_error = None
+
+_D = ctypes.POINTER(ctypes.c_double)
+_I64 = ctypes.c_int64
+_INT = ctypes.c_int
+_VP = ctypes.c_void_p
+
+# (name, argtypes) for every symbol declared in include/mpmm_cuda.h
+_SIGNATURES = {
+    "mpmm_abi_version": [],
+    "mpmm_last_error": [],
+    "mpmm_device_count": [ctypes.POINTER(_INT)],
+    "mpmm_tile_for_nmin": [_I64, ctypes.POINTER(_INT), ctypes.POINTER(_INT)],
+    "mpmm_gemm_geometry": [_INT, _INT, _I64] + [ctypes.POINTER(_INT)] * 5,
+    "mpmm_dd_simple_rows": [_D, _D, _D, _I64, _I64, _I64, _I64, _I64],
+    "mpmm_qd_simple_rows": [_D, _D, _D, _I64, _I64, _I64, _I64, _I64],
+    "mpmm_dd_block_cells": [_D, _D, _D, _I64, _I64, _I64, _I64, _I64, _I64],
+    "mpmm_qd_block_cells": [_D, _D, _D, _I64, _I64, _I64, _I64, _I64, _I64],
+    "mpmm_dd_ewise_add": [_D, _D, _D, _I64, _I64, _I64, _I64],
+    "mpmm_dd_ewise_sub": [_D, _D, _D, _I64, _I64, _I64, _I64],
+    "mpmm_qd_ewise_add": [_D, _D, _D, _I64, _I64, _I64, _I64],
+    "mpmm_qd_ewise_sub": [_D, _D, _D, _I64, _I64, _I64, _I64],
+    "mpmm_gemm_dev": [_INT, _INT, _I64, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64,
+                      _INT, _VP, _VP],
+    "mpmm_block_cells_dev": [_INT, _I64, _I64, _I64, _I64, _I64, _I64, _VP, _I64, _VP, _I64,
+                             _VP, _I64, _VP],
+    "mpmm_ewise_dev": [_INT, _INT, _I64, _I64, _VP, _I64, _VP, _I64, _INT, _VP, _I64, _INT,
+                       _VP, _I64, _INT, _VP, _I64, _VP],
+    "mpmm_nonfinite_dev": [_INT, _I64, _I64, _VP, _I64, _VP, _VP],
+    "mpmm_fp64_burn_dev": [_INT, _INT, _INT, _I64, _VP, _VP],
+    "mpmm_host_frobenius_norm": [_INT, _D, _I64, _D],
+    "mpmm_host_frobenius_rel_diff": [_INT, _D, _D, _I64, _D],
+}
+
+ALGO_SIMPLE = 0
+ALGO_BLOCK = 1
+
+
+def load():
+    """Load the library once; raise DeviceError when it is missing."""
+    global _lib, _load_error
+    if _lib is not None:
+        return _lib
+    if _load_error is not None:
+        raise DeviceError(_load_error)
+    if not os.path.exists(LIB_PATH):
+        _load_error = (f"CUDA extension not built: {LIB_PATH} is missing "
+                       "(run `python -c 'import __graft_entry__ as g; g.build()'`)")
+        raise DeviceError(_load_error)
+    try:
+        lib = ctypes.CDLL(LIB_PATH)
+    except OSError as ex:
+        _load_error = f"cannot load {LIB_PATH}: {ex}"
+        raise DeviceError(_load_error) from None
+    for name, argtypes in _SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = argtypes
+        fn.restype = ctypes.c_char_p if name == "mpmm_last_error" else ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def available():
+    try:
+        load()
+        return True
+    except DeviceError:
+        return False
+
+
+def exported_symbols():
+    return list(_SIGNATURES)
+
+
+def check(rc):
+    if rc != 0:
+        msg = load().mpmm_last_error().decode(errors="replace")
+        if rc == 1:
+            raise ValueError(msg)
+        raise DeviceError(msg)
+
+
+def device_count():
+    n = ctypes.c_int(0)
+    check(load().mpmm_device_count(ctypes.byref(n)))
+    return n.value
+
+
+def tile_for_nmin(n_min):
+    t, s = ctypes.c_int(0), ctypes.c_int(0)
+    check(load().mpmm_tile_for_nmin(n_min, ctypes.byref(t), ctypes.byref(s)))
+    return t.value, s.value
+
+
+def gemm_geometry(comps, algo, n_min):
+    """dict(tile_m, tile_n, threads, ctas_per_sm, sm_count) on the current device."""
+    vals = [ctypes.c_int(0) for _ in range(5)]
+    check(load().mpmm_gemm_geometry(comps, algo, n_min, *[ctypes.byref(v) for v in vals]))
+    keys = ("tile_m", "tile_n", "threads", "ctas_per_sm", "sm_count")
+    return dict(zip(keys, (v.value for v in vals)))
+
+
+# ---------------------------------------------------------------------------
+# reference kernel-module protocol (host numpy arrays)
+# ---------------------------------------------------------------------------
+
+def _arr(x, comps):
+    if not isinstance(x, np.ndarray) or x.dtype != np.float64 or x.ndim != 3 \
+            or not x.flags.c_contiguous:
+        raise TypeError("expected a C-contiguous float64 (rows, cols, comps) array")
+    if x.shape[2] != comps:
+        raise ShapeError(f"expected {comps} components, got {x.shape[2]}")
+    return x.ctypes.data_as(_D)
+
+
+def _simple(comps, fn, a, b, c, i0, i1):
+    m, l = a.shape[0], a.shape[1]
+    n = b.shape[1]
+    check(fn(_arr(a, comps), _arr(b, comps), _arr(c, comps), m, l, n, i0, i1))
+
+
+def _cells(comps, fn, a, b, c, n_min, cell0, cell1):
+    m, l = a.shape[0], a.shape[1]
+    n = b.shape[1]
+    check(fn(_arr(a, comps), _arr(b, comps), _arr(c, comps), m, l, n, n_min, cell0, cell1))
+
+
+def _ew(comps, fn, x, y, out, i0, i1):
+    check(fn(_arr(x, comps), _arr(y, comps), _arr(out, comps), x.shape[0], x.shape[1], i0, i1))
+
+
+def dd_simple_rows(a, b, c, i0, i1):
+    """_kernels.pyx:36-100 on the GPU."""
+    _simple(2, load().mpmm_dd_simple_rows, a, b, c, i0, i1)
+
+
+def qd_simple_rows(a, b, c, i0, i1):
+    """_kernels.pyx:344-363 on the GPU."""
+    _simple(4, load().mpmm_qd_simple_rows, a, b, c, i0, i1)
+
+
+def dd_block_cells(a, b, c, n_min, cell0, cell1):
+    """_kernels.pyx:103-186 on the GPU (accumulates into c)."""
+    _cells(2, load().mpmm_dd_block_cells, a, b, c, n_min, cell0, cell1)
+
+
+def qd_block_cells(a, b, c, n_min, cell0, cell1):
+    """_kernels.pyx:366-404 on the GPU (accumulates into c)."""
+    _cells(4, load().mpmm_qd_block_cells, a, b, c, n_min, cell0, cell1)
+
+
+def dd_ewise_add(x, y, out, i0, i1):
+    _ew(2, load().mpmm_dd_ewise_add, x, y, out, i0, i1)
+
+
+def dd_ewise_sub(x, y, out, i0, i1):
+    _ew(2, load().mpmm_dd_ewise_sub, x, y, out, i0, i1)
+
+
+def qd_ewise_add(x, y, out, i0, i1):
+    _ew(4, load().mpmm_qd_ewise_add, x, y, out, i0, i1)
+
+
+def qd_ewise_sub(x, y, out, i0, i1):
+    _ew(4, load().mpmm_qd_ewise_sub, x, y, out, i0, i1)
+
+
+# ---------------------------------------------------------------------------
+# device-resident entry points (raw pointers, element leading dimensions)
+# ---------------------------------------------------------------------------
+
+def gemm_dev(comps, algo, n_min, m, l, n, A, lda, B, ldb, C, ldc, accumulate,
+             nonfinite=None, stream=None):
+    check(load().mpmm_gemm_dev(comps, algo, n_min, m, l, n, A, lda, B, ldb, C, ldc,
+                               1 if accumulate else 0, nonfinite, stream))
+
+
+def block_cells_dev(comps, n_min, cell0, cell1, m, l, n, A, lda, B, ldb, C, ldc, stream=None):
+    check(load().mpmm_block_cells_dev(comps, n_min, cell0, cell1, m, l, n, A, lda, B, ldb,
+                                      C, ldc, stream))
+
+
+def ewise_dev(comps, rows, cols, O, ldo, X, ldx, Y, ldy, sy, Z=None, ldz=0, sz=1, W=None,
+              ldw=0, sw=1, stream=None):
+    nops = 1 + (Z is not None) + (W is not None)
+    check(load().mpmm_ewise_dev(comps, nops, rows, cols, X, ldx, Y, ldy, sy, Z, ldz, sz,
+                                W, ldw, sw, O, ldo, stream))
+
+
+def nonfinite_dev(comps, rows, cols, X, ldx, flag, stream=None):
+    check(load().mpmm_nonfinite_dev(comps, rows, cols, X, ldx, flag, stream))
+
+
+def fp64_burn_dev(op, blocks, threads, iters, scratch, stream=None):
+    check(load().mpmm_fp64_burn_dev(op, blocks, threads, iters, scratch, stream))
+
+
+def host_frobenius_norm(comps, x):
+    out = ctypes.c_double(0.0)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    return load().mpmm_host_frobenius_norm(comps, x.ctypes.data_as(_D), x.size // comps,
+                                           ctypes.byref(out)), out.value
+
+
+def host_frobenius_rel_diff(comps, x, y):
+    out = ctypes.c_double(0.0)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    return load().mpmm_host_frobenius_rel_diff(comps, x.ctypes.data_as(_D), y.ctypes.data_as(_D),
+                                               x.size // comps, ctypes.byref(out)), out.value

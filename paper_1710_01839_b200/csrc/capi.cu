@@ -1,0 +1,301 @@
+// capi.cu -- the extern "C" boundary of libmpmm_cuda.so (include/mpmm_cuda.h).
+//
+// Replaces the reference's compiled kernel module (pkg/src/mpmm/_kernels.pyx,
+// selected by backend.py:28-56): the eight range kernels keep their
+// argument meaning on host pointers, and device-resident whole-GEMM /
+// elementwise entry points serve the multiply/predict/tune layers.
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/mpmm_cuda.h"
+#include "kernels.h"
+
+using namespace mpmm;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(MPMM_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CU(call)                                  \
+  do {                                            \
+    cudaError_t _e = (call);                      \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+  } while (0)
+
+bool dims_ok(int64_t m, int64_t l, int64_t n) {
+  const int64_t lim = (int64_t)1 << 30;
+  return m >= 0 && l >= 0 && n >= 0 && m < lim && l < lim && n < lim;
+}
+
+void tile_for(int64_t n_min, int* tile, int* super) {
+  // n_min is the reference's cache block size (multiply.py:148-160).  On the
+  // GPU it selects the CTA tile; n_min beyond one CTA tile becomes an L2
+  // super-tile of (n_min/64)^2 CTAs walked together.
+  *super = 1;
+  if (n_min <= 16) {
+    *tile = TILE_16;
+  } else if (n_min <= 32) {
+    *tile = TILE_32;
+  } else if (n_min <= 64) {
+    *tile = TILE_64;
+  } else {
+    *tile = TILE_64;
+    *super = (int)((n_min + 63) / 64);
+  }
+}
+
+cudaError_t gemm(int comps, const GemmArgs& g) {
+  return comps == 2 ? dd_gemm_launch(g) : qd_gemm_launch(g);
+}
+
+// Device buffers for the host-pointer protocol; freed on scope exit.
+struct DevBuf {
+  double* p = nullptr;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t alloc(size_t doubles) {
+    return cudaMalloc(&p, doubles ? doubles * sizeof(double) : sizeof(double));
+  }
+};
+
+int block_cells_impl(int comps, int64_t n_min, int64_t cell0, int64_t cell1, int64_t m,
+                     int64_t l, int64_t n, const double* A, int64_t lda, const double* B,
+                     int64_t ldb, double* C, int64_t ldc, cudaStream_t stream) {
+  if (n_min < 1) return fail(MPMM_ERR_ARG, "block size must be positive");
+  if (m == 0 || n == 0 || cell1 <= cell0) return MPMM_OK;
+  const int64_t nbc = (n + n_min - 1) / n_min;
+  const int64_t nbr = (m + n_min - 1) / n_min;
+  if (cell0 < 0 || cell1 > nbc * nbr) return fail(MPMM_ERR_ARG, "cell range out of bounds");
+  int tile, super;
+  tile_for(n_min, &tile, &super);
+  // The flattened cell range [cell0, cell1) is at most three rectangles:
+  // the tail of the first block row, whole block rows, the head of the last.
+  auto rect = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) -> int {
+    r1 = r1 < m ? r1 : m;
+    c1 = c1 < n ? c1 : n;
+    if (r1 <= r0 || c1 <= c0) return MPMM_OK;
+    GemmArgs g{ALGO_BLOCK, tile, super, (int)(r1 - r0), (int)(c1 - c0), (int)l,
+               A + comps * (r0 * lda), lda, B + comps * c0, ldb,
+               C + comps * (r0 * ldc + c0), ldc, 1, nullptr, stream};
+    cudaError_t e = gemm(comps, g);
+    return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "block_cells launch");
+  };
+  const int64_t ib0 = cell0 / nbc, jb0 = cell0 % nbc;
+  const int64_t ib1 = (cell1 - 1) / nbc, jb1 = (cell1 - 1) % nbc;
+  int rc;
+  if (ib0 == ib1) return rect(ib0 * n_min, (ib0 + 1) * n_min, jb0 * n_min, (jb1 + 1) * n_min);
+  if ((rc = rect(ib0 * n_min, (ib0 + 1) * n_min, jb0 * n_min, n)) != MPMM_OK) return rc;
+  if (ib1 > ib0 + 1 && (rc = rect((ib0 + 1) * n_min, ib1 * n_min, 0, n)) != MPMM_OK) return rc;
+  return rect(ib1 * n_min, (ib1 + 1) * n_min, 0, (jb1 + 1) * n_min);
+}
+
+int host_simple_rows(int comps, const double* a, const double* b, double* c, int64_t m,
+                     int64_t l, int64_t n, int64_t i0, int64_t i1) {
+  if (!dims_ok(m, l, n) || i0 < 0 || i1 > m) return fail(MPMM_ERR_ARG, "bad shape or row range");
+  if (i1 <= i0 || n == 0) return MPMM_OK;
+  const int64_t rows = i1 - i0;
+  DevBuf dA, dB, dC;
+  CU(dA.alloc(rows * l * comps));
+  CU(dB.alloc(l * n * comps));
+  CU(dC.alloc(rows * n * comps));
+  CU(cudaMemcpy(dA.p, a + i0 * l * comps, rows * l * comps * sizeof(double),
+                cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(dB.p, b, l * n * comps * sizeof(double), cudaMemcpyHostToDevice));
+  GemmArgs g{ALGO_SIMPLE, TILE_16, 1, (int)rows, (int)n, (int)l, dA.p, l, dB.p, n, dC.p, n,
+             0, nullptr, 0};
+  CU(gemm(comps, g));
+  CU(cudaMemcpy(c + i0 * n * comps, dC.p, rows * n * comps * sizeof(double),
+                cudaMemcpyDeviceToHost));
+  return MPMM_OK;
+}
+
+int host_block_cells(int comps, const double* a, const double* b, double* c, int64_t m,
+                     int64_t l, int64_t n, int64_t n_min, int64_t cell0, int64_t cell1) {
+  if (!dims_ok(m, l, n)) return fail(MPMM_ERR_ARG, "bad shape");
+  if (n_min < 1) return fail(MPMM_ERR_ARG, "block size must be positive");
+  if (m == 0 || n == 0 || cell1 <= cell0) return MPMM_OK;
+  const int64_t nbc = (n + n_min - 1) / n_min;
+  if (cell0 < 0 || cell1 > nbc * ((m + n_min - 1) / n_min))
+    return fail(MPMM_ERR_ARG, "cell range out of bounds");
+  const int64_t ib0 = cell0 / nbc, ib1 = (cell1 - 1) / nbc;
+  const int64_t r0 = ib0 * n_min;
+  const int64_t r1 = (ib1 + 1) * n_min < m ? (ib1 + 1) * n_min : m;
+  const int64_t rows = r1 - r0;
+  DevBuf dA, dB, dC;
+  CU(dA.alloc(rows * l * comps));
+  CU(dB.alloc(l * n * comps));
+  CU(dC.alloc(rows * n * comps));
+  CU(cudaMemcpy(dA.p, a + r0 * l * comps, rows * l * comps * sizeof(double),
+                cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(dB.p, b, l * n * comps * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(dC.p, c + r0 * n * comps, rows * n * comps * sizeof(double),
+                cudaMemcpyHostToDevice));
+  int rc = block_cells_impl(comps, n_min, cell0 - ib0 * nbc, cell1 - ib0 * nbc, rows, l, n, dA.p,
+                            l, dB.p, n, dC.p, n, 0);
+  if (rc != MPMM_OK) return rc;
+  CU(cudaMemcpy(c + r0 * n * comps, dC.p, rows * n * comps * sizeof(double),
+                cudaMemcpyDeviceToHost));
+  return MPMM_OK;
+}
+
+int host_ewise(int comps, int sign, const double* x, const double* y, double* out,
+               int64_t rows, int64_t cols, int64_t i0, int64_t i1) {
+  if (rows < 0 || cols < 0 || i0 < 0 || i1 > rows) return fail(MPMM_ERR_ARG, "bad row range");
+  if (i1 <= i0 || cols == 0) return MPMM_OK;
+  const int64_t r = i1 - i0, sz = r * cols * comps;
+  DevBuf dX, dY;
+  CU(dX.alloc(sz));
+  CU(dY.alloc(sz));
+  CU(cudaMemcpy(dX.p, x + i0 * cols * comps, sz * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(dY.p, y + i0 * cols * comps, sz * sizeof(double), cudaMemcpyHostToDevice));
+  EwiseArgs e{comps, 1, (int)r, (int)cols, dX.p, cols, dY.p, cols, sign, nullptr, 0, 1,
+              nullptr, 0, 1, dX.p, cols, 0};
+  CU(ewise_launch(e));
+  CU(cudaMemcpy(out + i0 * cols * comps, dX.p, sz * sizeof(double), cudaMemcpyDeviceToHost));
+  return MPMM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mpmm_abi_version(void) { return MPMM_ABI_VERSION; }
+
+const char* mpmm_last_error(void) { return g_err.c_str(); }
+
+int mpmm_device_count(int* count) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) {
+    cudaGetLastError();
+    c = 0;
+  }
+  *count = c;
+  return MPMM_OK;
+}
+
+int mpmm_tile_for_nmin(int64_t n_min, int* tile, int* super_tiles) {
+  if (n_min < 1) return fail(MPMM_ERR_ARG, "block size must be positive");
+  tile_for(n_min, tile, super_tiles);
+  return MPMM_OK;
+}
+
+int mpmm_gemm_geometry(int comps, int algo, int64_t n_min, int* tile_m, int* tile_n,
+                       int* threads, int* ctas_per_sm, int* sm_count) {
+  if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
+  int tile = TILE_16, super = 1;
+  if (algo == MPMM_ALGO_BLOCK) {
+    if (n_min < 1) return fail(MPMM_ERR_ARG, "block size must be positive");
+    tile_for(n_min, &tile, &super);
+  }
+  Geometry geo{0, 0, 0, 0};
+  cudaError_t e = comps == 2 ? dd_gemm_geometry(algo, tile, &geo) : qd_gemm_geometry(algo, tile, &geo);
+  if (e != cudaSuccess) return cuda_fail(e, "occupancy query");
+  int dev = 0, sms = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  *tile_m = geo.bm;
+  *tile_n = geo.bn;
+  *threads = geo.threads;
+  *ctas_per_sm = geo.ctas_per_sm;
+  *sm_count = sms;
+  return MPMM_OK;
+}
+
+int mpmm_dd_simple_rows(const double* a, const double* b, double* c, int64_t m, int64_t l,
+                        int64_t n, int64_t i0, int64_t i1) {
+  return host_simple_rows(2, a, b, c, m, l, n, i0, i1);
+}
+int mpmm_qd_simple_rows(const double* a, const double* b, double* c, int64_t m, int64_t l,
+                        int64_t n, int64_t i0, int64_t i1) {
+  return host_simple_rows(4, a, b, c, m, l, n, i0, i1);
+}
+int mpmm_dd_block_cells(const double* a, const double* b, double* c, int64_t m, int64_t l,
+                        int64_t n, int64_t n_min, int64_t cell0, int64_t cell1) {
+  return host_block_cells(2, a, b, c, m, l, n, n_min, cell0, cell1);
+}
+int mpmm_qd_block_cells(const double* a, const double* b, double* c, int64_t m, int64_t l,
+                        int64_t n, int64_t n_min, int64_t cell0, int64_t cell1) {
+  return host_block_cells(4, a, b, c, m, l, n, n_min, cell0, cell1);
+}
+int mpmm_dd_ewise_add(const double* x, const double* y, double* out, int64_t rows, int64_t cols,
+                      int64_t i0, int64_t i1) {
+  return host_ewise(2, 1, x, y, out, rows, cols, i0, i1);
+}
+int mpmm_dd_ewise_sub(const double* x, const double* y, double* out, int64_t rows, int64_t cols,
+                      int64_t i0, int64_t i1) {
+  return host_ewise(2, -1, x, y, out, rows, cols, i0, i1);
+}
+int mpmm_qd_ewise_add(const double* x, const double* y, double* out, int64_t rows, int64_t cols,
+                      int64_t i0, int64_t i1) {
+  return host_ewise(4, 1, x, y, out, rows, cols, i0, i1);
+}
+int mpmm_qd_ewise_sub(const double* x, const double* y, double* out, int64_t rows, int64_t cols,
+                      int64_t i0, int64_t i1) {
+  return host_ewise(4, -1, x, y, out, rows, cols, i0, i1);
+}
+
+int mpmm_gemm_dev(int comps, int algo, int64_t n_min, int64_t m, int64_t l, int64_t n,
+                  const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                  int64_t ldc, int accumulate, int* nonfinite, void* stream) {
+  if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
+  if (!dims_ok(m, l, n)) return fail(MPMM_ERR_ARG, "bad shape");
+  if (lda < l || ldb < n || ldc < n) return fail(MPMM_ERR_ARG, "leading dimension too small");
+  if (algo != MPMM_ALGO_SIMPLE && algo != MPMM_ALGO_BLOCK) return fail(MPMM_ERR_ARG, "bad algo");
+  if (algo == MPMM_ALGO_BLOCK && n_min < 1) return fail(MPMM_ERR_ARG, "block size must be positive");
+  int tile = TILE_16, super = 1;
+  if (algo == MPMM_ALGO_BLOCK) tile_for(n_min, &tile, &super);
+  GemmArgs g{algo, tile, super, (int)m, (int)n, (int)l, A, lda, B, ldb, C, ldc,
+             accumulate ? 1 : 0, nonfinite, (cudaStream_t)stream};
+  cudaError_t e = gemm(comps, g);
+  return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "gemm launch");
+}
+
+int mpmm_block_cells_dev(int comps, int64_t n_min, int64_t cell0, int64_t cell1, int64_t m,
+                         int64_t l, int64_t n, const double* A, int64_t lda, const double* B,
+                         int64_t ldb, double* C, int64_t ldc, void* stream) {
+  if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
+  if (!dims_ok(m, l, n)) return fail(MPMM_ERR_ARG, "bad shape");
+  return block_cells_impl(comps, n_min, cell0, cell1, m, l, n, A, lda, B, ldb, C, ldc,
+                          (cudaStream_t)stream);
+}
+
+int mpmm_ewise_dev(int comps, int nops, int64_t rows, int64_t cols, const double* X,
+                   int64_t ldx, const double* Y, int64_t ldy, int sy, const double* Z,
+                   int64_t ldz, int sz, const double* W, int64_t ldw, int sw, double* O,
+                   int64_t ldo, void* stream) {
+  if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
+  if (nops < 1 || nops > 3) return fail(MPMM_ERR_ARG, "nops must be 1..3");
+  if (!dims_ok(rows, 0, cols)) return fail(MPMM_ERR_ARG, "bad shape");
+  EwiseArgs e{comps, nops, (int)rows, (int)cols, X, ldx, Y, ldy, sy < 0 ? -1 : 1,
+              Z, ldz, sz < 0 ? -1 : 1, W, ldw, sw < 0 ? -1 : 1, O, ldo, (cudaStream_t)stream};
+  cudaError_t err = ewise_launch(e);
+  return err == cudaSuccess ? MPMM_OK : cuda_fail(err, "ewise launch");
+}
+
+int mpmm_nonfinite_dev(int comps, int64_t rows, int64_t cols, const double* X, int64_t ldx,
+                       int* flag, void* stream) {
+  if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
+  cudaError_t err = nonfinite_launch(comps, X, ldx, (int)rows, (int)cols, flag,
+                                     (cudaStream_t)stream);
+  return err == cudaSuccess ? MPMM_OK : cuda_fail(err, "nonfinite launch");
+}
+
+int mpmm_fp64_burn_dev(int op, int blocks, int threads, int64_t iters, double* scratch,
+                       void* stream) {
+  if (op != 0 && op != 1) return fail(MPMM_ERR_ARG, "op must be 0 (DFMA) or 1 (DADD)");
+  cudaError_t err = fp64_burn_launch(op, blocks, threads, iters, scratch, (cudaStream_t)stream);
+  return err == cudaSuccess ? MPMM_OK : cuda_fail(err, "fp64 burn launch");
+}
+
+}  // extern "C"

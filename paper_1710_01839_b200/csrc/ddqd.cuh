@@ -1,0 +1,251 @@
+// ddqd.cuh -- double-double / quad-double device arithmetic for sm_100a.
+//
+// Every routine here reproduces, rounding for rounding, the operation
+// sequence of the reference kernels (/root/reference/pkg/src/mpmm/
+// _kernels.pyx), so the GPU results are bit-identical to the reference CPU
+// results.  Two rules make that hold:
+//
+//  * this translation unit is compiled with -fmad=false, so nvcc never
+//    contracts an a*b+c into a DFMA on its own: every multiply and add
+//    rounds separately, as the reference's -ffp-contract=off build does;
+//  * TwoProd uses ONE explicit DFMA for the error term (err = fma(a,b,-p))
+//    instead of the reference's Veltkamp/Dekker split (_kernels.pyx:19-29).
+//    Both yield the unique exact error a*b - p whenever the Dekker split is
+//    exact (|a|,|b| < 2^996, no underflow of the error -- the reference's
+//    own eft.py:21-24 range), so the two are bit-identical there.  This
+//    removes 20 of the 87 FP64 operations of a DD multiply-add.
+#pragma once
+
+#include <cstdint>
+
+namespace mpmm {
+
+// eft.py:27-30 _two_sum_raw
+__device__ __forceinline__ double two_sum(double a, double b, double& err) {
+  double s = a + b;
+  double bb = s - a;
+  err = (a - (s - bb)) + (b - bb);
+  return s;
+}
+
+// eft.py:33-36 _quick_two_sum_raw
+__device__ __forceinline__ double quick_two_sum(double a, double b, double& err) {
+  double s = a + b;
+  err = b - (s - a);
+  return s;
+}
+
+// eft.py:45-49 _two_prod_raw, error term by DFMA (exact; see header).
+__device__ __forceinline__ double two_prod(double a, double b, double& err) {
+  double p = a * b;
+  err = __fma_rn(a, b, -p);
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// double-double
+// ---------------------------------------------------------------------------
+
+// ddqd.py:63-70 dd_add == _kernels.pyx:189-204 (20 DADD)
+__device__ __forceinline__ void dd_add(double xh, double xl, double yh, double yl,
+                                       double& hi, double& lo) {
+  double s2, t2, e;
+  double s1 = two_sum(xh, yh, s2);
+  double t1 = two_sum(xl, yl, t2);
+  s2 = s2 + t1;
+  s1 = quick_two_sum(s1, s2, e);
+  s2 = e + t2;
+  hi = quick_two_sum(s1, s2, lo);
+}
+
+// ddqd.py:77-91 dd_mul, as inlined at _kernels.pyx:140-171
+// (4 DMUL + 3 DFMA + 23 DADD).
+__device__ __forceinline__ void dd_mul(double ah, double al, double bh, double bl,
+                                       double& ph, double& pl) {
+  double e, e1, e2, r1, r2, w;
+  double p = two_prod(ah, bh, e);
+  double p1 = two_prod(ah, bl, e1);
+  double p2 = two_prod(al, bh, e2);
+  double tail = (e1 + e2) + al * bl;
+  double s = two_sum(p1, p2, r1);
+  s = two_sum(e, s, r2);
+  double losum = (r1 + r2) + tail;
+  double h = quick_two_sum(p, s, w);
+  w = w + losum;
+  ph = quick_two_sum(h, w, pl);
+}
+
+// One DD multiply-add, the k-loop body of _kernels.pyx:135-184:
+// c <- dd_add(c, dd_mul(a, b)).  50 FP64 instructions, 53 flops.
+__device__ __forceinline__ void dd_madd(double& ch, double& cl, double ah, double al,
+                                        double bh, double bl) {
+  double ph, pl;
+  dd_mul(ah, al, bh, bl, ph, pl);
+  dd_add(ch, cl, ph, pl, ch, cl);
+}
+
+// ---------------------------------------------------------------------------
+// quad-double
+// ---------------------------------------------------------------------------
+
+// ddqd.py:140-172 _renorm5 == _kernels.pyx:237-271, branch-free: the
+// data-dependent "if e != 0" emission becomes predicated selects.  In the
+// reference's k == 3 case "acc += v" equals the s computed below, so the
+// only behavioural difference of the k == 3 case is that nothing is emitted.
+__device__ __forceinline__ void renorm5(double x0, double x1, double x2, double x3,
+                                        double x4, double out[4]) {
+  double s, t;
+  s = quick_two_sum(x3, x4, x4);
+  t = quick_two_sum(x2, s, x3);
+  s = quick_two_sum(x1, t, x2);
+  t = quick_two_sum(x0, s, x1);
+  double o0 = 0.0, o1 = 0.0, o2 = 0.0, o3 = 0.0;
+  double acc = t;
+  int k = 0;
+  const double rest[4] = {x1, x2, x3, x4};
+#pragma unroll
+  for (int idx = 0; idx < 4; ++idx) {
+    double v = rest[idx];
+    double sn = acc + v;
+    double e = v - (sn - acc);
+    bool emit = (k < 3) && (e != 0.0);
+    if (emit) {
+      o0 = (k == 0) ? sn : o0;
+      o1 = (k == 1) ? sn : o1;
+      o2 = (k == 2) ? sn : o2;
+    }
+    acc = emit ? e : sn;
+    k += emit ? 1 : 0;
+  }
+  o0 = (k == 0) ? acc : o0;
+  o1 = (k == 1) ? acc : o1;
+  o2 = (k == 2) ? acc : o2;
+  o3 = (k == 3) ? acc : o3;
+  out[0] = o0;
+  out[1] = o1;
+  out[2] = o2;
+  out[3] = o3;
+}
+
+// ddqd.py:175-193 _compress4 for N terms that are ALL nonzero (the zero
+// filter is then the identity).  Fully unrolled: registers only.
+template <int N>
+__device__ __forceinline__ void compress4_dense(double (&v)[N], double out[4]) {
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    double s = v[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) s = two_sum(s, v[i], v[i - 1]);
+    v[N - 1] = s;
+  }
+  if constexpr (N <= 4) {
+    double w[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < N; ++i) w[4 - N + i] = v[i];
+    renorm5(w[3], w[2], w[1], w[0], 0.0, out);
+  } else {
+    double tail = 0.0;
+#pragma unroll
+    for (int i = 0; i < N - 4; ++i) tail += v[i];
+    renorm5(v[N - 1], v[N - 2], v[N - 3], v[N - 4], tail, out);
+  }
+}
+
+// ddqd.py:175-193 _compress4, general case (some terms zero): compaction
+// with a runtime count.  Rare on full-entropy data; kept out of line so the
+// dense path stays in registers.
+static __device__ __noinline__ void compress4_general(const double* terms, int nterms,
+                                                     double* out) {
+  double buf[24];
+  int n = 0;
+  for (int i = 0; i < nterms; ++i)
+    if (terms[i] != 0.0) buf[n++] = terms[i];
+  if (n == 0) {
+    out[0] = out[1] = out[2] = out[3] = 0.0;
+    return;
+  }
+  for (int p = 0; p < 4; ++p) {
+    double s = buf[0];
+    for (int i = 1; i < n; ++i) s = two_sum(s, buf[i], buf[i - 1]);
+    buf[n - 1] = s;
+  }
+  if (n <= 4) {
+    double w[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int i = 0; i < n; ++i) w[4 - n + i] = buf[i];
+    renorm5(w[3], w[2], w[1], w[0], 0.0, out);
+    return;
+  }
+  double tail = 0.0;
+  for (int i = 0; i < n - 4; ++i) tail += buf[i];
+  renorm5(buf[n - 1], buf[n - 2], buf[n - 3], buf[n - 4], tail, out);
+}
+
+// Copy into a private array before the out-of-line call so the caller's
+// term array never has its address taken (it then stays in registers).
+template <int N>
+__device__ __forceinline__ void compress4_slow(const double (&v)[N], double out[4]) {
+  double tmp[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) tmp[i] = v[i];
+  double o[4];
+  compress4_general(tmp, N, o);
+  out[0] = o[0];
+  out[1] = o[1];
+  out[2] = o[2];
+  out[3] = o[3];
+}
+
+// _kernels.pyx:311-341 _qd_mul_add: cc += x*y, bit-identical.
+__device__ __forceinline__ void qd_mul_add(double cc[4], const double x[4], const double y[4]) {
+  double t[23];
+  t[0] = two_prod(x[0], y[0], t[1]);
+  t[2] = two_prod(x[0], y[1], t[3]);
+  t[4] = two_prod(x[1], y[0], t[5]);
+  t[6] = two_prod(x[0], y[2], t[7]);
+  t[8] = two_prod(x[1], y[1], t[9]);
+  t[10] = two_prod(x[2], y[0], t[11]);
+  t[12] = two_prod(x[0], y[3], t[13]);
+  t[14] = two_prod(x[1], y[2], t[15]);
+  t[16] = two_prod(x[2], y[1], t[17]);
+  t[18] = two_prod(x[3], y[0], t[19]);
+  t[20] = x[1] * y[3];
+  t[21] = x[2] * y[2];
+  t[22] = x[3] * y[1];
+  bool dense = true;
+#pragma unroll
+  for (int i = 0; i < 23; ++i) dense &= (t[i] != 0.0);
+  double prod[4];
+  if (dense) {
+    compress4_dense<23>(t, prod);
+  } else {
+    compress4_slow<23>(t, prod);
+  }
+  double add[8] = {cc[0], prod[0], cc[1], prod[1], cc[2], prod[2], cc[3], prod[3]};
+  bool cz = (cc[0] == 0.0) & (cc[1] == 0.0) & (cc[2] == 0.0) & (cc[3] == 0.0);
+  bool pd = (prod[0] != 0.0) & (prod[1] != 0.0) & (prod[2] != 0.0) & (prod[3] != 0.0);
+  bool cd = (cc[0] != 0.0) & (cc[1] != 0.0) & (cc[2] != 0.0) & (cc[3] != 0.0);
+  if (cd & pd) {
+    compress4_dense<8>(add, cc);
+  } else if (cz & pd) {
+    // filtered term list is exactly prod[0..3] (k = 0 of every product)
+    double p4[4] = {prod[0], prod[1], prod[2], prod[3]};
+    compress4_dense<4>(p4, cc);
+  } else {
+    compress4_slow<8>(add, cc);
+  }
+}
+
+// qd_ewise_add / qd_ewise_sub body (_kernels.pyx:407-452)
+__device__ __forceinline__ void qd_add(const double x[4], const double y[4], double out[4]) {
+  double add[8] = {x[0], y[0], x[1], y[1], x[2], y[2], x[3], y[3]};
+  bool dense = true;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) dense &= (add[i] != 0.0);
+  if (dense) {
+    compress4_dense<8>(add, out);
+  } else {
+    compress4_slow<8>(add, out);
+  }
+}
+
+}  // namespace mpmm

@@ -1,0 +1,64 @@
+// kernels.h -- internal launcher interface shared by the .cu files and the
+// C-ABI layer (capi.cu).  Not part of the public ABI (that is
+// include/mpmm_cuda.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace mpmm {
+
+enum Algo { ALGO_SIMPLE = 0, ALGO_BLOCK = 1 };
+
+// CTA tile configurations of the blocked kernels.  The reference's block
+// size n_min selects one (tile_for_nmin); results never depend on it.
+enum Tile { TILE_16 = 0, TILE_32 = 1, TILE_64 = 2, TILE_32x64 = 3, TILE_COUNT = 4 };
+
+struct GemmArgs {
+  int algo;          // ALGO_SIMPLE or ALGO_BLOCK
+  int tile;          // Tile (ALGO_BLOCK)
+  int super;         // L2 super-tile edge in CTA tiles (1 = row-major raster)
+  int m, n, l;
+  const double* A;   // element (i,k) at A + comps*(i*lda + k)
+  int64_t lda;
+  const double* B;
+  int64_t ldb;
+  double* C;
+  int64_t ldc;
+  int accumulate;    // 0: acc starts at 0 and C is overwritten; 1: C += A*B
+  int* nonfinite;    // device flag, OR-ed with 1 if any output is non-finite (may be null)
+  cudaStream_t stream;
+};
+
+cudaError_t dd_gemm_launch(const GemmArgs& g);
+cudaError_t qd_gemm_launch(const GemmArgs& g);
+
+// CTA tile and residency of the kernel a launch would use.
+struct Geometry {
+  int bm, bn, threads, ctas_per_sm;
+};
+cudaError_t dd_gemm_geometry(int algo, int tile, Geometry* geo);
+cudaError_t qd_gemm_geometry(int algo, int tile, Geometry* geo);
+
+// out = ((x s1 y) s2 z) s3 w for nops = 1, 2, 3 (signs +1/-1), elementwise,
+// each step one reference ewise add/sub (_kernels.pyx:207-230, :407-452).
+struct EwiseArgs {
+  int comps;
+  int nops;
+  int rows, cols;
+  const double* X; int64_t ldx;
+  const double* Y; int64_t ldy; int sy;
+  const double* Z; int64_t ldz; int sz;
+  const double* W; int64_t ldw; int sw;
+  double* O; int64_t ldo;
+  cudaStream_t stream;
+};
+cudaError_t ewise_launch(const EwiseArgs& e);
+
+cudaError_t nonfinite_launch(int comps, const double* X, int64_t ldx, int rows, int cols,
+                             int* flag, cudaStream_t stream);
+
+cudaError_t fp64_burn_launch(int op, int blocks, int threads, int64_t iters, double* out,
+                             cudaStream_t stream);
+
+}  // namespace mpmm

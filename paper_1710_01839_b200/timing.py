@@ -1,0 +1,120 @@
+"""Measurement policy (reference ``timing.py:1-59``) for device work.
+
+``TimingPolicy`` and ``measure`` keep the reference's contract: warm-up
+runs, ``measured_runs`` samples aggregated by median/min/mean, an injectable
+clock, ``setup`` outside the timed region, and ``MeasurementError`` on a
+non-positive elapsed time.
+
+The difference is the default clock.  Device work is asynchronous, so the
+default ``device_clock`` synchronises the current CUDA device before
+reading the host's monotonic clock; ``measure`` then brackets exactly the
+device work ``fn`` enqueued.  ``EventTimer`` gives the CUDA-event timings
+(on the launching stream) used by the predictor and by ``bench.py``.
+"""
+
+import statistics
+import time
+from dataclasses import dataclass, field
+
+from .errors import MeasurementError
+
+_AGGREGATORS = {
+    "median": statistics.median,
+    "min": min,
+    "mean": statistics.fmean,
+}
+
+
+def device_clock():
+    """Monotonic seconds after all queued work on the current device."""
+    try:
+        import torch
+        if torch.cuda.is_available() and torch.cuda.is_initialized():
+            torch.cuda.synchronize()
+    except ImportError:  # pragma: no cover - torch is part of the image
+        pass
+    return time.perf_counter()
+
+
+@dataclass
+class TimingPolicy:
+    warmup_runs: int = 0
+    measured_runs: int = 1
+    aggregator: str = "median"
+    clock: object = field(default=device_clock, repr=False)
+
+    def __post_init__(self):
+        if self.measured_runs < 1:
+            raise ValueError("measured_runs must be >= 1")
+        if self.warmup_runs < 0:
+            raise ValueError("warmup_runs must be >= 0")
+        if self.aggregator not in _AGGREGATORS:
+            raise ValueError(f"unknown aggregator {self.aggregator!r}")
+
+
+def measure(fn, policy, setup=None):
+    """Elapsed seconds for ``fn()`` under ``policy`` (reference
+    timing.py:38-59); ``setup`` runs before every sample, untimed."""
+    clock = policy.clock
+    for _ in range(policy.warmup_runs):
+        if setup is not None:
+            setup()
+        fn()
+    samples = []
+    for _ in range(policy.measured_runs):
+        if setup is not None:
+            setup()
+        t0 = clock()
+        fn()
+        elapsed = clock() - t0
+        if elapsed <= 0.0:
+            raise MeasurementError(f"non-positive elapsed time {elapsed!r}")
+        samples.append(elapsed)
+    return _AGGREGATORS[policy.aggregator](samples)
+
+
+class EventTimer:
+    """CUDA-event timing on a given stream (default: the current stream).
+
+    ``with EventTimer() as t: enqueue(...)`` then ``t.seconds`` (syncs).
+    """
+
+    def __init__(self, stream=None):
+        import torch
+        self._torch = torch
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        self.start = torch.cuda.Event(enable_timing=True)
+        self.end = torch.cuda.Event(enable_timing=True)
+
+    def __enter__(self):
+        self.start.record(self.stream)
+        return self
+
+    def __exit__(self, *exc):
+        self.end.record(self.stream)
+        return False
+
+    @property
+    def seconds(self):
+        self.end.synchronize()
+        return self.start.elapsed_time(self.end) / 1e3
+
+
+def measure_events(fn, policy, setup=None, stream=None):
+    """Like :func:`measure` but each sample is a CUDA-event interval on
+    ``stream`` around the device work ``fn`` enqueues."""
+    for _ in range(policy.warmup_runs):
+        if setup is not None:
+            setup()
+        fn()
+    samples = []
+    for _ in range(policy.measured_runs):
+        if setup is not None:
+            setup()
+        with EventTimer(stream) as t:
+            fn()
+        elapsed = t.seconds
+        if elapsed <= 0.0:
+            raise MeasurementError(f"non-positive elapsed time {elapsed!r}")
+        samples.append(elapsed)
+    return _AGGREGATORS[policy.aggregator](samples)

@@ -60,7 +60,7 @@ def load_reference():
 def main():
     mpmm = load_reference()
     from mpmm import ddqd
-    from mpmm.matrix import DenseMatrix, generate_test_pair
+    from mpmm.matrix import DenseMatrix, frobenius_norm, frobenius_rel_diff, generate_test_pair
     from mpmm.multiply import _ewise, matmul_block, matmul_simple, matmul_strassen
     from mpmm.scalar import PrecisionSpec
 
@@ -114,9 +114,12 @@ def main():
     for tok, n, cut, leaf in (("dd", 33, 8, 4), ("qd", 11, 4, 4)):
         p = prec_of[tok]
         ga, gb = generate_test_pair(n, p)
+        cs, cp = matmul_strassen(ga, gb, cut, leaf), matmul_simple(ga, gb)
+        # matrix.py:229-294 norms, evaluated by the reference
+        norms = np.array([frobenius_norm(ga), frobenius_rel_diff(cs, cp),
+                          frobenius_rel_diff(ga, gb)])
         save(f"{tok}_strassen_pair{n}_c{cut}_l{leaf}", a=ga.data, b=gb.data,
-             c_strassen=matmul_strassen(ga, gb, cut, leaf).data,
-             c_simple=matmul_simple(ga, gb).data)
+             c_strassen=cs.data, c_simple=cp.data, norms=norms)
     a, b = inputs.gemm_inputs("dd", 64, 64, 64, seed=16)
     save("dd_strassen_rand64_c16_l8", a=a, b=b,
          c_strassen=matmul_strassen(M(a, DD), M(b, DD), 16, 8).data)

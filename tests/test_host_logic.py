@@ -1,0 +1,273 @@
+"""Host-side logic of the drop-in (no GPU): choices, validation, partition,
+prediction arithmetic, timing policy, tuning tables, wave model, shards.
+Mirrors the reference's unit tests (tests/test_multiply.py, test_predict.py,
+test_tune.py, test_acceptance.py criteria 5 and 9)."""
+
+import math
+
+import numpy as np
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+import paper_1710_01839_b200 as mp
+from paper_1710_01839_b200 import shard
+from paper_1710_01839_b200.errors import MeasurementError, ShapeError, TableFormatError
+from paper_1710_01839_b200.multiply import _split_range
+from paper_1710_01839_b200.predict import (WaveModel, gpu_slice_rows,
+                                           predict_full_time_waves)
+
+DD = mp.PrecisionSpec.dd()
+QD = mp.PrecisionSpec.qd()
+
+
+def test_algorithm_choice_tokens():
+    for tok in ("simple", "block:64", "strassen:64/32"):
+        assert mp.AlgorithmChoice.parse(tok).token == tok
+    with pytest.raises(ValueError):
+        mp.AlgorithmChoice.parse("winograd")
+    with pytest.raises(ValueError):
+        mp.AlgorithmChoice(mp.Algorithm.BLOCK)
+    with pytest.raises(ValueError):
+        mp.AlgorithmChoice(mp.Algorithm.STRASSEN, n_min=8, cutoff=1)
+
+
+def test_precision_tokens_and_bounds():
+    assert mp.PrecisionSpec.parse("dd") == DD and DD.comps == 2 and QD.comps == 4
+    assert DD.gemm_bound_u == 2.0 ** -104 and QD.gemm_bound_u == 2.0 ** -209
+    assert mp.PrecisionSpec.parse("ap:128").bits == 128
+    with pytest.raises(ValueError):
+        mp.PrecisionSpec.parse("fp128")
+
+
+def test_shape_and_prec_errors():
+    a = mp.DenseMatrix.zeros(3, 4, DD)
+    with pytest.raises(ShapeError):
+        mp.matmul_simple(a, mp.DenseMatrix.zeros(3, 4, DD))
+    with pytest.raises(mp.PrecisionMismatchError):
+        mp.matmul_simple(mp.DenseMatrix.zeros(3, 3, DD), mp.DenseMatrix.zeros(3, 3, QD))
+    with pytest.raises(ShapeError):
+        mp.matmul_strassen(a, a)
+    sq = mp.DenseMatrix.zeros(4, 4, DD)
+    with pytest.raises(ValueError):
+        mp.matmul_strassen(sq, sq, cutoff=1)
+    with pytest.raises(ValueError):
+        mp.matmul_simple(sq, sq, threads=0)
+    with pytest.raises(ValueError):
+        mp.matmul_block(sq, sq, 0)
+    with pytest.raises(ShapeError):
+        mp.DenseMatrix(0, 3, DD, np.zeros((0, 3, 2)))
+
+
+def test_split_range_and_partition():
+    assert _split_range(10, 3) == [(0, 4), (4, 7), (7, 10)]
+    assert _split_range(2, 8) == [(0, 1), (1, 2)]
+    p = mp.make_partition(100, 64, 33, 32)
+    assert p.row_extents == (32, 32, 32, 4) and p.inner_extents == (32, 32)
+    assert p.col_extents == (32, 1) and p.n_blocks == 2
+
+
+def test_leading_rows_shares_storage():
+    m = mp.DenseMatrix.zeros(5, 3, DD)
+    s = mp.leading_rows(m, 2)
+    s.data[0, 0, 0] = 7.0
+    assert m.data[0, 0, 0] == 7.0
+    with pytest.raises(ShapeError):
+        mp.leading_rows(m, 6)
+
+
+def test_from_ints_and_identity_are_exact():
+    a = mp.DenseMatrix.from_ints([[1, 2], [3, 2 ** 60 + 1]], DD)
+    assert a.data[1, 1, 0] + a.data[1, 1, 1] == 2 ** 60 + 1
+    assert int(a.data[1, 1, 0]) + int(a.data[1, 1, 1]) == 2 ** 60 + 1
+    e = mp.DenseMatrix.identity(3, QD)
+    assert e.data[:, :, 0].tolist() == np.eye(3).tolist()
+
+
+# --- prediction (reference test_predict.py, acceptance criterion 5) --------
+
+def fake_clock(deltas):
+    state = {"t": 0.0, "i": 0}
+
+    def clock():
+        t = state["t"]
+        state["t"] += deltas[state["i"] % len(deltas)]
+        state["i"] += 1
+        return t
+    return clock
+
+
+def test_measure_aggregators():
+    for agg, want in (("median", 2.0), ("min", 1.0), ("mean", 2.0)):
+        pol = mp.TimingPolicy(measured_runs=3, aggregator=agg,
+                              clock=fake_clock([1.0, 0.0, 2.0, 0.0, 3.0, 0.0]))
+        assert mp.measure(lambda: None, pol) == want
+
+
+def test_measure_rejects_zero_and_validates():
+    with pytest.raises(MeasurementError):
+        mp.measure(lambda: None, mp.TimingPolicy(clock=lambda: 1.0))
+    with pytest.raises(ValueError):
+        mp.TimingPolicy(measured_runs=0)
+    with pytest.raises(ValueError):
+        mp.TimingPolicy(aggregator="max")
+    calls = []
+    mp.measure(lambda: None, mp.TimingPolicy(measured_runs=3, warmup_runs=1,
+                                             clock=fake_clock([0.5])),
+               setup=lambda: calls.append(1))
+    assert len(calls) == 4
+
+
+def test_slice_rows_and_published_values():
+    assert mp.slice_rows_for(64, 1024) == 128
+    assert mp.slice_rows_for(512, 1024) == 1024
+    assert mp.slice_rows_for(64, 1024, slice_multiplier=4) == 256
+    assert mp.predict_full_time(5.77, 1024, 64) == pytest.approx(46.16, abs=1e-12)
+    assert mp.predict_full_time(32.5, 1024, 128) == pytest.approx(130.0, abs=1e-12)
+    assert round(100 * mp.rel_diff(46.1, 45.97), 2) == 0.28
+    assert round(100 * mp.rel_diff(13.8, 14.66), 2) == 5.87
+    with pytest.raises(ValueError):
+        mp.predict_full_time(0.0, 100, 8)
+    with pytest.raises(ValueError):
+        mp.slice_rows_for(0, 10)
+
+
+@settings(max_examples=200, deadline=None)
+@given(st.floats(min_value=1e-6, max_value=1e6), st.integers(1, 10000), st.integers(1, 4096))
+def test_predict_linearity(t, m, n_min):
+    if 2 * n_min <= m:
+        assert mp.predict_full_time(t, 2 * m, n_min) == 2.0 * mp.predict_full_time(t, m, n_min)
+
+
+def test_choose_best_tie_break():
+    rec = lambda n, p: mp.PredictionRecord(n, 1, 1, p, p)  # noqa: E731
+    assert mp.choose_best([rec(64, 10.0), rec(128, 9.0), rec(256, 9.0)]) == 128
+
+
+def test_wave_model():
+    wm = WaveModel(tile_m=64, tile_n=64, concurrent_ctas=148)
+    assert wm.ctas(1024, 1024) == 256 and wm.waves(1024, 1024) == 2
+    rows = gpu_slice_rows(wm, 64, 1024, 1024)
+    assert rows % 64 == 0 and wm.ctas(rows, 1024) >= 148
+    assert predict_full_time_waves(1.0, wm, rows, 1024, 1024) == \
+        pytest.approx(wm.waves(1024, 1024) / wm.waves(rows, 1024))
+    assert gpu_slice_rows(wm, 64, 100, 1024) == 100
+
+
+# --- tuning tables (reference test_tune.py, acceptance criterion 9) --------
+
+def mk_row(prec, n, threads, strassen, best=8, t=1.0, gpus=1):
+    win = (mp.AlgorithmChoice(mp.Algorithm.STRASSEN, n_min=best, cutoff=64) if strassen
+           else mp.AlgorithmChoice(mp.Algorithm.BLOCK, n_min=best))
+    return mp.TuningResult(prec=prec, n=n, threads=threads, best_n_min=best, block_time_s=t,
+                           selection_time_s=t / 4, predicted_s=t * 1.01, rel_diff=0.01,
+                           simple_time_s=t * 2, strassen_time_s=t * (0.5 if strassen else 2.0),
+                           winner=win, gpus=gpus)
+
+
+def test_threshold_rules():
+    rows = [mk_row(DD, n, 1, s) for n, s in ((64, False), (128, True), (256, True), (512, True))]
+    assert mp.extract_threshold(rows, DD, 1) == 128
+    assert mp.extract_threshold([mk_row(DD, n, 1, False) for n in (64, 128)], DD, 1) is None
+    assert mp.extract_threshold([mk_row(QD, n, 1, True) for n in (63, 64, 128)], QD, 1) == 63
+    rows = [mk_row(DD, 64, 1, True), mk_row(DD, 64, 2, False)]
+    assert mp.extract_threshold(rows, DD, 2) is None
+
+
+def test_reference_fixture_round_trips_byte_for_byte(tmp_path):
+    # the v1 fixture of the reference's acceptance criterion 9
+    fixture = "\n".join([
+        "mpmmtune v1",
+        "total " + (45.97).hex(),
+        "predtotal " + (5.77).hex(),
+        f"dd,106 1024 1 64 {(45.97).hex()} {(5.77).hex()} {(46.1).hex()} "
+        f"{(0.0028).hex()} - {(25.54).hex()} strassen:64/64",
+        f"ap,128 1024 2 32 {(67.72).hex()} {(4.43).hex()} {(70.8).hex()} "
+        f"{(0.0455).hex()} - {(88.15).hex()} block:32",
+        "threshold dd,106 1 64",
+    ]) + "\n"
+    p = tmp_path / "f.tbl"
+    p.write_text(fixture)
+    t = mp.load_table(str(p))
+    assert t.rows[0].block_time_s == 45.97 and t.rows[0].winner.kind is mp.Algorithm.STRASSEN
+    assert t.thresholds[(DD, 1)] == 64
+    q = tmp_path / "g.tbl"
+    mp.save_table(t, str(q))
+    assert q.read_text() == fixture
+
+
+def test_v2_table_with_gpus(tmp_path):
+    t = mp.TuningTable(rows=[mk_row(DD, 1024, 1, False, gpus=8), mk_row(QD, 512, 1, True)],
+                       thresholds={(QD, 1): 512, (DD, 1, 8): 2048}, total_tuning_time_s=3.5,
+                       prediction_total_s=0.25,
+                       failures=[mp.TuningFailure(DD, 64, 1, "gap here", gpus=2)])
+    p = tmp_path / "v2.tbl"
+    mp.save_table(t, str(p))
+    assert p.read_text().startswith("mpmmtune v2")
+    assert mp.load_table(str(p)) == t
+    assert mp.lookup_best(t, DD, 1024, 1, gpus=8) == (t.rows[0].winner, "exact")
+    assert mp.lookup_best(t, DD, 4096, 1, gpus=8)[1] == "nearest"
+
+
+def test_table_errors(tmp_path):
+    p = tmp_path / "bad.tbl"
+    p.write_text("mpmmtune v9\n")
+    with pytest.raises(TableFormatError):
+        mp.load_table(str(p))
+    p.write_text("")
+    with pytest.raises(TableFormatError):
+        mp.load_table(str(p))
+    p.write_text("mpmmtune v1\ndd,106 1 2 3\n")
+    with pytest.raises(TableFormatError):
+        mp.load_table(str(p))
+
+
+def test_lookup_fallbacks():
+    t = mp.TuningTable(rows=[mk_row(DD, 128, 1, True)], thresholds={(DD, 1): 128})
+    assert mp.lookup_best(t, DD, 128, 1)[1] == "exact"
+    assert mp.lookup_best(t, DD, 200, 1)[1] == "nearest"
+    assert mp.lookup_best(t, DD, 64, 1)[1] == "default"
+    t2 = mp.TuningTable(rows=[], thresholds={(DD, 1): 128})
+    assert mp.lookup_best(t2, DD, 256, 1)[1] == "threshold"
+
+
+def test_tuning_config_validation():
+    with pytest.raises(ValueError):
+        mp.TuningConfig(precisions=[DD], dims=[], block_candidates=[4], thread_counts=[1])
+    with pytest.raises(ValueError):
+        mp.TuningConfig(precisions=[DD], dims=[1, 16], block_candidates=[4], thread_counts=[1])
+    cfg = mp.TuningConfig(precisions=[DD], dims=[16], block_candidates=[8, 4], thread_counts=[1])
+    assert cfg.block_candidates == [4, 8]
+
+
+def test_tune_sweep_records_failures(monkeypatch):
+    import paper_1710_01839_b200.tune as tune_mod
+
+    def flaky(prec, n, threads, cfg, _accum=None):
+        if n == 24:
+            raise RuntimeError("injected fault")
+        return mk_row(prec, n, threads, False)
+
+    monkeypatch.setattr(tune_mod, "tune_one", flaky)
+    monkeypatch.setattr(tune_mod, "_device_pair",
+                        lambda n, prec: (mp.DenseMatrix.zeros(n, n, prec),) * 2)
+    monkeypatch.setattr(tune_mod, "_block_into", lambda *a, **k: None)
+    cfg = mp.TuningConfig(precisions=[DD], dims=[16, 24], block_candidates=[4, 8],
+                          thread_counts=[1])
+    table = mp.tune_sweep(cfg)
+    assert len(table.rows) == 1 and len(table.failures) == 1
+    assert "injected" in table.failures[0].message
+
+
+# --- sharding -----------------------------------------------------------------
+
+def test_row_shards_cover_exactly():
+    for m, world, align in ((1024, 8, 64), (1000, 3, 16), (5, 8, 1), (0, 2, 1)):
+        parts = shard.row_shards(m, world, align)
+        assert len(parts) == world
+        covered = [i for lo, hi in parts for i in range(lo, hi)]
+        assert covered == list(range(m))
+        for lo, hi in parts:
+            assert lo % align == 0 or lo == m
+    assert shard.panel_bounds(10, 4) == [(0, 4), (4, 8), (8, 10)]
+    assert shard.panel_bounds(10, None) == [(0, 10)]

@@ -1,0 +1,69 @@
+"""Multi-rank sharding on CPU: world_size 2 over gloo.
+
+Each rank owns a row block of A and C; B is broadcast from rank 0 in
+k-panels; the per-panel compute is injected (the CPU oracle here, the
+sm_100a kernels in production).  The gathered C must be bitwise equal to
+the single-process product for every panel size: the GPU-count
+invariance contract.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as tmp
+
+import oracle
+from paper_1710_01839_b200 import inputs, shard
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _oracle_local_gemm(a_local, b_panel, c_local, k0, k1, accumulate):
+    a = a_local.numpy()[:, k0:k1].copy()
+    b = b_panel.numpy().copy()
+    c = c_local.numpy()
+    if not accumulate:
+        c[...] = 0.0
+    # block_cells accumulates into c over all cells: C += A_panel B_panel
+    cells = (-(-a.shape[0] // 8)) * (-(-b.shape[1] // 8)) if a.shape[0] else 0
+    if cells:
+        oracle.block_cells(a, b, c, 8, 0, cells)
+
+
+def _worker(rank, world, port, tok, m, l, n, panel, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a, b = inputs.gemm_inputs(tok, m, l, n, seed=5)
+        lo, hi = shard.row_shards(m, world, align=4)[rank]
+        a_local = torch.from_numpy(np.ascontiguousarray(a[lo:hi]))
+        b_buf = torch.from_numpy(b.copy()) if rank == 0 else torch.zeros(b.shape, dtype=torch.float64)
+        c_local = shard.broadcast_matmul(a_local, b_buf, panel_rows=panel, src=0,
+                                         local_gemm=_oracle_local_gemm)
+        np.save(f"{out_path}.{rank}.npy", c_local.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("tok,m,l,n,panel", [("dd", 21, 17, 9, 5), ("dd", 16, 16, 16, None),
+                                              ("qd", 7, 6, 5, 4)])
+def test_two_rank_broadcast_matmul_is_bitwise_invariant(tmp_path, tok, m, l, n, panel):
+    world = 2
+    out = str(tmp_path / "c")
+    tmp.spawn(_worker, args=(world, _free_port(), tok, m, l, n, panel, out), nprocs=world,
+              join=True)
+    parts = [np.load(f"{out}.{r}.npy") for r in range(world)]
+    c = np.concatenate(parts, axis=0)
+    a, b = inputs.gemm_inputs(tok, m, l, n, seed=5)
+    assert np.array_equal(c, oracle.matmul_simple(a, b))
