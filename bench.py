@@ -47,7 +47,8 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--prec", default="dd", choices=["dd", "qd"])
     p.add_argument("--n", type=int, default=1024)
-    p.add_argument("--nmin", type=int, default=64)
+    p.add_argument("--nmin", type=int, default=0,
+                   help="block size; 0 = let the GPU predictor pick from 16..256")
     p.add_argument("--panel", type=int, default=0, help="k-panel rows for the B broadcast")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=8.0)
@@ -150,6 +151,8 @@ def cpu_reference_run(prec_tok, n, n_min, seconds):
 def run_reference(args, rank, world):
     if rank != 0:
         return
+    if args.nmin <= 0:
+        args.nmin = 64   # the reference's DEFAULT_BLOCK_SIZE (multiply.py:32)
     steps = max(1, args.steps)
     per_step = max(1.0, min(args.cpu_seconds, 60.0 / (steps + args.warmup)))
     vals = []
@@ -247,6 +250,22 @@ def run_ours(args, rank, world, local_rank):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     panel = args.panel if args.panel > 0 else None
     panels = len(shard.panel_bounds(n, panel))
+    tuner = None
+    if args.nmin <= 0:
+        # the reference's step 1 (tune.py:137-143) on the device, outside
+        # the timed region: wave-aware prediction over the BASELINE sweep
+        Bt = B if rank == 0 else torch.from_numpy(b_full).to(dev)
+        best, recs = mp.select_block_size(
+            DenseMatrix(n, n, prec, A), DenseMatrix(n, n, prec, Bt), [16, 32, 64, 128, 256],
+            policy=mp.TimingPolicy(warmup_runs=1, measured_runs=3, aggregator="min"))
+        if world > 1:
+            t_best = torch.tensor([best], dtype=torch.int64, device=dev)
+            dist.broadcast(t_best, src=0)
+            best = int(t_best.item())
+        args.nmin = best
+        tuner = {"chosen_n_min": best, "records": [
+            {"n_min": r.n_min, "slice_rows": r.slice_rows, "slice_ms": r.slice_time_s * 1e3,
+             "predicted_ms": r.predicted_full_s * 1e3} for r in recs]}
 
     def step():
         return shard.broadcast_matmul(A, B, n_min=args.nmin, src=0, panel_rows=panel)
@@ -354,6 +373,7 @@ def run_ours(args, rank, world, local_rank):
                        "shard.sharded_matmul_host"},
         "roofline": roofline,
         "gpu_launches": gemm_launches,
+        "tuner": tuner,
         "wall_s_timed_region": t_wall,
         "clocks": clocks,
     }

@@ -98,6 +98,15 @@ int mpmm_gemm_dev(int comps, int algo, int64_t n_min, int64_t m, int64_t l, int6
                   const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
                   int64_t ldc, int accumulate, int *nonfinite, void *stream);
 
+/* Batched form of mpmm_gemm_dev: `batch` independent problems of one
+ * shape, described by a DEVICE array of `batch` records of six 64-bit
+ * words {A, B, C, lda, ldb, ldc} (pointers, then element leading dims).
+ * Used for the 7^d leaf products of a Strassen recursion
+ * (multiply.py:293-332) so they fill the GPU in one launch. */
+int mpmm_gemm_batched_dev(int comps, int algo, int64_t n_min, int64_t batch, int64_t m,
+                          int64_t l, int64_t n, const void *problems, int accumulate,
+                          int *nonfinite, void *stream);
+
 /* The reference's cell-range protocol on device pointers
  * (_kernels.pyx:103-186 / :366-404): cells [cell0,cell1) accumulate into C. */
 int mpmm_block_cells_dev(int comps, int64_t n_min, int64_t cell0, int64_t cell1, int64_t m,
@@ -111,6 +120,12 @@ int mpmm_ewise_dev(int comps, int nops, int64_t rows, int64_t cols, const double
                    int64_t ldx, const double *Y, int64_t ldy, int sy, const double *Z,
                    int64_t ldz, int sz, const double *W, int64_t ldw, int sw, double *O,
                    int64_t ldo, void *stream);
+
+/* Batched form of mpmm_ewise_dev: a DEVICE array of `batch` records of 14
+ * 64-bit words {X, Y, Z, W, O, ldx, ldy, ldz, ldw, ldo, nops, sy, sz, sw}
+ * sharing rows x cols (one Strassen level's operand sums or combinations). */
+int mpmm_ewise_batched_dev(int comps, int64_t batch, int64_t rows, int64_t cols,
+                           const void *problems, void *stream);
 
 /* multiply.py:124-127 _check_finite on the device: *flag |= 1 if any
  * component of the rows x cols view X is not finite. */

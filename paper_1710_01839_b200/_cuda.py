@@ -48,6 +48,8 @@ _SIGNATURES = {
     "mpmm_qd_ewise_sub": [_D, _D, _D, _I64, _I64, _I64, _I64],
     "mpmm_gemm_dev": [_INT, _INT, _I64, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64,
                       _INT, _VP, _VP],
+    "mpmm_gemm_batched_dev": [_INT, _INT, _I64, _I64, _I64, _I64, _I64, _VP, _INT, _VP, _VP],
+    "mpmm_ewise_batched_dev": [_INT, _I64, _I64, _I64, _VP, _VP],
     "mpmm_block_cells_dev": [_INT, _I64, _I64, _I64, _I64, _I64, _I64, _VP, _I64, _VP, _I64,
                              _VP, _I64, _VP],
     "mpmm_ewise_dev": [_INT, _INT, _I64, _I64, _VP, _I64, _VP, _I64, _INT, _VP, _I64, _INT,
@@ -199,6 +201,18 @@ def gemm_dev(comps, algo, n_min, m, l, n, A, lda, B, ldb, C, ldc, accumulate,
              nonfinite=None, stream=None):
     check(load().mpmm_gemm_dev(comps, algo, n_min, m, l, n, A, lda, B, ldb, C, ldc,
                                1 if accumulate else 0, nonfinite, stream))
+
+
+def gemm_batched_dev(comps, algo, n_min, batch, m, l, n, problems, accumulate, nonfinite=None,
+                     stream=None):
+    """``problems``: device pointer to ``batch`` x 6 int64 {A, B, C, lda, ldb, ldc}."""
+    check(load().mpmm_gemm_batched_dev(comps, algo, n_min, batch, m, l, n, problems,
+                                       1 if accumulate else 0, nonfinite, stream))
+
+
+def ewise_batched_dev(comps, batch, rows, cols, problems, stream=None):
+    """``problems``: device pointer to ``batch`` x 14 int64 (see mpmm_cuda.h)."""
+    check(load().mpmm_ewise_batched_dev(comps, batch, rows, cols, problems, stream))
 
 
 def block_cells_dev(comps, n_min, cell0, cell1, m, l, n, A, lda, B, ldb, C, ldc, stream=None):

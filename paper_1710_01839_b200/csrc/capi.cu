@@ -39,18 +39,19 @@ bool dims_ok(int64_t m, int64_t l, int64_t n) {
 
 void tile_for(int64_t n_min, int* tile, int* super) {
   // n_min is the reference's cache block size (multiply.py:148-160).  On the
-  // GPU it selects the CTA tile; n_min beyond one CTA tile becomes an L2
-  // super-tile of (n_min/64)^2 CTAs walked together.
+  // GPU it selects the CTA tile configuration; results never
+  // depend on it.  `super` is kept in the ABI for table compatibility (1).
   *super = 1;
   if (n_min <= 16) {
     *tile = TILE_16;
   } else if (n_min <= 32) {
     *tile = TILE_32;
   } else if (n_min <= 64) {
-    *tile = TILE_64;
+    *tile = TILE_LPT;
+  } else if (n_min <= 128) {
+    *tile = TILE_32x64;
   } else {
     *tile = TILE_64;
-    *super = (int)((n_min + 63) / 64);
   }
 }
 
@@ -85,7 +86,7 @@ int block_cells_impl(int comps, int64_t n_min, int64_t cell0, int64_t cell1, int
     r1 = r1 < m ? r1 : m;
     c1 = c1 < n ? c1 : n;
     if (r1 <= r0 || c1 <= c0) return MPMM_OK;
-    GemmArgs g{ALGO_BLOCK, tile, super, (int)(r1 - r0), (int)(c1 - c0), (int)l,
+    GemmArgs g{ALGO_BLOCK, tile, (int)(r1 - r0), (int)(c1 - c0), (int)l,
                A + comps * (r0 * lda), lda, B + comps * c0, ldb,
                C + comps * (r0 * ldc + c0), ldc, 1, nullptr, stream};
     cudaError_t e = gemm(comps, g);
@@ -112,7 +113,7 @@ int host_simple_rows(int comps, const double* a, const double* b, double* c, int
   CU(cudaMemcpy(dA.p, a + i0 * l * comps, rows * l * comps * sizeof(double),
                 cudaMemcpyHostToDevice));
   CU(cudaMemcpy(dB.p, b, l * n * comps * sizeof(double), cudaMemcpyHostToDevice));
-  GemmArgs g{ALGO_SIMPLE, TILE_16, 1, (int)rows, (int)n, (int)l, dA.p, l, dB.p, n, dC.p, n,
+  GemmArgs g{ALGO_SIMPLE, TILE_16, (int)rows, (int)n, (int)l, dA.p, l, dB.p, n, dC.p, n,
              0, nullptr, 0};
   CU(gemm(comps, g));
   CU(cudaMemcpy(c + i0 * n * comps, dC.p, rows * n * comps * sizeof(double),
@@ -255,10 +256,29 @@ int mpmm_gemm_dev(int comps, int algo, int64_t n_min, int64_t m, int64_t l, int6
   if (algo == MPMM_ALGO_BLOCK && n_min < 1) return fail(MPMM_ERR_ARG, "block size must be positive");
   int tile = TILE_16, super = 1;
   if (algo == MPMM_ALGO_BLOCK) tile_for(n_min, &tile, &super);
-  GemmArgs g{algo, tile, super, (int)m, (int)n, (int)l, A, lda, B, ldb, C, ldc,
+  GemmArgs g{algo, tile, (int)m, (int)n, (int)l, A, lda, B, ldb, C, ldc,
              accumulate ? 1 : 0, nonfinite, (cudaStream_t)stream};
   cudaError_t e = gemm(comps, g);
   return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "gemm launch");
+}
+
+int mpmm_gemm_batched_dev(int comps, int algo, int64_t n_min, int64_t batch, int64_t m,
+                          int64_t l, int64_t n, const void* problems, int accumulate,
+                          int* nonfinite, void* stream) {
+  if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
+  if (!dims_ok(m, l, n) || batch < 0 || batch > (1 << 24)) return fail(MPMM_ERR_ARG, "bad shape");
+  if (algo != MPMM_ALGO_SIMPLE && algo != MPMM_ALGO_BLOCK) return fail(MPMM_ERR_ARG, "bad algo");
+  if (algo == MPMM_ALGO_BLOCK && n_min < 1) return fail(MPMM_ERR_ARG, "block size must be positive");
+  if (batch == 0) return MPMM_OK;
+  if (problems == nullptr) return fail(MPMM_ERR_ARG, "null problem array");
+  int tile = TILE_16, super = 1;
+  if (algo == MPMM_ALGO_BLOCK) tile_for(n_min, &tile, &super);
+  GemmArgs g{algo, tile, (int)m, (int)n, (int)l, nullptr, 0, nullptr, 0, nullptr, 0,
+             accumulate ? 1 : 0, nonfinite, (cudaStream_t)stream};
+  g.batch = (int)batch;
+  g.probs = static_cast<const GemmProblem*>(problems);
+  cudaError_t e = gemm(comps, g);
+  return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "batched gemm launch");
 }
 
 int mpmm_block_cells_dev(int comps, int64_t n_min, int64_t cell0, int64_t cell1, int64_t m,
@@ -281,6 +301,18 @@ int mpmm_ewise_dev(int comps, int nops, int64_t rows, int64_t cols, const double
               Z, ldz, sz < 0 ? -1 : 1, W, ldw, sw < 0 ? -1 : 1, O, ldo, (cudaStream_t)stream};
   cudaError_t err = ewise_launch(e);
   return err == cudaSuccess ? MPMM_OK : cuda_fail(err, "ewise launch");
+}
+
+int mpmm_ewise_batched_dev(int comps, int64_t batch, int64_t rows, int64_t cols,
+                           const void* problems, void* stream) {
+  if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
+  if (!dims_ok(rows, 0, cols) || batch < 0 || batch > 65535) return fail(MPMM_ERR_ARG, "bad shape");
+  if (batch == 0) return MPMM_OK;
+  if (problems == nullptr) return fail(MPMM_ERR_ARG, "null problem array");
+  cudaError_t err = ewise_batched_launch(comps, (int)batch, (int)rows, (int)cols,
+                                         static_cast<const EwiseProblem*>(problems),
+                                         (cudaStream_t)stream);
+  return err == cudaSuccess ? MPMM_OK : cuda_fail(err, "batched ewise launch");
 }
 
 int mpmm_nonfinite_dev(int comps, int64_t rows, int64_t cols, const double* X, int64_t ldx,

@@ -13,92 +13,75 @@
 
 namespace mpmm {
 
-__global__ void __launch_bounds__(256)
-dd_ewise_kernel(EwiseArgs e) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
-  int i = blockIdx.y;
-  if (j >= e.cols) return;
-  const double2* X = reinterpret_cast<const double2*>(e.X);
-  const double2* Y = reinterpret_cast<const double2*>(e.Y);
-  double2 x = X[(int64_t)i * e.ldx + j];
-  double2 y = Y[(int64_t)i * e.ldy + j];
-  double h, lo;
-  double yh = e.sy < 0 ? -y.x : y.x, yl = e.sy < 0 ? -y.y : y.y;
-  dd_add(x.x, x.y, yh, yl, h, lo);
-  if (e.nops >= 2) {
-    double2 z = reinterpret_cast<const double2*>(e.Z)[(int64_t)i * e.ldz + j];
-    double zh = e.sz < 0 ? -z.x : z.x, zl = e.sz < 0 ? -z.y : z.y;
-    dd_add(h, lo, zh, zl, h, lo);
-  }
-  if (e.nops >= 3) {
-    double2 w = reinterpret_cast<const double2*>(e.W)[(int64_t)i * e.ldw + j];
-    double wh = e.sw < 0 ? -w.x : w.x, wl = e.sw < 0 ? -w.y : w.y;
-    dd_add(h, lo, wh, wl, h, lo);
-  }
-  reinterpret_cast<double2*>(e.O)[(int64_t)i * e.ldo + j] = make_double2(h, lo);
-}
-
-__device__ __forceinline__ void qd_load(const double* base, int64_t ld, int i, int j, int sign,
-                                        double v[4]) {
-  const double2* p = reinterpret_cast<const double2*>(base) + 2 * ((int64_t)i * ld + j);
-  double2 a = p[0], b = p[1];
-  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
-  if (sign < 0) {
-    v[0] = -v[0]; v[1] = -v[1]; v[2] = -v[2]; v[3] = -v[3];
+__device__ __forceinline__ void load_elem(const double* base, int64_t ld, int i, int j, int V,
+                                          int sign, double* v) {
+  const double2* p = reinterpret_cast<const double2*>(base) + ((int64_t)i * ld + j) * V;
+  for (int q = 0; q < V; ++q) {
+    double2 x = p[q];
+    v[2 * q] = sign < 0 ? -x.x : x.x;
+    v[2 * q + 1] = sign < 0 ? -x.y : x.y;
   }
 }
 
+// out = ((x sy y) sz z) sw w, one reference ewise op per step.
+template <int V>
+__device__ __forceinline__ void ewise_elem(const EwiseProblem& e, int i, int j) {
+  double x[2 * V], y[2 * V], r[2 * V];
+  load_elem(e.X, e.ldx, i, j, V, 1, x);
+  load_elem(e.Y, e.ldy, i, j, V, (int)e.sy, y);
+  const double* ops[2] = {e.Z, e.W};
+  const int64_t lds[2] = {e.ldz, e.ldw};
+  const int sg[2] = {(int)e.sz, (int)e.sw};
+  if constexpr (V == 1) {
+    dd_add(x[0], x[1], y[0], y[1], r[0], r[1]);
+    for (int s = 0; s < 2 && s + 2 <= e.nops; ++s) {
+      load_elem(ops[s], lds[s], i, j, V, sg[s], y);
+      dd_add(r[0], r[1], y[0], y[1], r[0], r[1]);
+    }
+  } else {
+    qd_add(x, y, r);
+    for (int s = 0; s < 2 && s + 2 <= e.nops; ++s) {
+      load_elem(ops[s], lds[s], i, j, V, sg[s], y);
+      double t[4] = {r[0], r[1], r[2], r[3]};
+      qd_add(t, y, r);
+    }
+  }
+  double2* o = reinterpret_cast<double2*>(e.O) + ((int64_t)i * e.ldo + j) * V;
+  for (int q = 0; q < V; ++q) o[q] = make_double2(r[2 * q], r[2 * q + 1]);
+}
+
+template <int V>
 __global__ void __launch_bounds__(256)
-qd_ewise_kernel(EwiseArgs e) {
+ewise_kernel(const EwiseProblem* __restrict__ probs, EwiseProblem single, int rows, int cols) {
+  const EwiseProblem e = probs ? probs[blockIdx.z] : single;
   int j = blockIdx.x * blockDim.x + threadIdx.x;
-  int i = blockIdx.y;
-  if (j >= e.cols) return;
-  double x[4], y[4], r[4];
-  qd_load(e.X, e.ldx, i, j, 1, x);
-  qd_load(e.Y, e.ldy, i, j, e.sy, y);
-  qd_add(x, y, r);
-  if (e.nops >= 2) {
-    qd_load(e.Z, e.ldz, i, j, e.sz, y);
-    double t[4] = {r[0], r[1], r[2], r[3]};
-    qd_add(t, y, r);
-  }
-  if (e.nops >= 3) {
-    qd_load(e.W, e.ldw, i, j, e.sw, y);
-    double t[4] = {r[0], r[1], r[2], r[3]};
-    qd_add(t, y, r);
-  }
-  double2* o = reinterpret_cast<double2*>(e.O) + 2 * ((int64_t)i * e.ldo + j);
-  o[0] = make_double2(r[0], r[1]);
-  o[1] = make_double2(r[2], r[3]);
+  if (j >= cols) return;
+  for (int i = blockIdx.y; i < rows; i += gridDim.y) ewise_elem<V>(e, i, j);
+}
+
+static cudaError_t ewise_go(int comps, int batch, int rows, int cols, const EwiseProblem* probs,
+                            const EwiseProblem& single, cudaStream_t stream) {
+  if (rows <= 0 || cols <= 0 || batch <= 0) return cudaSuccess;
+  if (batch > 65535) return cudaErrorInvalidValue;
+  int threads = cols >= 256 ? 256 : ((cols + 31) / 32) * 32;
+  dim3 grid((cols + threads - 1) / threads, rows < 4096 ? rows : 4096, batch);
+  if (comps == 2)
+    ewise_kernel<1><<<grid, threads, 0, stream>>>(probs, single, rows, cols);
+  else
+    ewise_kernel<2><<<grid, threads, 0, stream>>>(probs, single, rows, cols);
+  return cudaGetLastError();
 }
 
 cudaError_t ewise_launch(const EwiseArgs& e) {
-  if (e.rows <= 0 || e.cols <= 0) return cudaSuccess;
-  if (e.rows > 65535 * 1024) return cudaErrorInvalidValue;
-  int threads = e.cols >= 256 ? 256 : ((e.cols + 31) / 32) * 32;
-  dim3 grid((e.cols + threads - 1) / threads, e.rows);
-  if (e.rows > 65535) {
-    // fall back to row chunks: gridDim.y is limited to 65535
-    for (int r0 = 0; r0 < e.rows; r0 += 65535) {
-      EwiseArgs c = e;
-      int rr = e.rows - r0 < 65535 ? e.rows - r0 : 65535;
-      int64_t off = (int64_t)r0 * e.comps;
-      c.rows = rr;
-      c.X = e.X + off * e.ldx;
-      c.Y = e.Y + off * e.ldy;
-      if (e.Z) c.Z = e.Z + off * e.ldz;
-      if (e.W) c.W = e.W + off * e.ldw;
-      c.O = e.O + off * e.ldo;
-      cudaError_t err = ewise_launch(c);
-      if (err != cudaSuccess) return err;
-    }
-    return cudaSuccess;
-  }
-  if (e.comps == 2)
-    dd_ewise_kernel<<<grid, threads, 0, e.stream>>>(e);
-  else
-    qd_ewise_kernel<<<grid, threads, 0, e.stream>>>(e);
-  return cudaGetLastError();
+  EwiseProblem p{e.X, e.Y, e.Z, e.W, e.O, e.ldx, e.ldy, e.ldz, e.ldw, e.ldo,
+                 e.nops, e.sy, e.sz, e.sw};
+  return ewise_go(e.comps, 1, e.rows, e.cols, nullptr, p, e.stream);
+}
+
+cudaError_t ewise_batched_launch(int comps, int batch, int rows, int cols,
+                                 const EwiseProblem* probs, cudaStream_t stream) {
+  EwiseProblem none{};
+  return ewise_go(comps, batch, rows, cols, probs, none, stream);
 }
 
 // multiply.py:124-127 _check_finite: any non-finite component -> flag.

@@ -1,0 +1,340 @@
+// gemm.cuh -- generic DD/QD GEMM kernels for sm_100a (bit-exact mirrors).
+//
+// C (m x n) = A (m x l) * B (l x n), or C += A*B, for a batch of P
+// independent problems of one shape (P = 1 for a plain product; the 7^d
+// leaves of a Strassen recursion otherwise).  Matrices are row-major views
+// of DD (one double2 per element) or QD (two double2) elements with leading
+// dimensions in elements: the reference's AoS layout (matrix.py:20,43-48).
+//
+// Per output element the k loop runs in ascending order from an
+// accumulator that starts at zero (overwrite) or at C (accumulate), and
+// every step is the reference's multiply-add (Ops::madd, ddqd.cuh), so each
+// element is bit-identical to the reference kernels for ANY tiling, tile
+// order or batch grouping: tile shapes are performance knobs only.
+//
+// Kernels are bound by the FP64 pipe (DD: 50 FP64 instructions per
+// multiply-add; QD: ~786).  Operand tiles are staged in shared memory with
+// cp.async double buffering; each thread owns a TM x TN register tile.
+//
+// Load balance.  At moderate sizes the tile count is a few waves of 148
+// SMs, and the last partial wave costs up to half a wave of idle FP64
+// pipes.  gemm_lpt is a persistent kernel (one CTA per resident slot) that
+// processes whole-wave batches of big tiles first and splits the remaining
+// big tiles into four quarter tiles (largest-processing-time-first), so
+// every SM ends within about one quarter tile of the others.
+#pragma once
+
+#include "common.cuh"
+#include "ddqd.cuh"
+#include "kernels.h"
+
+namespace mpmm {
+
+struct DDOps {
+  static constexpr int V = 1;     // double2 vectors per element
+  static constexpr int NACC = 2;  // accumulator doubles
+  __device__ __forceinline__ static void madd(double* acc, const double2* a, const double2* b) {
+    dd_madd(acc[0], acc[1], a[0].x, a[0].y, b[0].x, b[0].y);
+  }
+};
+
+struct QDOps {
+  static constexpr int V = 2;
+  static constexpr int NACC = 4;
+  __device__ __forceinline__ static void madd(double* acc, const double2* a, const double2* b) {
+    const double x[4] = {a[0].x, a[0].y, a[1].x, a[1].y};
+    const double y[4] = {b[0].x, b[0].y, b[1].x, b[1].y};
+    qd_mul_add(acc, x, y);
+  }
+};
+
+// Problem descriptor (pointers as double2 views, leading dims in elements).
+struct Prob {
+  const double2* A;
+  const double2* B;
+  double2* C;
+  int64_t lda, ldb, ldc;
+};
+
+__device__ __forceinline__ Prob get_prob(const GemmProblem* probs, const Prob& single, int p) {
+  if (probs == nullptr) return single;
+  const GemmProblem& g = probs[p];
+  return Prob{reinterpret_cast<const double2*>(g.A), reinterpret_cast<const double2*>(g.B),
+              reinterpret_cast<double2*>(g.C), g.lda, g.ldb, g.ldc};
+}
+
+// Shared-memory footprint (in double2) of one BM x BN x BK tile pair.
+template <class Ops, int BM, int BN, int BK>
+struct TileSmem {
+  static constexpr int A_STAGE = BM * (BK + 1) * Ops::V;
+  static constexpr int B_STAGE = BK * BN * Ops::V;
+  static constexpr int TOTAL = 2 * (A_STAGE + B_STAGE);
+};
+
+// One CTA computes the BM x BN output tile at (m0, n0) of problem `pr`.
+// NT threads: thread (tx, ty) owns rows ty + r*NTY, cols tx + c*NTX.
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int NT>
+__device__ __forceinline__ void gemm_tile(const Prob& pr, int m, int n, int l, int accumulate,
+                                          int m0, int n0, double2* smem, bool& bad) {
+  constexpr int V = Ops::V;
+  constexpr int NTX = BN / TN, NTY = BM / TM;
+  static_assert(NTX * NTY == NT, "thread tile does not cover the CTA tile");
+  using S = TileSmem<Ops, BM, BN, BK>;
+  // As[stage][row][k][v], Bs[stage][k][col][v]
+  auto As = [&](int st, int r, int k, int v) -> double2& {
+    return smem[st * S::A_STAGE + (r * (BK + 1) + k) * V + v];
+  };
+  auto Bs = [&](int st, int k, int c, int v) -> double2& {
+    return smem[2 * S::A_STAGE + st * S::B_STAGE + (k * BN + c) * V + v];
+  };
+  const int tid = threadIdx.x;
+  const int tx = tid % NTX, ty = tid / NTX;
+
+  double acc[TM][TN][Ops::NACC];
+#pragma unroll
+  for (int r = 0; r < TM; ++r)
+#pragma unroll
+    for (int c = 0; c < TN; ++c) {
+      int i = m0 + ty + r * NTY, j = n0 + tx + c * NTX;
+      bool load = accumulate && i < m && j < n;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        double2 x = load ? pr.C[((int64_t)i * pr.ldc + j) * V + v] : make_double2(0.0, 0.0);
+        acc[r][c][2 * v] = x.x;
+        acc[r][c][2 * v + 1] = x.y;
+      }
+    }
+
+  const int ktiles = (l + BK - 1) / BK;
+  auto load = [&](int kt, int st) {
+    const int k0 = kt * BK;
+#pragma unroll
+    for (int e = tid; e < BM * BK * V; e += NT) {
+      int v = e % V, el = e / V;
+      int row = el / BK, col = el % BK;
+      int gi = m0 + row, gk = k0 + col;
+      bool ok = gi < m && gk < l;
+      const double2* src = ok ? pr.A + ((int64_t)gi * pr.lda + gk) * V + v : pr.A;
+      cp_async16(&As(st, row, col, v), src, ok);
+    }
+#pragma unroll
+    for (int e = tid; e < BK * BN * V; e += NT) {
+      int v = e % V, el = e / V;
+      int row = el / BN, col = el % BN;
+      int gk = k0 + row, gj = n0 + col;
+      bool ok = gk < l && gj < n;
+      const double2* src = ok ? pr.B + ((int64_t)gk * pr.ldb + gj) * V + v : pr.B;
+      cp_async16(&Bs(st, row, col, v), src, ok);
+    }
+  };
+
+  if (ktiles > 0) {
+    load(0, 0);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int st = kt & 1;
+    if (kt + 1 < ktiles) {
+      load(kt + 1, st ^ 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int kcount = min(BK, l - kt * BK);
+    auto step = [&](int kk) {
+      double2 a[TM][V], b[TN][V];
+#pragma unroll
+      for (int r = 0; r < TM; ++r)
+#pragma unroll
+        for (int v = 0; v < V; ++v) a[r][v] = As(st, ty + r * NTY, kk, v);
+#pragma unroll
+      for (int c = 0; c < TN; ++c)
+#pragma unroll
+        for (int v = 0; v < V; ++v) b[c][v] = Bs(st, kk, tx + c * NTX, v);
+#pragma unroll
+      for (int r = 0; r < TM; ++r)
+#pragma unroll
+        for (int c = 0; c < TN; ++c) Ops::madd(acc[r][c], a[r], b[c]);
+    };
+    if (kcount == BK) {
+#pragma unroll 2
+      for (int kk = 0; kk < BK; ++kk) step(kk);
+    } else {
+      for (int kk = 0; kk < kcount; ++kk) step(kk);
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int r = 0; r < TM; ++r)
+#pragma unroll
+    for (int c = 0; c < TN; ++c) {
+      int i = m0 + ty + r * NTY, j = n0 + tx + c * NTX;
+      if (i < m && j < n) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          pr.C[((int64_t)i * pr.ldc + j) * V + v] =
+              make_double2(acc[r][c][2 * v], acc[r][c][2 * v + 1]);
+          bad |= !finite2(acc[r][c][2 * v], acc[r][c][2 * v + 1]);
+        }
+      }
+    }
+}
+
+// Plain tiled kernel: one CTA per (problem, tile).
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
+gemm_tiled(const GemmProblem* __restrict__ probs, Prob single, int m, int n, int l,
+           int accumulate, int* __restrict__ nonfinite) {
+  constexpr int NT = (BM / TM) * (BN / TN);
+  __shared__ __align__(16) double2 smem[TileSmem<Ops, BM, BN, BK>::TOTAL];
+  const int tiles_n = (n + BN - 1) / BN, tiles_m = (m + BM - 1) / BM;
+  const int per = tiles_m * tiles_n;
+  const int p = blockIdx.x / per, t = blockIdx.x % per;
+  const Prob pr = get_prob(probs, single, p);
+  bool bad = false;
+  gemm_tile<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, (t / tiles_n) * BM,
+                                         (t % tiles_n) * BN, smem, bad);
+  if (nonfinite != nullptr && bad) atomicOr(nonfinite, 1);
+}
+
+// Persistent largest-first kernel: big BM x BN tiles in whole waves, then
+// the leftover big tiles as quarter tiles (BM/2 x BN/2, TM/2 x TN/2 per
+// thread, same thread count).
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
+gemm_lpt(const GemmProblem* __restrict__ probs, Prob single, int P, int m, int n, int l,
+         int accumulate, int* __restrict__ nonfinite) {
+  constexpr int NT = (BM / TM) * (BN / TN);
+  static_assert(TM % 2 == 0 && TN % 2 == 0, "quarter tiles need even thread tiles");
+  __shared__ __align__(16) double2 smem[TileSmem<Ops, BM, BN, BK>::TOTAL];
+  const int tiles_n = (n + BN - 1) / BN, tiles_m = (m + BM - 1) / BM;
+  const int per = tiles_m * tiles_n;
+  const int T = P * per;
+  const int S = gridDim.x;
+  const int nbig = (T / S) * S;
+  const int units = nbig + 4 * (T - nbig);
+  bool bad = false;
+  for (int u = blockIdx.x; u < units; u += S) {
+    int t, q = -1;
+    if (u < nbig) {
+      t = u;
+    } else {
+      t = nbig + (u - nbig) / 4;
+      q = (u - nbig) % 4;
+    }
+    const int p = t / per, tt = t % per;
+    const Prob pr = get_prob(probs, single, p);
+    int m0 = (tt / tiles_n) * BM, n0 = (tt % tiles_n) * BN;
+    if (q < 0) {
+      gemm_tile<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, m0, n0, smem, bad);
+    } else {
+      m0 += (q / 2) * (BM / 2);
+      n0 += (q % 2) * (BN / 2);
+      if (m0 < m && n0 < n)  // uniform per CTA: no divergent barriers
+        gemm_tile<Ops, BM / 2, BN / 2, BK, TM / 2, TN / 2, NT>(pr, m, n, l, accumulate, m0, n0,
+                                                              smem, bad);
+    }
+  }
+  if (nonfinite != nullptr && bad) atomicOr(nonfinite, 1);
+}
+
+// The reference's "simple" algorithm: one thread per output element, the
+// operands read straight from global memory (L1/L2), no staging.
+template <class Ops>
+__global__ void __launch_bounds__(256)
+gemm_simple(const GemmProblem* __restrict__ probs, Prob single, int m, int n, int l,
+            int accumulate, int* __restrict__ nonfinite) {
+  constexpr int V = Ops::V;
+  const int p = blockIdx.z;
+  const Prob pr = get_prob(probs, single, p);
+  int j = blockIdx.x * 32 + (threadIdx.x & 31);
+  int i = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (i >= m || j >= n) return;
+  double acc[Ops::NACC];
+  double2* cp = pr.C + ((int64_t)i * pr.ldc + j) * V;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    double2 x = accumulate ? cp[v] : make_double2(0.0, 0.0);
+    acc[2 * v] = x.x;
+    acc[2 * v + 1] = x.y;
+  }
+  const double2* a = pr.A + (int64_t)i * pr.lda * V;
+  const double2* b = pr.B + (int64_t)j * V;
+  for (int k = 0; k < l; ++k) {
+    double2 av[V], bv[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      av[v] = __ldg(a + (int64_t)k * V + v);
+      bv[v] = __ldg(b + (int64_t)k * pr.ldb * V + v);
+    }
+    Ops::madd(acc, av, bv);
+  }
+  bool bad = false;
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    cp[v] = make_double2(acc[2 * v], acc[2 * v + 1]);
+    bad |= !finite2(acc[2 * v], acc[2 * v + 1]);
+  }
+  if (nonfinite != nullptr && bad) atomicOr(nonfinite, 1);
+}
+
+// ---------------------------------------------------------------------------
+// host-side launch helpers
+// ---------------------------------------------------------------------------
+
+inline Prob single_prob(const GemmArgs& g) {
+  return Prob{reinterpret_cast<const double2*>(g.A), reinterpret_cast<const double2*>(g.B),
+              reinterpret_cast<double2*>(g.C), g.lda, g.ldb, g.ldc};
+}
+
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB>
+cudaError_t launch_tiled(const GemmArgs& g) {
+  int64_t tiles = (int64_t)((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN) * g.batch;
+  if (tiles == 0) return cudaSuccess;
+  if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
+  gemm_tiled<Ops, BM, BN, BK, TM, TN, MINB><<<(unsigned)tiles, (BM / TM) * (BN / TN), 0,
+                                               g.stream>>>(g.probs, single_prob(g), g.m, g.n,
+                                                           g.l, g.accumulate, g.nonfinite);
+  return cudaGetLastError();
+}
+
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB>
+cudaError_t launch_lpt(const GemmArgs& g) {
+  auto kern = gemm_lpt<Ops, BM, BN, BK, TM, TN, MINB>;
+  constexpr int NT = (BM / TM) * (BN / TN);
+  int dev = 0, sms = 0, occ = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, 0);
+  if (e != cudaSuccess) return e;
+  int64_t tiles = (int64_t)((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN) * g.batch;
+  if (tiles == 0) return cudaSuccess;
+  if (tiles * 4 > 0x7fffffff) return cudaErrorInvalidValue;
+  int64_t slots = (int64_t)sms * (occ > 0 ? occ : 1);
+  // fewer units than slots: launch one CTA per unit (all quarter tiles)
+  int64_t units = tiles < slots ? 4 * tiles : slots;
+  int grid = (int)(units < slots ? units : slots);
+  kern<<<grid, NT, 0, g.stream>>>(g.probs, single_prob(g), g.batch, g.m, g.n, g.l,
+                                  g.accumulate, g.nonfinite);
+  return cudaGetLastError();
+}
+
+template <class Ops>
+cudaError_t launch_simple(const GemmArgs& g) {
+  if (g.batch > 65535) return cudaErrorInvalidValue;
+  dim3 grid((g.n + 31) / 32, (g.m + 7) / 8, g.batch), block(256);
+  gemm_simple<Ops><<<grid, block, 0, g.stream>>>(g.probs, single_prob(g), g.m, g.n, g.l,
+                                                 g.accumulate, g.nonfinite);
+  return cudaGetLastError();
+}
+
+template <class Kern>
+cudaError_t occupancy_of(Kern kern, int threads, Geometry* geo) {
+  geo->threads = threads;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&geo->ctas_per_sm, kern, threads, 0);
+}
+
+}  // namespace mpmm

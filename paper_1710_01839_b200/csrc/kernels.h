@@ -12,12 +12,20 @@ enum Algo { ALGO_SIMPLE = 0, ALGO_BLOCK = 1 };
 
 // CTA tile configurations of the blocked kernels.  The reference's block
 // size n_min selects one (tile_for_nmin); results never depend on it.
-enum Tile { TILE_16 = 0, TILE_32 = 1, TILE_64 = 2, TILE_32x64 = 3, TILE_COUNT = 4 };
+enum Tile { TILE_16 = 0, TILE_32 = 1, TILE_64 = 2, TILE_32x64 = 3, TILE_LPT = 4, TILE_COUNT = 5 };
+
+// One problem of a batched launch (all problems share m, n, l).  Same
+// layout as the 6 x int64 rows the Python side builds for Strassen leaves.
+struct GemmProblem {
+  const double* A;
+  const double* B;
+  double* C;
+  int64_t lda, ldb, ldc;
+};
 
 struct GemmArgs {
   int algo;          // ALGO_SIMPLE or ALGO_BLOCK
   int tile;          // Tile (ALGO_BLOCK)
-  int super;         // L2 super-tile edge in CTA tiles (1 = row-major raster)
   int m, n, l;
   const double* A;   // element (i,k) at A + comps*(i*lda + k)
   int64_t lda;
@@ -28,6 +36,8 @@ struct GemmArgs {
   int accumulate;    // 0: acc starts at 0 and C is overwritten; 1: C += A*B
   int* nonfinite;    // device flag, OR-ed with 1 if any output is non-finite (may be null)
   cudaStream_t stream;
+  int batch = 1;                         // number of problems
+  const GemmProblem* probs = nullptr;    // device array of `batch` problems, or null: A/B/C above
 };
 
 cudaError_t dd_gemm_launch(const GemmArgs& g);
@@ -54,6 +64,20 @@ struct EwiseArgs {
   cudaStream_t stream;
 };
 cudaError_t ewise_launch(const EwiseArgs& e);
+
+// One problem of a batched elementwise launch (all share rows x cols).
+// Layout = 14 int64 words, as built by the Python Strassen planner.
+struct EwiseProblem {
+  const double* X;
+  const double* Y;
+  const double* Z;
+  const double* W;
+  double* O;
+  int64_t ldx, ldy, ldz, ldw, ldo;
+  int64_t nops, sy, sz, sw;
+};
+cudaError_t ewise_batched_launch(int comps, int batch, int rows, int cols,
+                                 const EwiseProblem* probs, cudaStream_t stream);
 
 cudaError_t nonfinite_launch(int comps, const double* X, int64_t ldx, int rows, int cols,
                              int* flag, cudaStream_t stream);

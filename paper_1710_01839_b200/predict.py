@@ -8,13 +8,14 @@ keep their exact arithmetic here (``slice_rows_for``, ``predict_full_time``,
 depend on it.
 
 On a B200 a 2*n_min-row slice launches a few dozen CTAs against 148 SMs,
-so time does not scale with rows: it scales with *waves* of CTAs
+so time does not scale with rows: it scales with the per-SM load of CTAs
 (SURVEY.md s7 hard part 4).  ``select_block_size`` therefore predicts on
-the device with a wave model: the slice is grown to at least one full wave
-of resident CTAs (``gpu_slice_rows``), and the full time is
-``t_slice * waves(m) / waves(slice_rows)`` with
-``waves(r) = ceil(ctas(r) / (SMs * ctas_per_SM))`` from the kernel's real
-tile and occupancy (``mpmm_gemm_geometry``).
+the device with a load model built from the kernel's real tile and
+occupancy (``mpmm_gemm_geometry``): two slices, each at least one full
+complement of resident CTAs per SM (``gpu_slice_rows``), fix
+``t = alpha + beta * load(rows)`` and the fit is evaluated at the full row
+count (``fit_two_slices``).  When the slices would cover the whole
+product the product itself is timed.
 """
 
 import math
@@ -36,6 +37,8 @@ class PredictionRecord:
     full_rows: int
     slice_time_s: float
     predicted_full_s: float
+    slice2_rows: int = 0          # wave-aware mode: the second (smaller) slice
+    slice2_time_s: float = 0.0
 
     @property
     def scale_factor(self):
@@ -64,12 +67,27 @@ def predict_full_time(slice_time_s, m, n_min, slice_multiplier=DEFAULT_SLICE_MUL
 
 @dataclass(frozen=True)
 class WaveModel:
+    """Per-SM load of a launch: the kernels are FP64-pipe bound, so an SM
+    holding k CTAs of one product takes ~k times one CTA's pipe time, and
+    the launch takes as long as its most loaded SM."""
     tile_m: int
     tile_n: int
-    concurrent_ctas: int
+    ctas_per_sm: int
+    sm_count: int
+    balanced: bool = False   # persistent largest-first kernel (TILE_LPT)
+
+    @property
+    def concurrent_ctas(self):
+        return max(1, self.ctas_per_sm * self.sm_count)
 
     def ctas(self, rows, cols):
         return math.ceil(rows / self.tile_m) * math.ceil(cols / self.tile_n)
+
+    def load(self, rows, cols):
+        c = self.ctas(rows, cols)
+        if self.balanced:
+            return c / self.concurrent_ctas
+        return math.ceil(c / self.sm_count) / self.ctas_per_sm
 
     def waves(self, rows, cols):
         return max(1, math.ceil(self.ctas(rows, cols) / self.concurrent_ctas))
@@ -77,12 +95,18 @@ class WaveModel:
 
 def wave_model(comps, n_min):
     g = _cuda.gemm_geometry(comps, _cuda.ALGO_BLOCK, n_min)
-    return WaveModel(g["tile_m"], g["tile_n"], max(1, g["ctas_per_sm"] * g["sm_count"]))
+    tile, _ = _cuda.tile_for_nmin(n_min)
+    return WaveModel(g["tile_m"], g["tile_n"], max(1, g["ctas_per_sm"]), g["sm_count"],
+                     balanced=(tile == TILE_LPT))
+
+
+TILE_LPT = 4   # csrc/kernels.h enum Tile
 
 
 def gpu_slice_rows(model, n_min, m, n, slice_multiplier=DEFAULT_SLICE_MULTIPLIER):
-    """Smallest row count >= the reference's slice that fills a whole wave
-    (rounded to the tile height), clamped to m."""
+    """Smallest row count >= the reference's slice that gives every SM a
+    full complement of resident CTAs (rounded to the tile height), clamped
+    to m."""
     rows = max(slice_rows_for(n_min, m, slice_multiplier), model.tile_m)
     tiles_n = math.ceil(n / model.tile_n)
     rows_per_wave = math.ceil(model.concurrent_ctas / tiles_n) * model.tile_m
@@ -92,9 +116,23 @@ def gpu_slice_rows(model, n_min, m, n, slice_multiplier=DEFAULT_SLICE_MULTIPLIER
 
 
 def predict_full_time_waves(slice_time_s, model, slice_rows, m, n):
+    """One-point extrapolation by per-SM load."""
     if slice_time_s <= 0.0:
         raise ValueError("slice time must be positive")
-    return slice_time_s * model.waves(m, n) / model.waves(slice_rows, n)
+    return slice_time_s * model.load(m, n) / model.load(slice_rows, n)
+
+
+def fit_two_slices(model, r1, t1, r2, t2, m, n):
+    """t = alpha + beta * load(rows) through two slices; the launch and
+    ramp costs (alpha) are what make one-point scaling miss on a GPU."""
+    l1, l2, lf = model.load(r1, n), model.load(r2, n), model.load(m, n)
+    if l2 <= l1 or t2 <= 0.0 or t1 <= 0.0:
+        return predict_full_time_waves(t2 if t2 > 0 else t1, model, r2, m, n)
+    beta = (t2 - t1) / (l2 - l1)
+    if beta <= 0.0:
+        return predict_full_time_waves(t2, model, r2, m, n)
+    alpha = max(0.0, t1 - beta * l1)
+    return alpha + beta * lf
 
 
 # ---------------------------------------------------------------------------
@@ -151,12 +189,22 @@ def select_block_size(a, b, candidates, threads=1, policy=None,
     for n_min in candidates:
         if wave_aware:
             model = wave_model(a.prec.comps, n_min)
-            rows = gpu_slice_rows(model, n_min, a.rows, b.cols, slice_multiplier)
-            elapsed, rows = time_slice(a, b, n_min, threads, policy, slice_multiplier, rows)
-            predicted = predict_full_time_waves(elapsed, model, rows, a.rows, b.cols)
+            r1 = gpu_slice_rows(model, n_min, a.rows, b.cols, slice_multiplier)
+            r2 = min(a.rows, math.ceil(2 * r1 / model.tile_m) * model.tile_m)
+            if r2 >= a.rows:
+                # the slice would be the whole product: measure it (exact)
+                elapsed, rows = time_slice(a, b, n_min, threads, policy, slice_multiplier,
+                                           a.rows)
+                records.append(PredictionRecord(n_min, rows, a.rows, elapsed, elapsed))
+                continue
+            t1, _ = time_slice(a, b, n_min, threads, policy, slice_multiplier, r1)
+            t2, _ = time_slice(a, b, n_min, threads, policy, slice_multiplier, r2)
+            predicted = fit_two_slices(model, r1, t1, r2, t2, a.rows, b.cols)
+            records.append(PredictionRecord(n_min, r2, a.rows, t2, predicted,
+                                            slice2_rows=r1, slice2_time_s=t1))
         else:
             elapsed, rows = time_slice(a, b, n_min, threads, policy, slice_multiplier)
-            predicted = elapsed * (a.rows / rows)
-        records.append(PredictionRecord(n_min=n_min, slice_rows=rows, full_rows=a.rows,
-                                        slice_time_s=elapsed, predicted_full_s=predicted))
+            records.append(PredictionRecord(n_min=n_min, slice_rows=rows, full_rows=a.rows,
+                                            slice_time_s=elapsed,
+                                            predicted_full_s=elapsed * (a.rows / rows)))
     return choose_best(records), records

@@ -82,6 +82,11 @@ def broadcast_matmul(a_local, b, *, n_min=64, simple=False, group=None, src=0,
         local_gemm = cuda_local_gemm(comps, _cuda.ALGO_SIMPLE if simple else _cuda.ALGO_BLOCK,
                                      n_min)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1 and device.type == "cuda":
+        # nothing to receive: run the panels back to back on this stream
+        for p, (k0, k1) in enumerate(panels):
+            local_gemm(a_local, b[k0:k1], c_local, k0, k1, p > 0)
+        return c_local
     if device.type != "cuda":
         for p, (k0, k1) in enumerate(panels):
             if world > 1:

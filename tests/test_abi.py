@@ -43,8 +43,9 @@ def test_no_device_is_not_an_error():
 
 
 def test_tile_mapping():
-    assert _cuda.tile_for_nmin(16)[0] != _cuda.tile_for_nmin(64)[0]
-    assert _cuda.tile_for_nmin(256) == (_cuda.tile_for_nmin(64)[0], 4)
+    tiles = [_cuda.tile_for_nmin(n)[0] for n in (16, 32, 64, 128, 256)]
+    assert len(set(tiles)) == 5        # every BASELINE n_min is a distinct tile
+    assert _cuda.tile_for_nmin(1) == _cuda.tile_for_nmin(16)
     try:
         _cuda.tile_for_nmin(0)
     except ValueError:

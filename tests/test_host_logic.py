@@ -14,7 +14,7 @@ import paper_1710_01839_b200 as mp
 from paper_1710_01839_b200 import shard
 from paper_1710_01839_b200.errors import MeasurementError, ShapeError, TableFormatError
 from paper_1710_01839_b200.multiply import _split_range
-from paper_1710_01839_b200.predict import (WaveModel, gpu_slice_rows,
+from paper_1710_01839_b200.predict import (WaveModel, fit_two_slices, gpu_slice_rows,
                                            predict_full_time_waves)
 
 DD = mp.PrecisionSpec.dd()
@@ -145,13 +145,20 @@ def test_choose_best_tie_break():
 
 
 def test_wave_model():
-    wm = WaveModel(tile_m=64, tile_n=64, concurrent_ctas=148)
+    wm = WaveModel(tile_m=64, tile_n=64, ctas_per_sm=1, sm_count=148)
     assert wm.ctas(1024, 1024) == 256 and wm.waves(1024, 1024) == 2
+    assert wm.load(1024, 1024) == 2
     rows = gpu_slice_rows(wm, 64, 1024, 1024)
     assert rows % 64 == 0 and wm.ctas(rows, 1024) >= 148
     assert predict_full_time_waves(1.0, wm, rows, 1024, 1024) == \
-        pytest.approx(wm.waves(1024, 1024) / wm.waves(rows, 1024))
+        pytest.approx(wm.load(1024, 1024) / wm.load(rows, 1024))
     assert gpu_slice_rows(wm, 64, 100, 1024) == 100
+    lpt = WaveModel(64, 64, 1, 148, balanced=True)
+    assert lpt.load(1024, 1024) == pytest.approx(256 / 148)
+    # two-point fit recovers alpha + beta * load exactly
+    t = lambda r: 0.5 + 2.0 * wm.load(r, 4096)  # noqa: E731
+    assert fit_two_slices(wm, 640, t(640), 1280, t(1280), 8192, 4096) == \
+        pytest.approx(t(8192))
 
 
 # --- tuning tables (reference test_tune.py, acceptance criterion 9) --------
