@@ -39,6 +39,10 @@ extern "C" {
 
 #define MPMM_ALGO_SIMPLE 0
 #define MPMM_ALGO_BLOCK 1
+/* Opt-in faithful DD sequence (15 FP64 instructions per multiply-add)
+ * within the north_star bound 4 l u (|A||B|)_ij, u = 2^-104; NOT
+ * bit-identical to the reference.  DD only. */
+#define MPMM_ALGO_BLOCK_FAST 2
 
 int mpmm_abi_version(void);
 const char *mpmm_last_error(void);

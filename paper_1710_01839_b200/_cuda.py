@@ -62,6 +62,7 @@ _SIGNATURES = {
 
 ALGO_SIMPLE = 0
 ALGO_BLOCK = 1
+ALGO_BLOCK_FAST = 2   # opt-in faithful DD sequence (not bit-identical)
 
 
 def load():

@@ -195,7 +195,7 @@ int mpmm_gemm_geometry(int comps, int algo, int64_t n_min, int* tile_m, int* til
                        int* threads, int* ctas_per_sm, int* sm_count) {
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
   int tile = TILE_16, super = 1;
-  if (algo == MPMM_ALGO_BLOCK) {
+  if (algo != MPMM_ALGO_SIMPLE) {
     if (n_min < 1) return fail(MPMM_ERR_ARG, "block size must be positive");
     tile_for(n_min, &tile, &super);
   }
@@ -252,10 +252,13 @@ int mpmm_gemm_dev(int comps, int algo, int64_t n_min, int64_t m, int64_t l, int6
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
   if (!dims_ok(m, l, n)) return fail(MPMM_ERR_ARG, "bad shape");
   if (lda < l || ldb < n || ldc < n) return fail(MPMM_ERR_ARG, "leading dimension too small");
-  if (algo != MPMM_ALGO_SIMPLE && algo != MPMM_ALGO_BLOCK) return fail(MPMM_ERR_ARG, "bad algo");
-  if (algo == MPMM_ALGO_BLOCK && n_min < 1) return fail(MPMM_ERR_ARG, "block size must be positive");
+  if (algo != MPMM_ALGO_SIMPLE && algo != MPMM_ALGO_BLOCK && algo != MPMM_ALGO_BLOCK_FAST)
+    return fail(MPMM_ERR_ARG, "bad algo");
+  if (algo == MPMM_ALGO_BLOCK_FAST && comps != 2)
+    return fail(MPMM_ERR_ARG, "the fast accuracy mode is implemented for DD only");
+  if (algo != MPMM_ALGO_SIMPLE && n_min < 1) return fail(MPMM_ERR_ARG, "block size must be positive");
   int tile = TILE_16, super = 1;
-  if (algo == MPMM_ALGO_BLOCK) tile_for(n_min, &tile, &super);
+  if (algo != MPMM_ALGO_SIMPLE) tile_for(n_min, &tile, &super);
   GemmArgs g{algo, tile, (int)m, (int)n, (int)l, A, lda, B, ldb, C, ldc,
              accumulate ? 1 : 0, nonfinite, (cudaStream_t)stream};
   cudaError_t e = gemm(comps, g);
@@ -267,12 +270,15 @@ int mpmm_gemm_batched_dev(int comps, int algo, int64_t n_min, int64_t batch, int
                           int* nonfinite, void* stream) {
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
   if (!dims_ok(m, l, n) || batch < 0 || batch > (1 << 24)) return fail(MPMM_ERR_ARG, "bad shape");
-  if (algo != MPMM_ALGO_SIMPLE && algo != MPMM_ALGO_BLOCK) return fail(MPMM_ERR_ARG, "bad algo");
-  if (algo == MPMM_ALGO_BLOCK && n_min < 1) return fail(MPMM_ERR_ARG, "block size must be positive");
+  if (algo != MPMM_ALGO_SIMPLE && algo != MPMM_ALGO_BLOCK && algo != MPMM_ALGO_BLOCK_FAST)
+    return fail(MPMM_ERR_ARG, "bad algo");
+  if (algo == MPMM_ALGO_BLOCK_FAST && comps != 2)
+    return fail(MPMM_ERR_ARG, "the fast accuracy mode is implemented for DD only");
+  if (algo != MPMM_ALGO_SIMPLE && n_min < 1) return fail(MPMM_ERR_ARG, "block size must be positive");
   if (batch == 0) return MPMM_OK;
   if (problems == nullptr) return fail(MPMM_ERR_ARG, "null problem array");
   int tile = TILE_16, super = 1;
-  if (algo == MPMM_ALGO_BLOCK) tile_for(n_min, &tile, &super);
+  if (algo != MPMM_ALGO_SIMPLE) tile_for(n_min, &tile, &super);
   GemmArgs g{algo, tile, (int)m, (int)n, (int)l, nullptr, 0, nullptr, 0, nullptr, 0,
              accumulate ? 1 : 0, nonfinite, (cudaStream_t)stream};
   g.batch = (int)batch;

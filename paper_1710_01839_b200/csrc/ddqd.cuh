@@ -84,9 +84,42 @@ __device__ __forceinline__ void dd_madd(double& ch, double& cl, double ah, doubl
   dd_add(ch, cl, ph, pl, ch, cl);
 }
 
+// Faithful ("fast") DD multiply-add -- NOT the reference's sequence, an
+// opt-in accuracy mode that meets the north_star
+// bound |c - c_exact| <= 4 l u (|A||B|)_ij, u = 2^-104, checked against the
+// exact rational oracle (tests/test_gpu_fast.py).  15 FP64 instructions
+// (1 DMUL + 3 DFMA + 11 DADD = 18 flops) instead of the mirror's 50:
+//   p + e = ah*bh + ah*bl + al*bh to ~2^-106 (al*bl dropped, < 2^-106 |ab|),
+//   (ch, cl) += (p, e) with an exact TwoSum of the high parts and one
+//   rounded add of the low parts, renormalised every step.
+// Per step the new error is at most ~3 * 2^-106 * (|c| + |ab|), i.e. about
+// 0.2 of the bound's per-step budget 2^-102 (|A||B|)_ij.
+__device__ __forceinline__ void dd_madd_fast(double& ch, double& cl, double ah, double al,
+                                             double bh, double bl) {
+  double p = ah * bh;
+  double e = __fma_rn(ah, bh, -p);
+  e = __fma_rn(ah, bl, e);
+  e = __fma_rn(al, bh, e);
+  double t;
+  double s = two_sum(ch, p, t);
+  t = t + (cl + e);
+  ch = quick_two_sum(s, t, cl);
+}
+
 // ---------------------------------------------------------------------------
 // quad-double
 // ---------------------------------------------------------------------------
+
+// x != 0.0 with IEEE semantics (-0.0 is zero, NaN is not), tested on the
+// bit pattern so the check runs on the integer pipe instead of issuing a
+// DSETP on the FP64 pipe the arithmetic is bound by.
+// (The 64-bit shift form gets pattern-matched back into a DSETP by the
+// compiler; splitting the register pair in PTX keeps it on the ALU.)
+__device__ __forceinline__ bool nonzero(double x) {
+  unsigned lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(x));
+  return ((hi & 0x7fffffffu) | lo) != 0u;
+}
 
 // ddqd.py:140-172 _renorm5 == _kernels.pyx:237-271, branch-free: the
 // data-dependent "if e != 0" emission becomes predicated selects.  In the
@@ -108,7 +141,7 @@ __device__ __forceinline__ void renorm5(double x0, double x1, double x2, double 
     double v = rest[idx];
     double sn = acc + v;
     double e = v - (sn - acc);
-    bool emit = (k < 3) && (e != 0.0);
+    bool emit = (k < 3) && nonzero(e);
     if (emit) {
       o0 = (k == 0) ? sn : o0;
       o1 = (k == 1) ? sn : o1;
@@ -129,14 +162,29 @@ __device__ __forceinline__ void renorm5(double x0, double x1, double x2, double 
 
 // ddqd.py:175-193 _compress4 for N terms that are ALL nonzero (the zero
 // filter is then the identity).  Fully unrolled: registers only.
+//
+// The four error-free vector passes are issued as a wavefront: pass p's
+// step i runs in "round" i + 2p.  Step (p, i) needs v[i] from pass p-1's
+// step i+1 (round i+2p-1) and pass p's own running sum from step i-1
+// (round i+2p-1), and it overwrites v[i-1], which pass p-1 last read in
+// round i+2p-3 and pass p+1 first reads in round i+2p+1.  Every TwoSum
+// therefore sees exactly the operands of the sequential loop
+// (ddqd.py:181-186) -- same bits -- while each round holds up to four
+// independent TwoSums, so in-order issue is not stalled by the pass chains.
 template <int N>
 __device__ __forceinline__ void compress4_dense(double (&v)[N], double out[4]) {
+  double s[4];
 #pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    double s = v[0];
+  for (int d = 1; d <= (N - 1) + 6; ++d) {
 #pragma unroll
-    for (int i = 1; i < N; ++i) s = two_sum(s, v[i], v[i - 1]);
-    v[N - 1] = s;
+    for (int p = 0; p < 4; ++p) {
+      const int i = d - 2 * p;
+      if (i >= 1 && i <= N - 1) {
+        if (i == 1) s[p] = v[0];
+        s[p] = two_sum(s[p], v[i], v[i - 1]);
+        if (i == N - 1) v[N - 1] = s[p];
+      }
+    }
   }
   if constexpr (N <= 4) {
     double w[4] = {0.0, 0.0, 0.0, 0.0};
@@ -213,7 +261,7 @@ __device__ __forceinline__ void qd_mul_add(double cc[4], const double x[4], cons
   t[22] = x[3] * y[1];
   bool dense = true;
 #pragma unroll
-  for (int i = 0; i < 23; ++i) dense &= (t[i] != 0.0);
+  for (int i = 0; i < 23; ++i) dense &= nonzero(t[i]);
   double prod[4];
   if (dense) {
     compress4_dense<23>(t, prod);
@@ -221,9 +269,9 @@ __device__ __forceinline__ void qd_mul_add(double cc[4], const double x[4], cons
     compress4_slow<23>(t, prod);
   }
   double add[8] = {cc[0], prod[0], cc[1], prod[1], cc[2], prod[2], cc[3], prod[3]};
-  bool cz = (cc[0] == 0.0) & (cc[1] == 0.0) & (cc[2] == 0.0) & (cc[3] == 0.0);
-  bool pd = (prod[0] != 0.0) & (prod[1] != 0.0) & (prod[2] != 0.0) & (prod[3] != 0.0);
-  bool cd = (cc[0] != 0.0) & (cc[1] != 0.0) & (cc[2] != 0.0) & (cc[3] != 0.0);
+  bool cz = !nonzero(cc[0]) & !nonzero(cc[1]) & !nonzero(cc[2]) & !nonzero(cc[3]);
+  bool pd = nonzero(prod[0]) & nonzero(prod[1]) & nonzero(prod[2]) & nonzero(prod[3]);
+  bool cd = nonzero(cc[0]) & nonzero(cc[1]) & nonzero(cc[2]) & nonzero(cc[3]);
   if (cd & pd) {
     compress4_dense<8>(add, cc);
   } else if (cz & pd) {
@@ -240,7 +288,7 @@ __device__ __forceinline__ void qd_add(const double x[4], const double y[4], dou
   double add[8] = {x[0], y[0], x[1], y[1], x[2], y[2], x[3], y[3]};
   bool dense = true;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) dense &= (add[i] != 0.0);
+  for (int i = 0; i < 8; ++i) dense &= nonzero(add[i]);
   if (dense) {
     compress4_dense<8>(add, out);
   } else {

@@ -38,6 +38,15 @@ struct DDOps {
   }
 };
 
+// The opt-in faithful DD sequence (dd_madd_fast); same data layout.
+struct DDFastOps {
+  static constexpr int V = 1;
+  static constexpr int NACC = 2;
+  __device__ __forceinline__ static void madd(double* acc, const double2* a, const double2* b) {
+    dd_madd_fast(acc[0], acc[1], a[0].x, a[0].y, b[0].x, b[0].y);
+  }
+};
+
 struct QDOps {
   static constexpr int V = 2;
   static constexpr int NACC = 4;

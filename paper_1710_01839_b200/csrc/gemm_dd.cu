@@ -2,6 +2,9 @@
 //
 // DD element = one double2 {hi, lo}; each multiply-add is the reference's
 // dd_add(c, dd_mul(a, b)) (_kernels.pyx:135-184): 4 DMUL + 3 DFMA + 43 DADD.
+// ALGO_BLOCK_FAST runs the same tiles with the opt-in faithful sequence
+// dd_madd_fast (15 FP64 instructions, within the north_star bound, NOT
+// bit-identical to the reference).
 // Tile configurations (n_min -> tile: capi.cu tile_for):
 //   TILE_16    16x16 CTA tile, 1x1 per thread, 256 threads, 4 CTAs/SM
 //   TILE_32    32x32, 2x2, 256 threads, 2 CTAs/SM
@@ -12,20 +15,41 @@
 
 namespace mpmm {
 
-cudaError_t dd_gemm_launch(const GemmArgs& g) {
-  if (g.m <= 0 || g.n <= 0 || g.batch <= 0) return cudaSuccess;
-  if (g.algo == ALGO_SIMPLE) return launch_simple<DDOps>(g);
+template <class Ops>
+static cudaError_t dd_blocked(const GemmArgs& g) {
   switch (g.tile) {
-    case TILE_16: return launch_tiled<DDOps, 16, 16, 16, 1, 1, 4>(g);
-    case TILE_32: return launch_tiled<DDOps, 32, 32, 8, 2, 2, 2>(g);
-    case TILE_64: return launch_tiled<DDOps, 64, 64, 8, 4, 4, 1>(g);
-    case TILE_32x64: return launch_tiled<DDOps, 32, 64, 8, 2, 2, 1>(g);
-    case TILE_LPT: return launch_lpt<DDOps, 64, 64, 8, 4, 4, 1>(g);
+    case TILE_16: return launch_tiled<Ops, 16, 16, 16, 1, 1, 4>(g);
+    case TILE_32: return launch_tiled<Ops, 32, 32, 8, 2, 2, 2>(g);
+    case TILE_64: return launch_tiled<Ops, 64, 64, 8, 4, 4, 1>(g);
+    case TILE_32x64: return launch_tiled<Ops, 32, 64, 8, 2, 2, 1>(g);
+    case TILE_LPT: return launch_lpt<Ops, 64, 64, 8, 4, 4, 1>(g);
     default: return cudaErrorInvalidValue;
   }
 }
 
+cudaError_t dd_gemm_launch(const GemmArgs& g) {
+  if (g.m <= 0 || g.n <= 0 || g.batch <= 0) return cudaSuccess;
+  if (g.algo == ALGO_SIMPLE) return launch_simple<DDOps>(g);
+  if (g.algo == ALGO_BLOCK_FAST) return dd_blocked<DDFastOps>(g);
+  return dd_blocked<DDOps>(g);
+}
+
 cudaError_t dd_gemm_geometry(int algo, int tile, Geometry* geo) {
+  if (algo == ALGO_BLOCK_FAST) {
+    switch (tile) {
+      case TILE_16: geo->bm = 16, geo->bn = 16;
+        return occupancy_of(gemm_tiled<DDFastOps, 16, 16, 16, 1, 1, 4>, 256, geo);
+      case TILE_32: geo->bm = 32, geo->bn = 32;
+        return occupancy_of(gemm_tiled<DDFastOps, 32, 32, 8, 2, 2, 2>, 256, geo);
+      case TILE_64: geo->bm = 64, geo->bn = 64;
+        return occupancy_of(gemm_tiled<DDFastOps, 64, 64, 8, 4, 4, 1>, 256, geo);
+      case TILE_32x64: geo->bm = 32, geo->bn = 64;
+        return occupancy_of(gemm_tiled<DDFastOps, 32, 64, 8, 2, 2, 1>, 512, geo);
+      case TILE_LPT: geo->bm = 64, geo->bn = 64;
+        return occupancy_of(gemm_lpt<DDFastOps, 64, 64, 8, 4, 4, 1>, 256, geo);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   if (algo == ALGO_SIMPLE) {
     geo->bm = 8, geo->bn = 32;
     return occupancy_of(gemm_simple<DDOps>, 256, geo);

@@ -17,11 +17,12 @@ namespace mpmm {
 cudaError_t qd_gemm_launch(const GemmArgs& g) {
   if (g.m <= 0 || g.n <= 0 || g.batch <= 0) return cudaSuccess;
   if (g.algo == ALGO_SIMPLE) return launch_simple<QDOps>(g);
+  if (g.algo != ALGO_BLOCK) return cudaErrorNotSupported;
   switch (g.tile) {
     case TILE_16: return launch_tiled<QDOps, 16, 16, 8, 1, 1, 2>(g);
     case TILE_32: return launch_tiled<QDOps, 16, 32, 8, 1, 2, 1>(g);
     case TILE_64: return launch_tiled<QDOps, 32, 32, 8, 2, 2, 1>(g);
-    case TILE_32x64: return launch_tiled<QDOps, 8, 32, 8, 1, 1, 4>(g);
+    case TILE_32x64: return launch_tiled<QDOps, 8, 32, 8, 1, 1, 2>(g);
     case TILE_LPT: return launch_lpt<QDOps, 32, 32, 8, 2, 2, 1>(g);
     default: return cudaErrorInvalidValue;
   }
@@ -40,7 +41,7 @@ cudaError_t qd_gemm_geometry(int algo, int tile, Geometry* geo) {
     case TILE_64: geo->bm = 32, geo->bn = 32;
       return occupancy_of(gemm_tiled<QDOps, 32, 32, 8, 2, 2, 1>, 256, geo);
     case TILE_32x64: geo->bm = 8, geo->bn = 32;
-      return occupancy_of(gemm_tiled<QDOps, 8, 32, 8, 1, 1, 4>, 256, geo);
+      return occupancy_of(gemm_tiled<QDOps, 8, 32, 8, 1, 1, 2>, 256, geo);
     case TILE_LPT: geo->bm = 32, geo->bn = 32;
       return occupancy_of(gemm_lpt<QDOps, 32, 32, 8, 2, 2, 1>, 256, geo);
     default: return cudaErrorInvalidValue;

@@ -8,7 +8,7 @@
 
 namespace mpmm {
 
-enum Algo { ALGO_SIMPLE = 0, ALGO_BLOCK = 1 };
+enum Algo { ALGO_SIMPLE = 0, ALGO_BLOCK = 1, ALGO_BLOCK_FAST = 2 };
 
 // CTA tile configurations of the blocked kernels.  The reference's block
 // size n_min selects one (tile_for_nmin); results never depend on it.

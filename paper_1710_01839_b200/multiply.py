@@ -258,13 +258,32 @@ def matmul_simple(a, b, threads=1):
     return _result(_check_finite(c, flag), home)
 
 
-def matmul_block(a, b, n_min, threads=1):
+MODES = ("exact", "fast")
+
+
+def matmul_block(a, b, n_min, threads=1, *, mode="exact"):
     """Blocked product with block size ``n_min``; bit-identical to
-    :func:`matmul_simple` at every block size (multiply.py:171-182)."""
+    :func:`matmul_simple` at every block size (multiply.py:171-182).
+
+    ``mode="fast"`` (DD only) opts into the faithful 15-instruction DD
+    sequence: within the north_star bound 4 l u (|A||B|)_ij (u = 2^-104) but
+    NOT bit-identical to the reference."""
     _check_pair(a, b, threads)
     if n_min < 1:
         raise ValueError("block size must be positive")
+    if mode not in MODES:
+        raise ValueError(f"unknown mode {mode!r}; expected one of {MODES}")
+    if mode == "fast" and a.prec.kind is not Kind.DD:
+        raise ValueError("the fast accuracy mode is implemented for DD only")
     da, db, home = _operands(a, b)
+    if mode == "fast":
+        if not backend.is_cuda():
+            raise ValueError("the fast accuracy mode runs on the cuda backend only")
+        c = DenseMatrix.empty(a.rows, b.cols, a.prec, da.device)
+        flag = _flag(da.device)
+        _gemm_view(_cuda.ALGO_BLOCK_FAST, n_min, _View.of(da.data), _View.of(db.data),
+                   _View.of(c.data), False, flag.data_ptr())
+        return _result(_check_finite(c, flag), home)
     if backend.is_cuda():
         # zeros + accumulate-into == accumulate from a zero register
         # accumulator: skip the memset and start from zero in the kernel
