@@ -46,12 +46,17 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--prec", default="dd", choices=["dd", "qd"])
-    p.add_argument("--n", type=int, default=1024)
+    p.add_argument("--size", type=int, default=1024, help="m = l = n per rank")
     p.add_argument("--nmin", type=int, default=0,
                    help="block size; 0 = let the GPU predictor pick from 16..256")
     p.add_argument("--panel", type=int, default=0, help="k-panel rows for the B broadcast")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=8.0)
+    p.add_argument("--dist-backend", default="nccl",
+                   help="torch.distributed backend for N>1 (nccl; gloo only to test the "
+                        "multi-rank logic with all ranks on one GPU)")
+    p.add_argument("--same-device", action="store_true",
+                   help="put every rank on cuda:0 (multi-rank logic test on one GPU, gloo)")
     return p.parse_args()
 
 
@@ -157,7 +162,7 @@ def run_reference(args, rank, world):
     per_step = max(1.0, min(args.cpu_seconds, 60.0 / (steps + args.warmup)))
     vals = []
     for i in range(args.warmup + steps):
-        v, cores, kind, sample, _ = cpu_reference_run(args.prec, args.n, args.nmin, per_step)
+        v, cores, kind, sample, _ = cpu_reference_run(args.prec, args.size, args.nmin, per_step)
         if i >= args.warmup:
             vals.append(v)
     value = statistics.median(vals)
@@ -176,13 +181,13 @@ def run_reference(args, rank, world):
 
 
 def metric_name(args):
-    return f"{args.prec.upper()} GEMM 2mnl/s (blocked, m=l=n={args.n})"
+    return f"{args.prec.upper()} GEMM 2mnl/s (blocked, m=l=n={args.size})"
 
 
 def workload_config(args, world):
     return {"workload": f"BASELINE configs[1]: {args.prec.upper()} blocked GEMM "
-                        f"m=l=n={args.n}, n_min={args.nmin}, seeded uniform inputs (seed 0)",
-            "prec": args.prec, "m_per_rank": args.n, "l": args.n, "n": args.n,
+                        f"m=l=n={args.size}, n_min={args.nmin}, seeded uniform inputs (seed 0)",
+            "prec": args.prec, "m_per_rank": args.size, "l": args.size, "n": args.size,
             "n_min": args.nmin, "parallelism": f"row-shard x{world}, B NCCL broadcast",
             "l2": "flushed between steps (256 MiB write), inputs 16 MiB/matrix"}
 
@@ -237,7 +242,7 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     prec = mp.PrecisionSpec.parse(args.prec)
     comps = prec.comps
-    n = args.n
+    n = args.size
     F = F_DD if args.prec == "dd" else F_QD
 
     # per-rank inputs: rank r owns rows [r*n, (r+1)*n) of A; B from rank 0
@@ -400,7 +405,7 @@ def run_ours(args, rank, world, local_rank):
             "value": 2.0 * float(n) ** 3 * world / fast_s, "unit": "2mnl/s",
             "kernel_ms": fast_s * 1e3,
             "roofline_frac": 18 * float(n) ** 3 / fast_s / 1e12 / peak["dfma"]}
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.sizeo_cpu_baseline:
         v, cores, kind, sample, _ = cpu_reference_run(args.prec, n, args.nmin, args.cpu_seconds)
         line["cpu_baseline"] = {"value": v, "unit": "2mnl/s", "cores": cores, "kind": kind,
                                 "sample": sample}
@@ -415,11 +420,16 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if args.same_device:
+        local_rank = 0
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(args.dist_backend)
     try:
         run_ours(args, rank, world, local_rank)
     finally:
