@@ -46,6 +46,10 @@ extern "C" {
 
 int mpmm_abi_version(void);
 const char *mpmm_last_error(void);
+/* Select the device subsequent calls on this host thread use (the library
+ * links its own CUDA runtime, so a caller's cudaSetDevice in another
+ * runtime instance is mirrored here; the Python binding does it). */
+int mpmm_set_device(int device);
 /* Number of visible CUDA devices (0 without a GPU; never an error). */
 int mpmm_device_count(int *count);
 /* The CTA tile a reference block size n_min selects. */
@@ -86,6 +90,15 @@ int mpmm_qd_ewise_add(const double *x, const double *y, double *out, int64_t row
                       int64_t cols, int64_t i0, int64_t i1);
 int mpmm_qd_ewise_sub(const double *x, const double *y, double *out, int64_t rows,
                       int64_t cols, int64_t i0, int64_t i1);
+
+/* Whole product on HOST buffers: c (m x n) = a*b (accumulate=0) or
+ * c += a*b (accumulate=1), computed on the current device.  The H2D copies
+ * of a and b are split into k-panels on a copy stream so the GEMM of one
+ * panel overlaps the copy of the next (page-locked host memory makes the
+ * copies asynchronous).  nonfinite (host int, may be NULL) receives 1 when
+ * an output component is not finite (multiply.py:124-127). */
+int mpmm_gemm_host(int comps, int algo, int64_t n_min, int64_t m, int64_t l, int64_t n,
+                   const double *a, const double *b, double *c, int accumulate, int *nonfinite);
 
 /* ---------------------------------------------------------------------------
  * Device-resident entry points: all matrix pointers are DEVICE pointers on

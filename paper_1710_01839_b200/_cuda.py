@@ -13,6 +13,7 @@ point raises :class:`~paper_1710_01839_b200.errors.DeviceError`.
 
 import ctypes
 import os
+import threading
 
 import numpy as np
 
@@ -35,6 +36,7 @@ _VP = ctypes.c_void_p
 _SIGNATURES = {
     "mpmm_abi_version": [],
     "mpmm_last_error": [],
+    "mpmm_set_device": [_INT],
     "mpmm_device_count": [ctypes.POINTER(_INT)],
     "mpmm_tile_for_nmin": [_I64, ctypes.POINTER(_INT), ctypes.POINTER(_INT)],
     "mpmm_gemm_geometry": [_INT, _INT, _I64] + [ctypes.POINTER(_INT)] * 5,
@@ -46,6 +48,8 @@ _SIGNATURES = {
     "mpmm_dd_ewise_sub": [_D, _D, _D, _I64, _I64, _I64, _I64],
     "mpmm_qd_ewise_add": [_D, _D, _D, _I64, _I64, _I64, _I64],
     "mpmm_qd_ewise_sub": [_D, _D, _D, _I64, _I64, _I64, _I64],
+    "mpmm_gemm_host": [_INT, _INT, _I64, _I64, _I64, _I64, _D, _D, _D, _INT,
+                       ctypes.POINTER(_INT)],
     "mpmm_gemm_dev": [_INT, _INT, _I64, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64,
                       _INT, _VP, _VP],
     "mpmm_gemm_batched_dev": [_INT, _INT, _I64, _I64, _I64, _I64, _I64, _VP, _INT, _VP, _VP],
@@ -101,6 +105,19 @@ def exported_symbols():
     return list(_SIGNATURES)
 
 
+_tls = threading.local()
+
+
+def sync_device():
+    """Mirror torch's current device into the library's runtime (once per
+    change, per host thread)."""
+    import torch
+    dev = torch.cuda.current_device()
+    if getattr(_tls, "device", None) != dev:
+        check(load().mpmm_set_device(dev))
+        _tls.device = dev
+
+
 def check(rc):
     if rc != 0:
         msg = load().mpmm_last_error().decode(errors="replace")
@@ -143,18 +160,21 @@ def _arr(x, comps):
 
 
 def _simple(comps, fn, a, b, c, i0, i1):
+    sync_device()
     m, l = a.shape[0], a.shape[1]
     n = b.shape[1]
     check(fn(_arr(a, comps), _arr(b, comps), _arr(c, comps), m, l, n, i0, i1))
 
 
 def _cells(comps, fn, a, b, c, n_min, cell0, cell1):
+    sync_device()
     m, l = a.shape[0], a.shape[1]
     n = b.shape[1]
     check(fn(_arr(a, comps), _arr(b, comps), _arr(c, comps), m, l, n, n_min, cell0, cell1))
 
 
 def _ew(comps, fn, x, y, out, i0, i1):
+    sync_device()
     check(fn(_arr(x, comps), _arr(y, comps), _arr(out, comps), x.shape[0], x.shape[1], i0, i1))
 
 
@@ -198,8 +218,20 @@ def qd_ewise_sub(x, y, out, i0, i1):
 # device-resident entry points (raw pointers, element leading dimensions)
 # ---------------------------------------------------------------------------
 
+def gemm_host(comps, algo, n_min, a, b, c, accumulate=False):
+    """c = a*b (or c += a*b) for host arrays through the pipelined C-ABI
+    entry; returns True when every output component is finite."""
+    sync_device()
+    flag = ctypes.c_int(0)
+    check(load().mpmm_gemm_host(comps, algo, n_min, a.shape[0], a.shape[1], b.shape[1],
+                                _arr(a, comps), _arr(b, comps), _arr(c, comps),
+                                1 if accumulate else 0, ctypes.byref(flag)))
+    return flag.value == 0
+
+
 def gemm_dev(comps, algo, n_min, m, l, n, A, lda, B, ldb, C, ldc, accumulate,
              nonfinite=None, stream=None):
+    sync_device()
     check(load().mpmm_gemm_dev(comps, algo, n_min, m, l, n, A, lda, B, ldb, C, ldc,
                                1 if accumulate else 0, nonfinite, stream))
 
@@ -207,16 +239,19 @@ def gemm_dev(comps, algo, n_min, m, l, n, A, lda, B, ldb, C, ldc, accumulate,
 def gemm_batched_dev(comps, algo, n_min, batch, m, l, n, problems, accumulate, nonfinite=None,
                      stream=None):
     """``problems``: device pointer to ``batch`` x 6 int64 {A, B, C, lda, ldb, ldc}."""
+    sync_device()
     check(load().mpmm_gemm_batched_dev(comps, algo, n_min, batch, m, l, n, problems,
                                        1 if accumulate else 0, nonfinite, stream))
 
 
 def ewise_batched_dev(comps, batch, rows, cols, problems, stream=None):
     """``problems``: device pointer to ``batch`` x 14 int64 (see mpmm_cuda.h)."""
+    sync_device()
     check(load().mpmm_ewise_batched_dev(comps, batch, rows, cols, problems, stream))
 
 
 def block_cells_dev(comps, n_min, cell0, cell1, m, l, n, A, lda, B, ldb, C, ldc, stream=None):
+    sync_device()
     check(load().mpmm_block_cells_dev(comps, n_min, cell0, cell1, m, l, n, A, lda, B, ldb,
                                       C, ldc, stream))
 
@@ -224,15 +259,18 @@ def block_cells_dev(comps, n_min, cell0, cell1, m, l, n, A, lda, B, ldb, C, ldc,
 def ewise_dev(comps, rows, cols, O, ldo, X, ldx, Y, ldy, sy, Z=None, ldz=0, sz=1, W=None,
               ldw=0, sw=1, stream=None):
     nops = 1 + (Z is not None) + (W is not None)
+    sync_device()
     check(load().mpmm_ewise_dev(comps, nops, rows, cols, X, ldx, Y, ldy, sy, Z, ldz, sz,
                                 W, ldw, sw, O, ldo, stream))
 
 
 def nonfinite_dev(comps, rows, cols, X, ldx, flag, stream=None):
+    sync_device()
     check(load().mpmm_nonfinite_dev(comps, rows, cols, X, ldx, flag, stream))
 
 
 def fp64_burn_dev(op, blocks, threads, iters, scratch, stream=None):
+    sync_device()
     check(load().mpmm_fp64_burn_dev(op, blocks, threads, iters, scratch, stream))
 
 

@@ -5,6 +5,7 @@
 // argument meaning on host pointers, and device-resident whole-GEMM /
 // elementwise entry points serve the multiply/predict/tune layers.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -59,15 +60,52 @@ cudaError_t gemm(int comps, const GemmArgs& g) {
   return comps == 2 ? dd_gemm_launch(g) : qd_gemm_launch(g);
 }
 
-// Device buffers for the host-pointer protocol; freed on scope exit.
+// ---------------------------------------------------------------------------
+// host-pointer protocol plumbing: per-thread streams, stream-ordered buffers
+// ---------------------------------------------------------------------------
+
+// One copy stream and one compute stream per (host thread, device), created
+// on first use; the reference calls its kernels from a thread pool
+// (multiply.py:99-112), so per-thread streams keep concurrent calls apart.
+struct HostStreams {
+  int device = -1;
+  cudaStream_t copy = nullptr, comp = nullptr;
+};
+thread_local HostStreams g_hs;
+
+cudaError_t host_streams(HostStreams** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (g_hs.device != dev) {
+    g_hs.device = dev;
+    if ((e = cudaStreamCreateWithFlags(&g_hs.copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&g_hs.comp, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  }
+  *out = &g_hs;
+  return cudaSuccess;
+}
+
+// Stream-ordered device buffer (memory-pool backed: no device-wide sync).
 struct DevBuf {
   double* p = nullptr;
+  cudaStream_t s = nullptr;
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, s);
   }
-  cudaError_t alloc(size_t doubles) {
-    return cudaMalloc(&p, doubles ? doubles * sizeof(double) : sizeof(double));
+  cudaError_t alloc(size_t doubles, cudaStream_t stream) {
+    s = stream;
+    return cudaMallocAsync(reinterpret_cast<void**>(&p),
+                           doubles ? doubles * sizeof(double) : sizeof(double), stream);
   }
+};
+
+struct Event {
+  cudaEvent_t e = nullptr;
+  ~Event() {
+    if (e) cudaEventDestroy(e);
+  }
+  cudaError_t make() { return cudaEventCreateWithFlags(&e, cudaEventDisableTiming); }
 };
 
 int block_cells_impl(int comps, int64_t n_min, int64_t cell0, int64_t cell1, int64_t m,
@@ -101,24 +139,105 @@ int block_cells_impl(int comps, int64_t n_min, int64_t cell0, int64_t cell1, int
   return rect(ib1 * n_min, (ib1 + 1) * n_min, 0, (jb1 + 1) * n_min);
 }
 
+// rows x n block of C (host, row pitch n) = A rows (host, pitch l) * B
+// (host, l x n), through the device, with the H2D of A and B split into
+// k-panels on the copy stream so the GEMM of panel p overlaps the copy of
+// panel p+1.  Each element's accumulator is carried through C between
+// panels (bit-identical to one pass).  accumulate_c: start from C's value
+// (block_cells semantics) instead of zero (simple_rows semantics).
+int host_rows_gemm(int comps, int algo, int64_t n_min, int64_t rows, int64_t l, int64_t n,
+                   const double* a_rows, const double* b, double* c_rows, bool accumulate_c,
+                   int* nonfinite_host = nullptr) {
+  if (nonfinite_host) *nonfinite_host = 0;
+  if (rows == 0 || n == 0) return MPMM_OK;
+  HostStreams* hs = nullptr;
+  CU(host_streams(&hs));
+  const size_t el = comps * sizeof(double);
+  int* dflag = nullptr;
+  if (nonfinite_host) {
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&dflag), sizeof(int), hs->comp));
+    CU(cudaMemsetAsync(dflag, 0, sizeof(int), hs->comp));
+  }
+  DevBuf dA, dB, dC;
+  CU(dA.alloc(rows * l * comps, hs->comp));
+  CU(dB.alloc(l * n * comps, hs->comp));
+  CU(dC.alloc(rows * n * comps, hs->comp));
+  Event ready;                       // buffers allocated (stream-ordered on comp)
+  CU(ready.make());
+  CU(cudaEventRecord(ready.e, hs->comp));
+  CU(cudaStreamWaitEvent(hs->copy, ready.e, 0));
+  Event cin;
+  CU(cin.make());
+  if (accumulate_c) {
+    CU(cudaMemcpyAsync(dC.p, c_rows, rows * n * el, cudaMemcpyHostToDevice, hs->copy));
+    CU(cudaEventRecord(cin.e, hs->copy));
+    CU(cudaStreamWaitEvent(hs->comp, cin.e, 0));
+  }
+  // up to 8 k-panels of >= 128: the first panel's copy is the only
+  // exposed H2D; later copies hide under the previous panel's GEMM
+  int64_t want = l >= 1024 ? 8 : (l >= 256 ? l / 128 : 1);
+  if (const char* env = std::getenv("MPMM_HOST_PANELS")) {   // tuning knob
+    int64_t v = std::atoll(env);
+    if (v >= 1 && v <= 8) want = v < l ? v : (l > 0 ? l : 1);
+  }
+  const int64_t step = (l + want - 1) / want;
+  int tile = TILE_16, super = 1;
+  if (algo != ALGO_SIMPLE) tile_for(n_min, &tile, &super);
+  Event ev[8];
+  int p = 0;
+  const int64_t split = rows >= 256 ? ((rows / 2 + 63) / 64) * 64 : rows;  // D2H overlap
+  Event top;
+  CU(top.make());
+  for (int64_t k0 = 0; k0 < l || (l == 0 && p == 0); k0 += step, ++p) {
+    const int64_t k1 = (k0 + step < l) ? k0 + step : l;
+    if (l > 0) {
+      CU(cudaMemcpy2DAsync(dA.p + k0 * comps, l * el, a_rows + k0 * comps, l * el,
+                           (k1 - k0) * el, rows, cudaMemcpyHostToDevice, hs->copy));
+      CU(cudaMemcpyAsync(dB.p + k0 * n * comps, b + k0 * n * comps, (k1 - k0) * n * el,
+                         cudaMemcpyHostToDevice, hs->copy));
+    }
+    CU(ev[p].make());
+    CU(cudaEventRecord(ev[p].e, hs->copy));
+    CU(cudaStreamWaitEvent(hs->comp, ev[p].e, 0));
+    const bool last = (k1 >= l);
+    const int acc = (accumulate_c || p > 0) ? 1 : 0;
+    // the finite check only needs the final values: flag the last panel.
+    // The last panel runs in two row halves so the top half's D2H (on the
+    // copy stream) overlaps the bottom half's GEMM.
+    const int64_t parts[2][2] = {{0, last ? split : rows}, {last ? split : rows, rows}};
+    for (int h = 0; h < 2; ++h) {
+      const int64_t q0 = parts[h][0], q1 = parts[h][1];
+      if (q1 <= q0) continue;
+      GemmArgs g{algo, tile, (int)(q1 - q0), (int)n, (int)(k1 - k0),
+                 dA.p + (q0 * l + k0) * comps, l, dB.p + k0 * n * comps, n,
+                 dC.p + q0 * n * comps, n, acc, last ? dflag : nullptr, hs->comp};
+      CU(gemm(comps, g));
+      if (last && h == 0 && split < rows) {
+        CU(cudaEventRecord(top.e, hs->comp));
+        CU(cudaStreamWaitEvent(hs->copy, top.e, 0));
+        CU(cudaMemcpyAsync(c_rows, dC.p, split * n * el, cudaMemcpyDeviceToHost, hs->copy));
+      }
+    }
+    if (l == 0) break;
+  }
+  const int64_t rest0 = (split < rows && l > 0) ? split : 0;
+  CU(cudaMemcpyAsync(c_rows + rest0 * n * comps, dC.p + rest0 * n * comps,
+                     (rows - rest0) * n * el, cudaMemcpyDeviceToHost, hs->comp));
+  CU(cudaStreamSynchronize(hs->copy));
+  if (dflag) {
+    CU(cudaMemcpyAsync(nonfinite_host, dflag, sizeof(int), cudaMemcpyDeviceToHost, hs->comp));
+    CU(cudaFreeAsync(dflag, hs->comp));
+  }
+  CU(cudaStreamSynchronize(hs->comp));
+  return MPMM_OK;
+}
+
 int host_simple_rows(int comps, const double* a, const double* b, double* c, int64_t m,
                      int64_t l, int64_t n, int64_t i0, int64_t i1) {
   if (!dims_ok(m, l, n) || i0 < 0 || i1 > m) return fail(MPMM_ERR_ARG, "bad shape or row range");
   if (i1 <= i0 || n == 0) return MPMM_OK;
-  const int64_t rows = i1 - i0;
-  DevBuf dA, dB, dC;
-  CU(dA.alloc(rows * l * comps));
-  CU(dB.alloc(l * n * comps));
-  CU(dC.alloc(rows * n * comps));
-  CU(cudaMemcpy(dA.p, a + i0 * l * comps, rows * l * comps * sizeof(double),
-                cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(dB.p, b, l * n * comps * sizeof(double), cudaMemcpyHostToDevice));
-  GemmArgs g{ALGO_SIMPLE, TILE_16, (int)rows, (int)n, (int)l, dA.p, l, dB.p, n, dC.p, n,
-             0, nullptr, 0};
-  CU(gemm(comps, g));
-  CU(cudaMemcpy(c + i0 * n * comps, dC.p, rows * n * comps * sizeof(double),
-                cudaMemcpyDeviceToHost));
-  return MPMM_OK;
+  return host_rows_gemm(comps, ALGO_SIMPLE, 0, i1 - i0, l, n, a + i0 * l * comps, b,
+                        c + i0 * n * comps, false);
 }
 
 int host_block_cells(int comps, const double* a, const double* b, double* c, int64_t m,
@@ -133,20 +252,27 @@ int host_block_cells(int comps, const double* a, const double* b, double* c, int
   const int64_t r0 = ib0 * n_min;
   const int64_t r1 = (ib1 + 1) * n_min < m ? (ib1 + 1) * n_min : m;
   const int64_t rows = r1 - r0;
+  const int64_t ncells = nbc * ((m + n_min - 1) / n_min);
+  if (cell0 % nbc == 0 && (cell1 % nbc == 0 || cell1 == ncells)) {
+    // whole block rows: one pipelined pass over rows [r0, r1)
+    return host_rows_gemm(comps, ALGO_BLOCK, n_min, rows, l, n, a + r0 * l * comps, b,
+                          c + r0 * n * comps, true);
+  }
+  HostStreams* hs = nullptr;
+  CU(host_streams(&hs));
   DevBuf dA, dB, dC;
-  CU(dA.alloc(rows * l * comps));
-  CU(dB.alloc(l * n * comps));
-  CU(dC.alloc(rows * n * comps));
-  CU(cudaMemcpy(dA.p, a + r0 * l * comps, rows * l * comps * sizeof(double),
-                cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(dB.p, b, l * n * comps * sizeof(double), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(dC.p, c + r0 * n * comps, rows * n * comps * sizeof(double),
-                cudaMemcpyHostToDevice));
+  CU(dA.alloc(rows * l * comps, hs->comp));
+  CU(dB.alloc(l * n * comps, hs->comp));
+  CU(dC.alloc(rows * n * comps, hs->comp));
+  const size_t el = comps * sizeof(double);
+  CU(cudaMemcpyAsync(dA.p, a + r0 * l * comps, rows * l * el, cudaMemcpyHostToDevice, hs->comp));
+  CU(cudaMemcpyAsync(dB.p, b, l * n * el, cudaMemcpyHostToDevice, hs->comp));
+  CU(cudaMemcpyAsync(dC.p, c + r0 * n * comps, rows * n * el, cudaMemcpyHostToDevice, hs->comp));
   int rc = block_cells_impl(comps, n_min, cell0 - ib0 * nbc, cell1 - ib0 * nbc, rows, l, n, dA.p,
-                            l, dB.p, n, dC.p, n, 0);
+                            l, dB.p, n, dC.p, n, hs->comp);
   if (rc != MPMM_OK) return rc;
-  CU(cudaMemcpy(c + r0 * n * comps, dC.p, rows * n * comps * sizeof(double),
-                cudaMemcpyDeviceToHost));
+  CU(cudaMemcpyAsync(c + r0 * n * comps, dC.p, rows * n * el, cudaMemcpyDeviceToHost, hs->comp));
+  CU(cudaStreamSynchronize(hs->comp));
   return MPMM_OK;
 }
 
@@ -154,16 +280,22 @@ int host_ewise(int comps, int sign, const double* x, const double* y, double* ou
                int64_t rows, int64_t cols, int64_t i0, int64_t i1) {
   if (rows < 0 || cols < 0 || i0 < 0 || i1 > rows) return fail(MPMM_ERR_ARG, "bad row range");
   if (i1 <= i0 || cols == 0) return MPMM_OK;
+  HostStreams* hs = nullptr;
+  CU(host_streams(&hs));
   const int64_t r = i1 - i0, sz = r * cols * comps;
   DevBuf dX, dY;
-  CU(dX.alloc(sz));
-  CU(dY.alloc(sz));
-  CU(cudaMemcpy(dX.p, x + i0 * cols * comps, sz * sizeof(double), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(dY.p, y + i0 * cols * comps, sz * sizeof(double), cudaMemcpyHostToDevice));
+  CU(dX.alloc(sz, hs->comp));
+  CU(dY.alloc(sz, hs->comp));
+  CU(cudaMemcpyAsync(dX.p, x + i0 * cols * comps, sz * sizeof(double), cudaMemcpyHostToDevice,
+                     hs->comp));
+  CU(cudaMemcpyAsync(dY.p, y + i0 * cols * comps, sz * sizeof(double), cudaMemcpyHostToDevice,
+                     hs->comp));
   EwiseArgs e{comps, 1, (int)r, (int)cols, dX.p, cols, dY.p, cols, sign, nullptr, 0, 1,
-              nullptr, 0, 1, dX.p, cols, 0};
+              nullptr, 0, 1, dX.p, cols, hs->comp};
   CU(ewise_launch(e));
-  CU(cudaMemcpy(out + i0 * cols * comps, dX.p, sz * sizeof(double), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpyAsync(out + i0 * cols * comps, dX.p, sz * sizeof(double), cudaMemcpyDeviceToHost,
+                     hs->comp));
+  CU(cudaStreamSynchronize(hs->comp));
   return MPMM_OK;
 }
 
@@ -174,6 +306,11 @@ extern "C" {
 int mpmm_abi_version(void) { return MPMM_ABI_VERSION; }
 
 const char* mpmm_last_error(void) { return g_err.c_str(); }
+
+int mpmm_set_device(int device) {
+  cudaError_t e = cudaSetDevice(device);
+  return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "cudaSetDevice");
+}
 
 int mpmm_device_count(int* count) {
   int c = 0;
@@ -244,6 +381,18 @@ int mpmm_qd_ewise_add(const double* x, const double* y, double* out, int64_t row
 int mpmm_qd_ewise_sub(const double* x, const double* y, double* out, int64_t rows, int64_t cols,
                       int64_t i0, int64_t i1) {
   return host_ewise(4, -1, x, y, out, rows, cols, i0, i1);
+}
+
+int mpmm_gemm_host(int comps, int algo, int64_t n_min, int64_t m, int64_t l, int64_t n,
+                   const double* a, const double* b, double* c, int accumulate, int* nonfinite) {
+  if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
+  if (!dims_ok(m, l, n)) return fail(MPMM_ERR_ARG, "bad shape");
+  if (algo != MPMM_ALGO_SIMPLE && algo != MPMM_ALGO_BLOCK && algo != MPMM_ALGO_BLOCK_FAST)
+    return fail(MPMM_ERR_ARG, "bad algo");
+  if (algo == MPMM_ALGO_BLOCK_FAST && comps != 2)
+    return fail(MPMM_ERR_ARG, "the fast accuracy mode is implemented for DD only");
+  if (algo != MPMM_ALGO_SIMPLE && n_min < 1) return fail(MPMM_ERR_ARG, "block size must be positive");
+  return host_rows_gemm(comps, algo, n_min, m, l, n, a, b, c, accumulate != 0, nonfinite);
 }
 
 int mpmm_gemm_dev(int comps, int algo, int64_t n_min, int64_t m, int64_t l, int64_t n,

@@ -194,6 +194,23 @@ def _result(c, to_host):
     return c.to_host() if to_host else c
 
 
+def _pinned_empty(rows, cols, comps):
+    torch = _torch()
+    return torch.empty((rows, cols, comps), dtype=torch.float64, pin_memory=True).numpy()
+
+
+def _host_product(a, b, algo, n_min):
+    """Host operands, host result, one pipelined C-ABI call
+    (mpmm_gemm_host: k-panel H2D overlapped with the GEMM, page-locked
+    result buffer, finite flag from the GEMM epilogue)."""
+    out = _pinned_empty(a.rows, b.cols, a.prec.comps)
+    ok = _cuda.gemm_host(a.prec.comps, algo, n_min, np.ascontiguousarray(a.data),
+                         np.ascontiguousarray(b.data), out, accumulate=False)
+    if not ok:
+        raise RangeError("matrix product overflowed the working precision")
+    return DenseMatrix(a.rows, b.cols, a.prec, out)
+
+
 # ---------------------------------------------------------------------------
 # simple and blocked products (multiply.py:134-182)
 # ---------------------------------------------------------------------------
@@ -251,6 +268,8 @@ def _block_into(a, b, c, n_min, threads=1, flag=None):
 def matmul_simple(a, b, threads=1):
     """Triple-loop product; k accumulated in ascending order."""
     _check_pair(a, b, threads)
+    if backend.is_cuda() and not a.is_device and not b.is_device:
+        return _host_product(a, b, _cuda.ALGO_SIMPLE, 0)
     da, db, home = _operands(a, b)
     c = DenseMatrix.zeros(a.rows, b.cols, a.prec, da.device)
     flag = _flag(da.device) if c.is_device else None
@@ -275,6 +294,9 @@ def matmul_block(a, b, n_min, threads=1, *, mode="exact"):
         raise ValueError(f"unknown mode {mode!r}; expected one of {MODES}")
     if mode == "fast" and a.prec.kind is not Kind.DD:
         raise ValueError("the fast accuracy mode is implemented for DD only")
+    if backend.is_cuda() and not a.is_device and not b.is_device:
+        algo = _cuda.ALGO_BLOCK_FAST if mode == "fast" else _cuda.ALGO_BLOCK
+        return _host_product(a, b, algo, n_min)
     da, db, home = _operands(a, b)
     if mode == "fast":
         if not backend.is_cuda():
