@@ -149,6 +149,17 @@ int mpmm_ewise_batched_dev(int comps, int64_t batch, int64_t rows, int64_t cols,
 int mpmm_nonfinite_dev(int comps, int64_t rows, int64_t cols, const double *X, int64_t ldx,
                        int *flag, void *stream);
 
+/* Exact componentwise verification: for `count` sampled
+ * outputs (idx_i[s], idx_j[s]) (device int64 arrays) writes
+ *   ratio[s] = |c_ij - (AB)_ij| / (4 l 2^-u_exp (|A||B|)_ij)
+ * with (AB)_ij evaluated exactly in a fixed-point superaccumulator; <= 1
+ * means the north_star bound holds (u_exp 104 for DD, 209 for QD).  NaN
+ * marks a sample whose TwoProd error terms could underflow. */
+int mpmm_exact_check_dev(int comps, int64_t m, int64_t l, int64_t n, const double *A,
+                         int64_t lda, const double *B, int64_t ldb, const double *C, int64_t ldc,
+                         const int64_t *idx_i, const int64_t *idx_j, int64_t count, int u_exp,
+                         double *ratio, void *stream);
+
 /* FP64 roofline micro-benchmark: blocks x threads threads each run 8
  * independent chains of `iters` DFMA (op 0) or DADD (op 1). */
 int mpmm_fp64_burn_dev(int op, int blocks, int threads, int64_t iters, double *scratch,

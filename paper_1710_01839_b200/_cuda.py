@@ -60,6 +60,8 @@ _SIGNATURES = {
                        _VP, _I64, _INT, _VP, _I64, _VP],
     "mpmm_nonfinite_dev": [_INT, _I64, _I64, _VP, _I64, _VP, _VP],
     "mpmm_fp64_burn_dev": [_INT, _INT, _INT, _I64, _VP, _VP],
+    "mpmm_exact_check_dev": [_INT, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _VP,
+                             _I64, _INT, _VP, _VP],
     "mpmm_host_frobenius_norm": [_INT, _D, _I64, _D],
     "mpmm_host_frobenius_rel_diff": [_INT, _D, _D, _I64, _D],
 }
@@ -267,6 +269,13 @@ def ewise_dev(comps, rows, cols, O, ldo, X, ldx, Y, ldy, sy, Z=None, ldz=0, sz=1
 def nonfinite_dev(comps, rows, cols, X, ldx, flag, stream=None):
     sync_device()
     check(load().mpmm_nonfinite_dev(comps, rows, cols, X, ldx, flag, stream))
+
+
+def exact_check_dev(comps, m, l, n, A, lda, B, ldb, C, ldc, idx_i, idx_j, count, u_exp, ratio,
+                    stream=None):
+    sync_device()
+    check(load().mpmm_exact_check_dev(comps, m, l, n, A, lda, B, ldb, C, ldc, idx_i, idx_j,
+                                      count, u_exp, ratio, stream))
 
 
 def fp64_burn_dev(op, blocks, threads, iters, scratch, stream=None):

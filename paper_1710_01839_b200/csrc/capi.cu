@@ -478,6 +478,17 @@ int mpmm_nonfinite_dev(int comps, int64_t rows, int64_t cols, const double* X, i
   return err == cudaSuccess ? MPMM_OK : cuda_fail(err, "nonfinite launch");
 }
 
+int mpmm_exact_check_dev(int comps, int64_t m, int64_t l, int64_t n, const double* A,
+                         int64_t lda, const double* B, int64_t ldb, const double* C, int64_t ldc,
+                         const int64_t* idx_i, const int64_t* idx_j, int64_t count, int u_exp,
+                         double* ratio, void* stream) {
+  if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
+  if (!dims_ok(m, l, n) || count < 0) return fail(MPMM_ERR_ARG, "bad shape");
+  cudaError_t err = exact_check_launch(comps, (int)l, A, lda, B, ldb, C, ldc, idx_i, idx_j, count,
+                                       u_exp, ratio, (cudaStream_t)stream);
+  return err == cudaSuccess ? MPMM_OK : cuda_fail(err, "exact check launch");
+}
+
 int mpmm_fp64_burn_dev(int op, int blocks, int threads, int64_t iters, double* scratch,
                        void* stream) {
   if (op != 0 && op != 1) return fail(MPMM_ERR_ARG, "op must be 0 (DFMA) or 1 (DADD)");

@@ -82,6 +82,11 @@ cudaError_t ewise_batched_launch(int comps, int batch, int rows, int cols,
 cudaError_t nonfinite_launch(int comps, const double* X, int64_t ldx, int rows, int cols,
                              int* flag, cudaStream_t stream);
 
+cudaError_t exact_check_launch(int comps, int l, const double* A, int64_t lda, const double* B,
+                               int64_t ldb, const double* C, int64_t ldc, const int64_t* idx_i,
+                               const int64_t* idx_j, int64_t count, int u_exp, double* ratio,
+                               cudaStream_t stream);
+
 cudaError_t fp64_burn_launch(int op, int blocks, int threads, int64_t iters, double* out,
                              cudaStream_t stream);
 
