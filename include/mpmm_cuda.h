@@ -160,6 +160,16 @@ int mpmm_exact_check_dev(int comps, int64_t m, int64_t l, int64_t n, const doubl
                          const int64_t *idx_i, const int64_t *idx_j, int64_t count, int u_exp,
                          double *ratio, void *stream);
 
+/* Seeded BASELINE inputs generated on the device, bitwise equal to the
+ * numpy spec (paper_1710_01839_b200/inputs.py): the PCG64
+ * stream (128-bit state/increment as hi/lo words, as numpy's
+ * bit_generator.state reports them) starting at draw `first_draw`
+ * supplies comps * rows * cols uniforms, assembled into a (rows, cols)
+ * DD (comps 2) or QD (comps 4) matrix at `out`. */
+int mpmm_gen_inputs_dev(int comps, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                        uint64_t inc_lo, uint64_t first_draw, int64_t rows, int64_t cols,
+                        double *out, void *stream);
+
 /* FP64 roofline micro-benchmark: blocks x threads threads each run 8
  * independent chains of `iters` DFMA (op 0) or DADD (op 1). */
 int mpmm_fp64_burn_dev(int op, int blocks, int threads, int64_t iters, double *scratch,

@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmpmm_cuda.so")
-SOURCES = ["gemm_dd.cu", "gemm_qd.cu", "ewise.cu", "verify.cu", "capi.cu", "host_norms.cpp"]
+SOURCES = ["gemm_dd.cu", "gemm_qd.cu", "ewise.cu", "verify.cu", "rng.cu", "capi.cu", "host_norms.cpp"]
 HEADERS = ["ddqd.cuh", "common.cuh", "kernels.h", "gemm.cuh"]
 
 # -fmad=false: no implicit contraction (the reference is built with

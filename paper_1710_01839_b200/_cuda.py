@@ -60,6 +60,8 @@ _SIGNATURES = {
                        _VP, _I64, _INT, _VP, _I64, _VP],
     "mpmm_nonfinite_dev": [_INT, _I64, _I64, _VP, _I64, _VP, _VP],
     "mpmm_fp64_burn_dev": [_INT, _INT, _INT, _I64, _VP, _VP],
+    "mpmm_gen_inputs_dev": [_INT, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                            ctypes.c_uint64, ctypes.c_uint64, _I64, _I64, _VP, _VP],
     "mpmm_exact_check_dev": [_INT, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _VP,
                              _I64, _INT, _VP, _VP],
     "mpmm_host_frobenius_norm": [_INT, _D, _I64, _D],
@@ -276,6 +278,13 @@ def exact_check_dev(comps, m, l, n, A, lda, B, ldb, C, ldc, idx_i, idx_j, count,
     sync_device()
     check(load().mpmm_exact_check_dev(comps, m, l, n, A, lda, B, ldb, C, ldc, idx_i, idx_j,
                                       count, u_exp, ratio, stream))
+
+
+def gen_inputs_dev(comps, state, inc, first_draw, rows, cols, out, stream=None):
+    sync_device()
+    m64 = (1 << 64) - 1
+    check(load().mpmm_gen_inputs_dev(comps, state >> 64, state & m64, inc >> 64, inc & m64,
+                                     first_draw, rows, cols, out, stream))
 
 
 def fp64_burn_dev(op, blocks, threads, iters, scratch, stream=None):

@@ -489,6 +489,23 @@ int mpmm_exact_check_dev(int comps, int64_t m, int64_t l, int64_t n, const doubl
   return err == cudaSuccess ? MPMM_OK : cuda_fail(err, "exact check launch");
 }
 
+int mpmm_gen_inputs_dev(int comps, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                        uint64_t inc_lo, uint64_t first_draw, int64_t rows, int64_t cols,
+                        double* out, void* stream) {
+  if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
+  if (rows < 0 || cols < 0) return fail(MPMM_ERR_ARG, "bad shape");
+  const int64_t count = rows * cols;
+  if (count == 0) return MPMM_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  double* draws = nullptr;
+  CU(cudaMallocAsync(reinterpret_cast<void**>(&draws), comps * count * sizeof(double), s));
+  cudaError_t e = uniform_launch(state_hi, state_lo, inc_hi, inc_lo, first_draw, comps * count,
+                                 draws, s);
+  if (e == cudaSuccess) e = assemble_launch(comps, draws, count, out, s);
+  cudaFreeAsync(draws, s);
+  return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "input generation launch");
+}
+
 int mpmm_fp64_burn_dev(int op, int blocks, int threads, int64_t iters, double* scratch,
                        void* stream) {
   if (op != 0 && op != 1) return fail(MPMM_ERR_ARG, "op must be 0 (DFMA) or 1 (DADD)");

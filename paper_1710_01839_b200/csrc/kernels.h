@@ -87,6 +87,11 @@ cudaError_t exact_check_launch(int comps, int l, const double* A, int64_t lda, c
                                const int64_t* idx_j, int64_t count, int u_exp, double* ratio,
                                cudaStream_t stream);
 
+cudaError_t uniform_launch(uint64_t s_hi, uint64_t s_lo, uint64_t i_hi, uint64_t i_lo,
+                           uint64_t first, int64_t count, double* out, cudaStream_t stream);
+cudaError_t assemble_launch(int comps, const double* draws, int64_t count, double* out,
+                            cudaStream_t stream);
+
 cudaError_t fp64_burn_launch(int op, int blocks, int threads, int64_t iters, double* out,
                              cudaStream_t stream);
 

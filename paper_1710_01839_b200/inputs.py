@@ -139,3 +139,32 @@ def gemm_inputs(prec_token, m, l, n, seed=0, wide=False):
             raise ValueError("the wide-exponent set is defined for DD only")
         return qd_random(rng, m, l), qd_random(rng, l, n)
     raise ValueError(f"unsupported precision {prec_token!r}")
+
+
+def gemm_inputs_device(prec_token, m, l, n, seed=0, wide=False, device=None):
+    """The same A and B as :func:`gemm_inputs`, generated in HBM
+    (``csrc/rng.cu``: PCG64 jump-ahead + the numpy operation order), as
+    float64 CUDA tensors of shape (rows, cols, comps).  Bitwise equal to the
+    host generator (tests/test_gpu_inputs.py)."""
+    import torch
+
+    from . import _cuda
+    comps = {"dd": 2, "qd": 4}[prec_token]
+    if wide and prec_token != "dd":
+        raise ValueError("the wide-exponent set is defined for DD only")
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    rng = np.random.default_rng(seed)
+    st = rng.bit_generator.state["state"]
+    a = torch.empty((m, l, comps), dtype=torch.float64, device=dev)
+    b = torch.empty((l, n, comps), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    _cuda.gen_inputs_dev(comps, st["state"], st["inc"], 0, m, l, a.data_ptr(), stream)
+    _cuda.gen_inputs_dev(comps, st["state"], st["inc"], comps * m * l, l, n, b.data_ptr(),
+                         stream)
+    if wide:
+        rng.bit_generator.advance(comps * (m * l + l * n))
+        ka = rng.integers(-30, 31, (m, l))
+        kb = rng.integers(-30, 31, (l, n))
+        a.mul_(torch.from_numpy(np.ldexp(1.0, ka)).to(dev)[..., None])
+        b.mul_(torch.from_numpy(np.ldexp(1.0, kb)).to(dev)[..., None])
+    return a, b
