@@ -170,6 +170,38 @@ int mpmm_gen_inputs_dev(int comps, uint64_t state_hi, uint64_t state_lo, uint64_
                         uint64_t inc_lo, uint64_t first_draw, int64_t rows, int64_t cols,
                         double *out, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Exact int8 tensor-core mode (ozaki.cu; orchestrated by tensor.py).  The
+ * product of scaled-integer DD/QD operands is rebuilt exactly from int8
+ * residue GEMMs modulo the 54 pairwise-coprime prime powers <= 256 (CRT),
+ * then rounded once to DD/QD.  Not bit-identical to the reference (it is
+ * the exact product, correctly rounded).
+ * ------------------------------------------------------------------------- */
+/* Per row (by_cols 0) or column (1) of the components [c0,c1): E = max
+ * exponent (|x| < 2^E), L = lowest set bit (empty: E=-100000, L=100000). */
+int mpmm_oz_scan_dev(int by_cols, int comps, int c0, int c1, int64_t rows, int64_t cols,
+                     const double *X, int64_t ld, int *E, int *L, void *stream);
+/* int8 residues of x * 2^shift[row|col] modulo the first nmod moduli:
+ * by_cols 0 -> R[t*rplane + row*rpitch + col], by_cols 1 ->
+ * R[t*rplane + col*rpitch + row] (k contiguous; pads are left untouched).
+ * pow2: nmod x xmax table of 2^x mod p_t (xmax > largest scaled exponent). */
+int mpmm_oz_residues_dev(int by_cols, int comps, int c0, int c1, int64_t rows, int64_t cols,
+                         const double *X, int64_t ld, const int *shift, int nmod,
+                         const uint8_t *pow2, int xmax, int8_t *R, int64_t rpitch,
+                         int64_t rplane, void *stream);
+/* batch x (C_t = A_t * Bt_t^T): A_t m x k, Bt_t n x k (row-major int8),
+ * C_t m x n row-major int32, exact for k <= 131071 (cuBLASLt IMMA); m, n,
+ * k multiples of 16. */
+int mpmm_int8_gemm_batched_dev(int64_t m, int64_t n, int64_t k, int64_t batch, const int8_t *A,
+                               const int8_t *Bt, int32_t *C, void *workspace, int64_t ws_bytes,
+                               void *stream);
+/* CRT reconstruction of njobs jobs (device array of 56-byte records {G,
+ * srow, scol, table: pointers; N, K: int32; gpitch, gplane: int64}), exact
+ * sum, rounding to comps doubles per entry of C (m x n); *status |= 1
+ * non-finite, 2 window. */
+int mpmm_oz_combine_dev(int comps, const void *jobs, int njobs, int64_t m, int64_t n, double *C,
+                        int *status, void *stream);
+
 /* FP64 roofline micro-benchmark: blocks x threads threads each run 8
  * independent chains of `iters` DFMA (op 0) or DADD (op 1). */
 int mpmm_fp64_burn_dev(int op, int blocks, int threads, int64_t iters, double *scratch,

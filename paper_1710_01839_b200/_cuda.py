@@ -62,6 +62,11 @@ _SIGNATURES = {
     "mpmm_fp64_burn_dev": [_INT, _INT, _INT, _I64, _VP, _VP],
     "mpmm_gen_inputs_dev": [_INT, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                             ctypes.c_uint64, ctypes.c_uint64, _I64, _I64, _VP, _VP],
+    "mpmm_oz_scan_dev": [_INT, _INT, _INT, _INT, _I64, _I64, _VP, _I64, _VP, _VP, _VP],
+    "mpmm_oz_residues_dev": [_INT, _INT, _INT, _INT, _I64, _I64, _VP, _I64, _VP, _INT, _VP, _INT,
+                             _VP, _I64, _I64, _VP],
+    "mpmm_int8_gemm_batched_dev": [_I64, _I64, _I64, _I64, _VP, _VP, _VP, _VP, _I64, _VP],
+    "mpmm_oz_combine_dev": [_INT, _VP, _INT, _I64, _I64, _VP, _VP, _VP],
     "mpmm_exact_check_dev": [_INT, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _VP,
                              _I64, _INT, _VP, _VP],
     "mpmm_host_frobenius_norm": [_INT, _D, _I64, _D],
@@ -285,6 +290,29 @@ def gen_inputs_dev(comps, state, inc, first_draw, rows, cols, out, stream=None):
     m64 = (1 << 64) - 1
     check(load().mpmm_gen_inputs_dev(comps, state >> 64, state & m64, inc >> 64, inc & m64,
                                      first_draw, rows, cols, out, stream))
+
+
+def oz_scan_dev(by_cols, comps, c0, c1, rows, cols, X, ld, E, L, stream=None):
+    sync_device()
+    check(load().mpmm_oz_scan_dev(by_cols, comps, c0, c1, rows, cols, X, ld, E, L, stream))
+
+
+def oz_residues_dev(by_cols, comps, c0, c1, rows, cols, X, ld, shift, nmod, pow2, xmax, R,
+                    rpitch, rplane, stream=None):
+    sync_device()
+    check(load().mpmm_oz_residues_dev(by_cols, comps, c0, c1, rows, cols, X, ld, shift, nmod,
+                                      pow2, xmax, R, rpitch, rplane, stream))
+
+
+def int8_gemm_batched_dev(m, n, k, batch, A, Bt, C, workspace, ws_bytes, stream=None):
+    sync_device()
+    check(load().mpmm_int8_gemm_batched_dev(m, n, k, batch, A, Bt, C, workspace, ws_bytes,
+                                            stream))
+
+
+def oz_combine_dev(comps, jobs, njobs, m, n, C, status, stream=None):
+    sync_device()
+    check(load().mpmm_oz_combine_dev(comps, jobs, njobs, m, n, C, status, stream))
 
 
 def fp64_burn_dev(op, blocks, threads, iters, scratch, stream=None):

@@ -506,6 +506,48 @@ int mpmm_gen_inputs_dev(int comps, uint64_t state_hi, uint64_t state_lo, uint64_
   return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "input generation launch");
 }
 
+int mpmm_oz_scan_dev(int by_cols, int comps, int c0, int c1, int64_t rows, int64_t cols,
+                     const double* X, int64_t ld, int* E, int* L, void* stream) {
+  if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
+  if (c0 < 0 || c1 > comps || c0 >= c1) return fail(MPMM_ERR_ARG, "bad component range");
+  if (!dims_ok(rows, 0, cols)) return fail(MPMM_ERR_ARG, "bad shape");
+  cudaError_t e = oz_scan_launch(by_cols, X, ld, (int)rows, (int)cols, comps, c0, c1, E, L,
+                                 (cudaStream_t)stream);
+  return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "scan launch");
+}
+
+int mpmm_oz_residues_dev(int by_cols, int comps, int c0, int c1, int64_t rows, int64_t cols,
+                         const double* X, int64_t ld, const int* shift, int nmod,
+                         const uint8_t* pow2, int xmax, int8_t* R, int64_t rpitch,
+                         int64_t rplane, void* stream) {
+  if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
+  if (c0 < 0 || c1 > comps || c0 >= c1) return fail(MPMM_ERR_ARG, "bad component range");
+  if (!dims_ok(rows, 0, cols) || nmod < 1 || nmod > 54) return fail(MPMM_ERR_ARG, "bad shape");
+  cudaError_t e = oz_residues_launch(by_cols, X, ld, (int)rows, (int)cols, comps, c0, c1, shift,
+                                     nmod, pow2, xmax, R, rpitch, rplane, (cudaStream_t)stream);
+  return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "residues launch");
+}
+
+int mpmm_int8_gemm_batched_dev(int64_t m, int64_t n, int64_t k, int64_t batch, const int8_t* A,
+                               const int8_t* Bt, int32_t* C, void* workspace, int64_t ws_bytes,
+                               void* stream) {
+  if (m % 16 || n % 16 || k % 16)
+    return fail(MPMM_ERR_ARG, "int8 GEMM dimensions must be multiples of 16 (pad the operands)");
+  std::string err;
+  int rc = int8_gemm_batched(m, n, k, batch, A, Bt, C, workspace, (size_t)ws_bytes,
+                             (cudaStream_t)stream, &err);
+  return rc == 0 ? MPMM_OK : fail(rc == 1 ? MPMM_ERR_ARG : MPMM_ERR_CUDA, err);
+}
+
+int mpmm_oz_combine_dev(int comps, const void* jobs, int njobs, int64_t m, int64_t n, double* C,
+                        int* status, void* stream) {
+  if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
+  if (njobs < 1 || !dims_ok(m, 0, n)) return fail(MPMM_ERR_ARG, "bad shape");
+  cudaError_t e = oz_combine_launch(comps, jobs, njobs, (int)m, (int)n, C, status,
+                                    (cudaStream_t)stream);
+  return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "combine launch");
+}
+
 int mpmm_fp64_burn_dev(int op, int blocks, int threads, int64_t iters, double* scratch,
                        void* stream) {
   if (op != 0 && op != 1) return fail(MPMM_ERR_ARG, "op must be 0 (DFMA) or 1 (DADD)");

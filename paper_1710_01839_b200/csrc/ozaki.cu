@@ -1,0 +1,489 @@
+// ozaki.cu -- exact DD/QD products on the int8 tensor cores (CRT scheme).
+//
+// Opt-in "tensor" mode (a non-mirror kernel states its own
+// F and bound).  Every DD/QD entry is an exact scaled integer: with the
+// per-row shift s_i = -min over the row of the lowest set bit of any
+// component, a_ik * 2^s_i is an integer of at most beta_A bits (likewise
+// b_kj * 2^t_j, beta_B bits).  The integer product
+//     X_ij = sum_k (a_ik 2^s_i)(b_kj 2^t_j),  |X_ij| < l 2^(beta_A + beta_B)
+// is computed EXACTLY from its residues modulo N pairwise-coprime moduli
+// p_t <= 256 (product P > 2 |X|): residues of the inputs are int8, each
+// residue product is one int8 GEMM with exact int32 accumulation on the
+// tensor cores (int8gemm.cpp, cuBLASLt), and the Chinese remainder theorem
+// rebuilds X_ij.  c_ij = X_ij 2^-(s_i + t_j) is then rounded once to the
+// nearest DD (QD) expansion: the result is the exact product correctly
+// rounded, far inside the north_star bound, but not bit-identical to the
+// reference's step-by-step rounding.
+//
+// When beta_A + beta_B is too wide for the 54 available int8 moduli (363
+// bits), the host splits each entry into component ranges (hi/lo) and the
+// combine step sums the exact products of every pair of ranges, so the
+// result is still the exact product, rounded once.  The planner
+// (tensor.py) reports NotRepresentable when even single components do not
+// fit.
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace mpmm {
+
+// The 54 pairwise-coprime prime powers <= 256, descending (sum of log2 =
+// 362.8 bits).  ozaki.py holds the same list.
+__constant__ int kModsDev[54] = {
+    256, 251, 243, 241, 239, 233, 229, 227, 223, 211, 199, 197, 193, 191,
+    181, 179, 173, 169, 167, 163, 157, 151, 149, 139, 137, 131, 127, 125,
+    121, 113, 109, 107, 103, 101, 97,  89,  83,  79,  73,  71,  67,  61,
+    59,  53,  49,  47,  43,  41,  37,  31,  29,  23,  19,  17};
+constexpr int kNumMods = 54;
+// Lemire fastmod constants ceil(2^64 / p) and 2^32 mod p
+__constant__ unsigned long long kModM[54] = {
+    0x0100000000000000ull, 0x0105197f7d734042ull, 0x010db20a88f4695aull, 0x010fef010fef0110ull,
+    0x0112358e75d30337ull, 0x0119453808ca29c1ull, 0x011e2ef3b3fb8745ull, 0x0120b470c67c0d89ull,
+    0x0125e22708092f12ull, 0x013698df3de0747aull, 0x0149539e3b2d066full, 0x014cab88725af6e8ull,
+    0x015390948f40feadull, 0x01571ed3c506b39bull, 0x016a13cd15372905ull, 0x016e1f76b4337c6dull,
+    0x017ad2208e0ecc36ull, 0x0183c977ab2bedd3ull, 0x01886e5f0abb049aull, 0x01920fb49d0e228eull,
+    0x01a16d3f97a4b01bull, 0x01b2036406c80d91ull, 0x01b7d6c3dda338b3ull, 0x01d77b654b82c33aull,
+    0x01de5d6e3f8868a5ull, 0x01f44659e4a42716ull, 0x0204081020408103ull, 0x020c49ba5e353f7dull,
+    0x021d9ead7cd391fcull, 0x0243f6f0243f6f03ull, 0x02593f69b02593f7ull, 0x02647c69456217edull,
+    0x027c45979c952050ull, 0x0288df0cac5b3f5eull, 0x02a3a0fd5c5f02a4ull, 0x02e05c0b81702e06ull,
+    0x03159721ed7e7535ull, 0x033d91d2a2067b24ull, 0x0381c0e070381c0full, 0x039b0ad12073615bull,
+    0x03d226357e16ece6ull, 0x04325c53ef368eb1ull, 0x0456c797dd49c342ull, 0x04d4873ecade304eull,
+    0x05397829cbc14e5full, 0x0572620ae4c415caull, 0x05f417d05f417d06ull, 0x063e7063e7063e71ull,
+    0x06eb3e45306eb3e5ull, 0x0842108421084211ull, 0x08d3dcb08d3dcb09ull, 0x0b21642c8590b217ull,
+    0x0d79435e50d79436ull, 0x0f0f0f0f0f0f0f10ull};
+__constant__ unsigned kMod2p32[54] = {
+    0,  123, 130, 15, 110, 8,  161, 176, 7,  51, 46, 88, 108, 147, 15, 126, 96, 113,
+    7,  100, 93,  4,  129, 41, 34,  117, 16, 46, 59, 16, 75,  29,  63, 68,  35, 45,
+    77, 50,  32,  9,  33,  57, 51,  42,  39, 42, 16, 37, 7,   4,   16, 12,  6,  1};
+
+// a mod d for 32-bit a (Lemire, Kaser, Kurz: "Faster remainder by direct
+// computation"), M = ceil(2^64 / d)
+__device__ __forceinline__ unsigned fastmod(unsigned a, unsigned long long M, unsigned d) {
+  unsigned long long low = M * a;
+  return static_cast<unsigned>(__umul64hi(low, d));
+}
+
+namespace {
+
+__device__ __forceinline__ int top_exp(double x) {  // |x| < 2^top_exp
+  unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  int be = static_cast<int>((b >> 52) & 0x7ff);
+  unsigned long long man = b & ((1ull << 52) - 1);
+  if (be > 0) return be - 1022;
+  return -1074 + (64 - __clzll(static_cast<long long>(man)));
+}
+
+__device__ __forceinline__ int low_bit(double x) {  // weight exponent of the lowest set bit
+  unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  int be = static_cast<int>((b >> 52) & 0x7ff);
+  unsigned long long man = b & ((1ull << 52) - 1);
+  if (be > 0) man |= (1ull << 52);
+  int e = be > 0 ? be - 1075 : -1074;
+  return e + (__ffsll(static_cast<long long>(man)) - 1);
+}
+
+__device__ __forceinline__ bool is_zero(double x) {
+  return (static_cast<unsigned long long>(__double_as_longlong(x)) << 1) == 0ull;
+}
+
+constexpr int kEmptyE = -100000, kEmptyL = 100000;
+
+// one warp per row: E = max top_exp, L = min low_bit over the components
+// [c0, c1) of the row's entries
+__global__ void scan_rows_kernel(const double* __restrict__ X, int64_t ld, int rows, int cols,
+                                 int comps, int c0, int c1, int* __restrict__ E,
+                                 int* __restrict__ L) {
+  int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  int e = kEmptyE, lo = kEmptyL;
+  for (int k = lane; k < cols; k += 32) {
+    const double* p = X + ((int64_t)r * ld + k) * comps;
+    for (int c = c0; c < c1; ++c) {
+      double v = p[c];
+      if (!is_zero(v)) {
+        e = max(e, top_exp(v));
+        lo = min(lo, low_bit(v));
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    e = max(e, __shfl_xor_sync(0xffffffffu, e, o));
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+  }
+  if (lane == 0) {
+    E[r] = e;
+    L[r] = lo;
+  }
+}
+
+// one thread per column
+__global__ void scan_cols_kernel(const double* __restrict__ X, int64_t ld, int rows, int cols,
+                                 int comps, int c0, int c1, int* __restrict__ E,
+                                 int* __restrict__ L) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  int e = kEmptyE, lo = kEmptyL;
+  for (int k = 0; k < rows; ++k) {
+    const double* p = X + ((int64_t)k * ld + j) * comps;
+    for (int c = c0; c < c1; ++c) {
+      double v = p[c];
+      if (!is_zero(v)) {
+        e = max(e, top_exp(v));
+        lo = min(lo, low_bit(v));
+      }
+    }
+  }
+  E[j] = e;
+  L[j] = lo;
+}
+
+// Residues of sum_{c in [c0,c1)} x_c 2^shift (an exact integer) modulo the
+// first N moduli, centred into int8.  pow2: N x xmax table of 2^x mod p_t.
+__device__ __forceinline__ void entry_residues(const double* x, int c0, int c1, int shift, int N,
+                                               const uint8_t* __restrict__ pow2, int xmax,
+                                               int8_t* out, int64_t out_stride) {
+  unsigned long long man[4];
+  int ex[4];
+  bool neg[4];
+  int nc = 0;
+  for (int c = c0; c < c1; ++c) {
+    double v = x[c];
+    if (is_zero(v)) continue;
+    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    int be = static_cast<int>((b >> 52) & 0x7ff);
+    unsigned long long m = b & ((1ull << 52) - 1);
+    if (be > 0) m |= (1ull << 52);
+    int e = (be > 0 ? be - 1075 : -1074) + shift;
+    int tz = __ffsll(static_cast<long long>(m)) - 1;
+    m >>= tz;
+    e += tz;                      // >= 0 by the choice of shift (scan_*)
+    man[nc] = m;
+    ex[nc] = e < xmax ? e : xmax - 1;
+    neg[nc] = (b >> 63) != 0;
+    ++nc;
+  }
+#pragma unroll 1
+  for (int t = 0; t < N; ++t) {
+    const unsigned p = static_cast<unsigned>(kModsDev[t]);
+    const unsigned long long M = kModM[t];
+    const unsigned c32 = kMod2p32[t];
+    unsigned acc = 0;
+    for (int c = 0; c < nc; ++c) {
+      // man < 2^53: (hi * 2^32 + lo) mod p
+      unsigned lo = static_cast<unsigned>(man[c]), hi = static_cast<unsigned>(man[c] >> 32);
+      unsigned mr = fastmod(hi * c32 + fastmod(lo, M, p), M, p);
+      unsigned term = fastmod(mr * pow2[t * xmax + ex[c]], M, p);
+      acc += neg[c] ? p - term : term;
+    }
+    int r = static_cast<int>(fastmod(acc, M, p));
+    if (r >= static_cast<int>((p + 1) / 2)) r -= static_cast<int>(p);   // [-(p-1)/2, p/2)
+    out[t * out_stride] = static_cast<int8_t>(r);
+  }
+}
+
+// A (rows x cols) -> R[t][row][col]; thread per entry, consecutive cols
+__global__ void residues_rows_kernel(const double* __restrict__ X, int64_t ld, int rows, int cols,
+                                     int comps, int c0, int c1, const int* __restrict__ shift,
+                                     int N, const uint8_t* __restrict__ pow2, int xmax,
+                                     int8_t* __restrict__ R, int64_t rpitch, int64_t rplane) {
+  int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= static_cast<int64_t>(rows) * cols) return;
+  int r = static_cast<int>(e / cols), k = static_cast<int>(e % cols);
+  entry_residues(X + ((int64_t)r * ld + k) * comps, c0, c1, shift[r], N, pow2, xmax,
+                 R + r * rpitch + k, rplane);
+}
+
+// B (rows=l x cols=n) -> R[t][col][row] (k contiguous); thread per entry,
+// consecutive rows (k) so the int8 stores coalesce
+__global__ void residues_cols_kernel(const double* __restrict__ X, int64_t ld, int rows, int cols,
+                                     int comps, int c0, int c1, const int* __restrict__ shift,
+                                     int N, const uint8_t* __restrict__ pow2, int xmax,
+                                     int8_t* __restrict__ R, int64_t rpitch, int64_t rplane) {
+  int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= static_cast<int64_t>(rows) * cols) return;
+  int j = static_cast<int>(e / rows), k = static_cast<int>(e % rows);
+  entry_residues(X + ((int64_t)k * ld + j) * comps, c0, c1, shift[j], N, pow2, xmax,
+                 R + j * rpitch + k, rplane);
+}
+
+// ---------------------------------------------------------------------------
+// CRT reconstruction + exact combination + rounding to DD/QD
+// ---------------------------------------------------------------------------
+
+constexpr int kMaxLimbs = 13;    // P < 2^363 -> 12 limbs (+1 for the weighted sum)
+constexpr int kWin = 28;         // accumulator window: 28 x 32 = 896 bits
+
+// double of a limb vector (top 3 limbs suffice for ~2^-60 relative accuracy)
+__device__ double limbs_to_double(const uint32_t* v, int n) {
+  double d = 0.0;
+  int top = n - 1;
+  while (top > 0 && v[top] == 0) --top;
+  for (int q = top; q >= 0 && q >= top - 2; --q) d += ldexp(static_cast<double>(v[q]), 32 * q);
+  return d;
+}
+
+// add (sign ? -1 : +1) * X * 2^bitshift into the signed digit window
+__device__ void win_add(int64_t* win, const uint32_t* X, int nx, int bitshift, bool neg) {
+  int q0 = bitshift >> 5, r = bitshift & 31;
+  for (int q = 0; q < nx; ++q) {
+    uint64_t v = static_cast<uint64_t>(X[q]) << r;       // < 2^63
+    int64_t lo = static_cast<int64_t>(v & 0xffffffffull), hi = static_cast<int64_t>(v >> 32);
+    if (neg) {
+      lo = -lo;
+      hi = -hi;
+    }
+    if (q0 + q < kWin) win[q0 + q] += lo;
+    if (q0 + q + 1 < kWin) win[q0 + q + 1] += hi;
+  }
+}
+
+// carry-normalise; returns the sign; digits become the magnitude in [0,2^32)
+__device__ bool win_normalize(int64_t* win) {
+  int64_t carry = 0;
+  for (int q = 0; q < kWin; ++q) {
+    int64_t v = win[q] + carry;
+    carry = v >> 32;
+    win[q] = v - (carry << 32);
+  }
+  if (carry >= 0) return false;
+  int64_t c = 1;                                  // two's complement -> magnitude
+  for (int q = 0; q < kWin; ++q) {
+    int64_t v = (0xffffffffll - win[q]) + c;
+    c = v >> 32;
+    win[q] = v & 0xffffffffll;
+  }
+  return true;
+}
+
+// round-to-nearest double of magnitude digits * 2^ebase (top 64 bits + sticky)
+__device__ double win_round(const int64_t* win, int ebase) {
+  int top = kWin - 1;
+  while (top >= 0 && win[top] == 0) --top;
+  if (top < 0) return 0.0;
+  // gather the 96 bits below and including digit `top`, then take 64 + sticky
+  uint64_t hi = static_cast<uint64_t>(win[top]);
+  uint64_t mid = top >= 1 ? static_cast<uint64_t>(win[top - 1]) : 0;
+  uint64_t lo = top >= 2 ? static_cast<uint64_t>(win[top - 2]) : 0;
+  bool sticky = false;
+  for (int q = top - 3; q >= 0; --q) sticky |= (win[q] != 0);
+  int lz = __clzll(static_cast<long long>(hi)) - 32;      // leading zeros within the 32-bit digit
+  // 96-bit value (hi:mid:lo) normalised so its top bit is bit 95
+  unsigned __int128 w = (static_cast<unsigned __int128>(hi) << 64) |
+                        (static_cast<unsigned __int128>(mid) << 32) | lo;
+  w <<= lz;
+  uint64_t top64 = static_cast<uint64_t>(w >> 32);
+  if ((static_cast<uint64_t>(w) & 0xffffffffull) != 0 || sticky) top64 |= 1ull;
+  double d = __ull2double_rn(top64);
+  // value = top64 * 2^(32*(top-2) - lz + 32 - 32) ... top64 holds bits [95-63, 95] of w
+  int e = 32 * (top - 2) - lz + 32 + ebase;
+  return ldexp(d, e);
+}
+
+// subtract the double d (an integer multiple of 2^ebase) from the window
+__device__ void win_sub_double(int64_t* win, double d, int ebase) {
+  if (d == 0.0) return;
+  unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(d));
+  int be = static_cast<int>((b >> 52) & 0x7ff);
+  unsigned long long m = b & ((1ull << 52) - 1);
+  if (be > 0) m |= (1ull << 52);
+  int e = (be > 0 ? be - 1075 : -1074) - ebase;
+  int tz = __ffsll(static_cast<long long>(m)) - 1;
+  m >>= tz;
+  e += tz;                     // >= 0
+  uint32_t limbs[3] = {static_cast<uint32_t>(m), static_cast<uint32_t>(m >> 32), 0u};
+  win_add(win, limbs, 2, e, (b >> 63) == 0);   // subtract: add with flipped sign
+}
+
+}  // namespace
+
+// Per-job CRT data (device): moduli count, limb count, P limbs, weights.
+struct CrtJob {
+  const int32_t* G;         // [N][.][gpitch] residue products, plane stride gplane
+  const int* srow;          // [m] row shifts
+  const int* scol;          // [n] column shifts
+  const uint32_t* table;    // [K] P limbs, then [N][K] weight limbs
+  int N, K;
+  int64_t gpitch, gplane;
+};
+
+template <int COMPS>
+__global__ void __launch_bounds__(128)
+combine_kernel(const CrtJob* __restrict__ jobs, int njobs, int m, int n,
+               double* __restrict__ C, int* __restrict__ status) {
+  int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= static_cast<int64_t>(m) * n) return;
+  const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
+  // window base: the smallest weight exponent of the jobs
+  int ebase = 1 << 30;
+  for (int J = 0; J < njobs; ++J) ebase = min(ebase, -(jobs[J].srow[i] + jobs[J].scol[j]));
+  int64_t win[kWin];
+#pragma unroll
+  for (int q = 0; q < kWin; ++q) win[q] = 0;
+  for (int J = 0; J < njobs; ++J) {
+    const CrtJob& jb = jobs[J];
+    const int K = jb.K, N = jb.N;
+    const uint32_t* P = jb.table;
+    const uint32_t* W = jb.table + K;
+    uint64_t acc[kMaxLimbs + 1];
+    for (int q = 0; q <= K; ++q) acc[q] = 0;
+    const int32_t* Gij = jb.G + static_cast<int64_t>(i) * jb.gpitch + j;
+    for (int t = 0; t < N; ++t) {
+      int p = kModsDev[t];
+      int g = Gij[t * jb.gplane];
+      uint32_t r = static_cast<uint32_t>(((g % p) + p) % p);
+      for (int q = 0; q < K; ++q) acc[q] += static_cast<uint64_t>(r) * W[t * K + q];
+    }
+    uint32_t S[kMaxLimbs + 1];
+    uint64_t carry = 0;
+    for (int q = 0; q <= K; ++q) {
+      uint64_t v = acc[q] + carry;
+      S[q] = static_cast<uint32_t>(v);
+      carry = v >> 32;
+    }
+    // q = floor(S / P), corrected by one step either way
+    double qd = floor(limbs_to_double(S, K + 1) / limbs_to_double(P, K));
+    uint64_t qv = qd > 0.0 ? static_cast<uint64_t>(qd) : 0ull;
+    // X = S - qv * P (signed, K+1 limbs)
+    int64_t X[kMaxLimbs + 1];
+    int64_t borrow = 0;
+    for (int q = 0; q <= K; ++q) {
+      uint64_t pq = q < K ? static_cast<uint64_t>(P[q]) * qv : 0ull;
+      // compute in 64-bit with split carries
+      int64_t v = static_cast<int64_t>(S[q]) - static_cast<int64_t>(pq & 0xffffffffull) + borrow;
+      borrow = (v >> 32) - static_cast<int64_t>(pq >> 32);
+      X[q] = v & 0xffffffffll;
+    }
+    // borrow < 0: X negative -> add P;  compare X >= P -> subtract P
+    if (borrow < 0) {
+      int64_t c = 0;
+      for (int q = 0; q <= K; ++q) {
+        int64_t v = X[q] + (q < K ? static_cast<int64_t>(P[q]) : 0) + c;
+        c = v >> 32;
+        X[q] = v & 0xffffffffll;
+      }
+    } else {
+      bool ge = X[K] != 0;
+      if (!ge) {
+        ge = true;
+        for (int q = K - 1; q >= 0; --q) {
+          if (X[q] != static_cast<int64_t>(P[q])) {
+            ge = X[q] > static_cast<int64_t>(P[q]);
+            break;
+          }
+        }
+      }
+      if (ge) {
+        int64_t c = 0;
+        for (int q = 0; q <= K; ++q) {
+          int64_t v = X[q] - (q < K ? static_cast<int64_t>(P[q]) : 0) + c;
+          c = v >> 32;
+          X[q] = v & 0xffffffffll;
+        }
+      }
+    }
+    // centre: X > P/2 -> X - P (magnitude P - X, negative)
+    bool upper = false;
+    {
+      // compare 2X with P
+      uint32_t twoX[kMaxLimbs + 1];
+      uint64_t c = 0;
+      for (int q = 0; q <= K; ++q) {
+        uint64_t v = (static_cast<uint64_t>(X[q]) << 1) + c;
+        twoX[q] = static_cast<uint32_t>(v);
+        c = v >> 32;
+      }
+      upper = twoX[K] != 0 || c != 0;
+      if (!upper) {
+        for (int q = K - 1; q >= 0; --q) {
+          if (twoX[q] != P[q]) {
+            upper = twoX[q] > P[q];
+            break;
+          }
+        }
+      }
+    }
+    uint32_t mag[kMaxLimbs];
+    if (upper) {
+      int64_t c = 0;
+      for (int q = 0; q < K; ++q) {
+        int64_t v = static_cast<int64_t>(P[q]) - X[q] + c;
+        c = v >> 32;
+        mag[q] = static_cast<uint32_t>(v & 0xffffffffll);
+      }
+    } else {
+      for (int q = 0; q < K; ++q) mag[q] = static_cast<uint32_t>(X[q]);
+    }
+    const int eJ = -(jb.srow[i] + jb.scol[j]);
+    const int shift = eJ - ebase;
+    if (shift + 32 * K > 32 * kWin) atomicOr(status, 2);    // window too small
+    win_add(win, mag, K, shift, upper);
+  }
+  bool neg = win_normalize(win);
+  // extract COMPS round-to-nearest doubles from the exact value
+  double out[COMPS];
+  for (int c = 0; c < COMPS; ++c) {
+    double d = win_round(win, ebase);
+    out[c] = neg ? -d : d;
+    // remainder: win (magnitude) - d; it may turn negative
+    win_sub_double(win, d, ebase);
+    bool flip = win_normalize(win);
+    neg = neg ^ flip;
+  }
+  bool bad = false;
+  for (int c = 0; c < COMPS; ++c) {
+    C[e * COMPS + c] = out[c];
+    bad |= !isfinite(out[c]);
+  }
+  if (bad) atomicOr(status, 1);
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+
+cudaError_t oz_scan_launch(int by_cols, const double* X, int64_t ld, int rows, int cols, int comps,
+                           int c0, int c1, int* E, int* L, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  if (by_cols) {
+    scan_cols_kernel<<<(cols + 127) / 128, 128, 0, s>>>(X, ld, rows, cols, comps, c0, c1, E, L);
+  } else {
+    int64_t threads = static_cast<int64_t>(rows) * 32;
+    scan_rows_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(X, ld, rows, cols, comps,
+                                                                       c0, c1, E, L);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t oz_residues_launch(int by_cols, const double* X, int64_t ld, int rows, int cols,
+                               int comps, int c0, int c1, const int* shift, int N,
+                               const uint8_t* pow2, int xmax, int8_t* R, int64_t rpitch,
+                               int64_t rplane, cudaStream_t s) {
+  int64_t total = static_cast<int64_t>(rows) * cols;
+  if (total <= 0) return cudaSuccess;
+  if (N < 1 || N > kNumMods) return cudaErrorInvalidValue;
+  unsigned blocks = static_cast<unsigned>((total + 255) / 256);
+  if (by_cols)
+    residues_cols_kernel<<<blocks, 256, 0, s>>>(X, ld, rows, cols, comps, c0, c1, shift, N, pow2,
+                                                xmax, R, rpitch, rplane);
+  else
+    residues_rows_kernel<<<blocks, 256, 0, s>>>(X, ld, rows, cols, comps, c0, c1, shift, N, pow2,
+                                                xmax, R, rpitch, rplane);
+  return cudaGetLastError();
+}
+
+cudaError_t oz_combine_launch(int comps, const void* jobs, int njobs, int m, int n, double* C,
+                              int* status, cudaStream_t s) {
+  int64_t total = static_cast<int64_t>(m) * n;
+  if (total <= 0) return cudaSuccess;
+  unsigned blocks = static_cast<unsigned>((total + 127) / 128);
+  const CrtJob* J = static_cast<const CrtJob*>(jobs);
+  if (comps == 2)
+    combine_kernel<2><<<blocks, 128, 0, s>>>(J, njobs, m, n, C, status);
+  else
+    combine_kernel<4><<<blocks, 128, 0, s>>>(J, njobs, m, n, C, status);
+  return cudaGetLastError();
+}
+
+}  // namespace mpmm

@@ -1,0 +1,87 @@
+"""The exact int8 tensor-core mode: exact product, correctly rounded."""
+
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle import exact
+import paper_1710_01839_b200 as mp
+from paper_1710_01839_b200 import inputs
+from paper_1710_01839_b200.matrix import DenseMatrix
+from paper_1710_01839_b200.tensor import matmul_exact, plan
+from paper_1710_01839_b200.verify import exact_bound_ratio
+
+pytestmark = pytest.mark.gpu
+
+
+def M(x, prec):
+    return DenseMatrix(x.shape[0], x.shape[1], prec, np.ascontiguousarray(x))
+
+
+def _exact_entry(a, b, i, j):
+    return sum(sum(Fraction(float(v)) for v in a[i, k]) * sum(Fraction(float(v)) for v in b[k, j])
+               for k in range(a.shape[1]))
+
+
+def _rn_expansion(x, comps):
+    out = []
+    for _ in range(comps):
+        d = float(x)          # Fraction -> nearest double
+        out.append(d)
+        x -= Fraction(d)
+    return out
+
+
+@pytest.mark.parametrize("tok,shape,wide", [("dd", (20, 33, 17), False), ("dd", (9, 64, 11), True),
+                                            ("qd", (12, 10, 9), False)])
+def test_exact_and_correctly_rounded(gpu, tok, shape, wide):
+    prec = mp.PrecisionSpec.parse(tok)
+    a, b = inputs.gemm_inputs(tok, *shape, seed=7, wide=wide)
+    c = matmul_exact(M(a, prec), M(b, prec)).data
+    for i, j in ((0, 0), (shape[0] - 1, shape[2] - 1), (3, 5)):
+        want = _rn_expansion(_exact_entry(a, b, i, j), prec.comps)
+        assert list(c[i, j]) == want, (i, j)
+
+
+def test_plan_splits_wide_and_qd(gpu):
+    import torch
+    a, b = inputs.gemm_inputs("dd", 64, 64, 64, seed=1)
+    jobs = plan(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    assert len(jobs) == 1 and jobs[0][2] <= 54
+    a, b = inputs.gemm_inputs("qd", 32, 32, 32, seed=1)
+    jobs = plan(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    assert len(jobs) == 4          # hi/lo x hi/lo
+
+
+def test_integers_and_zero_rows(gpu):
+    dd = mp.PrecisionSpec.dd()
+    a = np.zeros((6, 5, 2))
+    b = np.zeros((5, 4, 2))
+    a[1:, :, 0] = np.arange(25).reshape(5, 5) - 12
+    b[..., 0] = np.arange(20).reshape(5, 4) % 7
+    c = matmul_exact(M(a, dd), M(b, dd)).data
+    assert np.array_equal(c[..., 0], a[..., 0] @ b[..., 0]) and not c[..., 1].any()
+
+
+@pytest.mark.parametrize("wide", [False, True])
+def test_cfg1_every_entry_and_speed(gpu, wide):
+    import torch
+    dd = mp.PrecisionSpec.dd()
+    A, B = inputs.gemm_inputs_device("dd", 1024, 1024, 1024, seed=0, wide=wide)
+    Am, Bm = DenseMatrix(1024, 1024, dd, A), DenseMatrix(1024, 1024, dd, B)
+    c = matmul_exact(Am, Bm)
+    worst, r, _ = exact_bound_ratio(Am, Bm, c)
+    ref = mp.matmul_block(Am, Bm, 32)
+    worst_ref, _, _ = exact_bound_ratio(Am, Bm, ref)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(3):
+        matmul_exact(Am, Bm)
+    e.record()
+    e.synchronize()
+    t = s.elapsed_time(e) / 3e3
+    print(f"tensor mode DD 1024^3 wide={wide}: max ratio {worst:.3e} (mirror {worst_ref:.3e}), "
+          f"{t*1e3:.3f} ms, {2*1024**3/t/1e9:.1f} G 2mnl/s")
+    assert worst <= worst_ref and worst <= 1e-3
