@@ -198,9 +198,10 @@ int mpmm_int8_gemm_batched_dev(int64_t m, int64_t n, int64_t k, int64_t batch, c
 /* CRT reconstruction of njobs jobs (device array of 56-byte records {G,
  * srow, scol, table: pointers; N, K: int32; gpitch, gplane: int64}), exact
  * sum, rounding to comps doubles per entry of C (m x n); *status |= 1
- * non-finite, 2 window. */
+ * non-finite, 2 window.  host_jobs: the same records in host memory (lets a
+ * single job take the register-resident kernel), or NULL. */
 int mpmm_oz_combine_dev(int comps, const void *jobs, int njobs, int64_t m, int64_t n, double *C,
-                        int *status, void *stream);
+                        int *status, const void *host_jobs, void *stream);
 
 /* FP64 roofline micro-benchmark: blocks x threads threads each run 8
  * independent chains of `iters` DFMA (op 0) or DADD (op 1). */

@@ -66,7 +66,7 @@ _SIGNATURES = {
     "mpmm_oz_residues_dev": [_INT, _INT, _INT, _INT, _I64, _I64, _VP, _I64, _VP, _INT, _VP, _INT,
                              _VP, _I64, _I64, _VP],
     "mpmm_int8_gemm_batched_dev": [_I64, _I64, _I64, _I64, _VP, _VP, _VP, _VP, _I64, _VP],
-    "mpmm_oz_combine_dev": [_INT, _VP, _INT, _I64, _I64, _VP, _VP, _VP],
+    "mpmm_oz_combine_dev": [_INT, _VP, _INT, _I64, _I64, _VP, _VP, _VP, _VP],
     "mpmm_exact_check_dev": [_INT, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _VP,
                              _I64, _INT, _VP, _VP],
     "mpmm_host_frobenius_norm": [_INT, _D, _I64, _D],
@@ -310,9 +310,9 @@ def int8_gemm_batched_dev(m, n, k, batch, A, Bt, C, workspace, ws_bytes, stream=
                                             stream))
 
 
-def oz_combine_dev(comps, jobs, njobs, m, n, C, status, stream=None):
+def oz_combine_dev(comps, jobs, njobs, m, n, C, status, host_jobs=None, stream=None):
     sync_device()
-    check(load().mpmm_oz_combine_dev(comps, jobs, njobs, m, n, C, status, stream))
+    check(load().mpmm_oz_combine_dev(comps, jobs, njobs, m, n, C, status, host_jobs, stream))
 
 
 def fp64_burn_dev(op, blocks, threads, iters, scratch, stream=None):

@@ -540,11 +540,11 @@ int mpmm_int8_gemm_batched_dev(int64_t m, int64_t n, int64_t k, int64_t batch, c
 }
 
 int mpmm_oz_combine_dev(int comps, const void* jobs, int njobs, int64_t m, int64_t n, double* C,
-                        int* status, void* stream) {
+                        int* status, const void* host_jobs, void* stream) {
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
   if (njobs < 1 || !dims_ok(m, 0, n)) return fail(MPMM_ERR_ARG, "bad shape");
   cudaError_t e = oz_combine_launch(comps, jobs, njobs, (int)m, (int)n, C, status,
-                                    (cudaStream_t)stream);
+                                    (cudaStream_t)stream, host_jobs);
   return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "combine launch");
 }
 

@@ -101,7 +101,7 @@ cudaError_t oz_residues_launch(int by_cols, const double* X, int64_t ld, int row
                                const uint8_t* pow2, int xmax, int8_t* R, int64_t rpitch,
                                int64_t rplane, cudaStream_t s);
 cudaError_t oz_combine_launch(int comps, const void* jobs, int njobs, int m, int n, double* C,
-                              int* status, cudaStream_t s);
+                              int* status, cudaStream_t s, const void* host_job);
 int int8_gemm_batched(int64_t m, int64_t n, int64_t k, int64_t batch, const int8_t* A,
                       const int8_t* Bt, int32_t* C, void* workspace, size_t ws_size,
                       cudaStream_t stream, std::string* err);

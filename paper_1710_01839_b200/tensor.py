@@ -186,7 +186,7 @@ def matmul_exact_tensors(A, B):
     C = torch.empty((m, n, comps), dtype=torch.float64, device=dev)
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     _cuda.oz_combine_dev(comps, drec.data_ptr(), len(recs), m, n, C.data_ptr(),
-                         status.data_ptr(), stream)
+                         status.data_ptr(), rec.ctypes.data, stream)
     st = int(status.item())
     if st & 2:
         raise NotRepresentable("CRT combine window exceeded")
