@@ -277,7 +277,7 @@ def matmul_simple(a, b, threads=1):
     return _result(_check_finite(c, flag), home)
 
 
-MODES = ("exact", "fast")
+MODES = ("exact", "fast", "tensor")
 
 
 def matmul_block(a, b, n_min, threads=1, *, mode="exact"):
@@ -286,7 +286,9 @@ def matmul_block(a, b, n_min, threads=1, *, mode="exact"):
 
     ``mode="fast"`` (DD only) opts into the faithful 15-instruction DD
     sequence: within the north_star bound 4 l u (|A||B|)_ij (u = 2^-104) but
-    NOT bit-identical to the reference."""
+    NOT bit-identical to the reference.
+    ``mode="tensor"`` (DD and QD) returns the exact product rounded once,
+    computed on the int8 tensor cores (``tensor.py``); n_min is ignored."""
     _check_pair(a, b, threads)
     if n_min < 1:
         raise ValueError("block size must be positive")
@@ -294,6 +296,11 @@ def matmul_block(a, b, n_min, threads=1, *, mode="exact"):
         raise ValueError(f"unknown mode {mode!r}; expected one of {MODES}")
     if mode == "fast" and a.prec.kind is not Kind.DD:
         raise ValueError("the fast accuracy mode is implemented for DD only")
+    if mode == "tensor":
+        if not backend.is_cuda():
+            raise ValueError("the tensor mode runs on the cuda backend only")
+        from .tensor import matmul_exact
+        return matmul_exact(a, b)
     if backend.is_cuda() and not a.is_device and not b.is_device:
         algo = _cuda.ALGO_BLOCK_FAST if mode == "fast" else _cuda.ALGO_BLOCK
         return _host_product(a, b, algo, n_min)
