@@ -213,13 +213,14 @@ struct EntryParts {
 
   __device__ __forceinline__ unsigned residue(int t, unsigned p, unsigned mu, unsigned c32,
                                               const uint8_t* pow2, int xmax) const {
+    // terms mr * 2^e mod-p factor stay below 2^16; negative terms add
+    // p * 2^16 - term, so the sum stays positive and < 2^(17 + log2 NC)
     unsigned acc = 0;
 #pragma unroll
     for (int q = 0; q < NC; ++q) {
       unsigned mr = barrett(mhi[q] * c32 + barrett(mlo[q], mu, p), mu, p);
-      unsigned term = barrett(mr * pow2[t * xmax + ex[q]], mu, p);
-      term = use[q] ? term : 0u;
-      acc += neg[q] ? p - term : term;
+      unsigned term = use[q] ? mr * pow2[t * xmax + ex[q]] : 0u;
+      acc += neg[q] ? (p << 16) - term : term;
     }
     int r = static_cast<int>(barrett(acc, mu, p));
     if (r >= static_cast<int>((p + 1) / 2)) r -= static_cast<int>(p);   // [-(p-1)/2, p/2)
@@ -281,90 +282,6 @@ residues_kernel(const double* __restrict__ X, int64_t ld, int rows, int cols, in
 // CRT reconstruction + exact combination + rounding to DD/QD
 // ---------------------------------------------------------------------------
 
-constexpr int kMaxLimbs = 13;    // P < 2^363 -> 12 limbs (+1 for the weighted sum)
-constexpr int kWin = 28;         // accumulator window: 28 x 32 = 896 bits
-
-// double of a limb vector (top 3 limbs suffice for ~2^-60 relative accuracy)
-__device__ double limbs_to_double(const uint32_t* v, int n) {
-  double d = 0.0;
-  int top = n - 1;
-  while (top > 0 && v[top] == 0) --top;
-  for (int q = top; q >= 0 && q >= top - 2; --q) d += ldexp(static_cast<double>(v[q]), 32 * q);
-  return d;
-}
-
-// add (sign ? -1 : +1) * X * 2^bitshift into the signed digit window
-__device__ void win_add(int64_t* win, const uint32_t* X, int nx, int bitshift, bool neg) {
-  int q0 = bitshift >> 5, r = bitshift & 31;
-  for (int q = 0; q < nx; ++q) {
-    uint64_t v = static_cast<uint64_t>(X[q]) << r;       // < 2^63
-    int64_t lo = static_cast<int64_t>(v & 0xffffffffull), hi = static_cast<int64_t>(v >> 32);
-    if (neg) {
-      lo = -lo;
-      hi = -hi;
-    }
-    if (q0 + q < kWin) win[q0 + q] += lo;
-    if (q0 + q + 1 < kWin) win[q0 + q + 1] += hi;
-  }
-}
-
-// carry-normalise; returns the sign; digits become the magnitude in [0,2^32)
-__device__ bool win_normalize(int64_t* win) {
-  int64_t carry = 0;
-  for (int q = 0; q < kWin; ++q) {
-    int64_t v = win[q] + carry;
-    carry = v >> 32;
-    win[q] = v - (carry << 32);
-  }
-  if (carry >= 0) return false;
-  int64_t c = 1;                                  // two's complement -> magnitude
-  for (int q = 0; q < kWin; ++q) {
-    int64_t v = (0xffffffffll - win[q]) + c;
-    c = v >> 32;
-    win[q] = v & 0xffffffffll;
-  }
-  return true;
-}
-
-// round-to-nearest double of magnitude digits * 2^ebase (top 64 bits + sticky)
-__device__ double win_round(const int64_t* win, int ebase) {
-  int top = kWin - 1;
-  while (top >= 0 && win[top] == 0) --top;
-  if (top < 0) return 0.0;
-  // gather the 96 bits below and including digit `top`, then take 64 + sticky
-  uint64_t hi = static_cast<uint64_t>(win[top]);
-  uint64_t mid = top >= 1 ? static_cast<uint64_t>(win[top - 1]) : 0;
-  uint64_t lo = top >= 2 ? static_cast<uint64_t>(win[top - 2]) : 0;
-  bool sticky = false;
-  for (int q = top - 3; q >= 0; --q) sticky |= (win[q] != 0);
-  int lz = __clzll(static_cast<long long>(hi)) - 32;      // leading zeros within the 32-bit digit
-  // 96-bit value (hi:mid:lo) normalised so its top bit is bit 95
-  unsigned __int128 w = (static_cast<unsigned __int128>(hi) << 64) |
-                        (static_cast<unsigned __int128>(mid) << 32) | lo;
-  w <<= lz;
-  uint64_t top64 = static_cast<uint64_t>(w >> 32);
-  if ((static_cast<uint64_t>(w) & 0xffffffffull) != 0 || sticky) top64 |= 1ull;
-  double d = __ull2double_rn(top64);
-  // value = top64 * 2^(32*(top-2) - lz + 32 - 32) ... top64 holds bits [95-63, 95] of w
-  int e = 32 * (top - 2) - lz + 32 + ebase;
-  return ldexp(d, e);
-}
-
-// subtract the double d (an integer multiple of 2^ebase) from the window
-__device__ void win_sub_double(int64_t* win, double d, int ebase) {
-  if (d == 0.0) return;
-  unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(d));
-  int be = static_cast<int>((b >> 52) & 0x7ff);
-  unsigned long long m = b & ((1ull << 52) - 1);
-  if (be > 0) m |= (1ull << 52);
-  int e = (be > 0 ? be - 1075 : -1074) - ebase;
-  int tz = __ffsll(static_cast<long long>(m)) - 1;
-  m >>= tz;
-  e += tz;                     // >= 0
-  uint32_t limbs[3] = {static_cast<uint32_t>(m), static_cast<uint32_t>(m >> 32), 0u};
-  win_add(win, limbs, 2, e, (b >> 63) == 0);   // subtract: add with flipped sign
-}
-
 }  // namespace
 
 // Per-job CRT data (device): moduli count, limb count, P limbs, weights.
@@ -376,137 +293,6 @@ struct CrtJob {
   int N, K;
   int64_t gpitch, gplane;
 };
-
-template <int COMPS>
-__global__ void __launch_bounds__(128)
-combine_kernel(const CrtJob* __restrict__ jobs, int njobs, int m, int n,
-               double* __restrict__ C, int* __restrict__ status) {
-  int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= static_cast<int64_t>(m) * n) return;
-  const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
-  // window base: the smallest weight exponent of the jobs
-  int ebase = 1 << 30;
-  for (int J = 0; J < njobs; ++J) ebase = min(ebase, -(jobs[J].srow[i] + jobs[J].scol[j]));
-  int64_t win[kWin];
-#pragma unroll
-  for (int q = 0; q < kWin; ++q) win[q] = 0;
-  for (int J = 0; J < njobs; ++J) {
-    const CrtJob& jb = jobs[J];
-    const int K = jb.K, N = jb.N;
-    const uint32_t* P = jb.table;
-    const uint32_t* W = jb.table + K;
-    uint64_t acc[kMaxLimbs + 1];
-    for (int q = 0; q <= K; ++q) acc[q] = 0;
-    const int32_t* Gij = jb.G + static_cast<int64_t>(i) * jb.gpitch + j;
-    for (int t = 0; t < N; ++t) {
-      int p = kModsDev[t];
-      int g = Gij[t * jb.gplane];
-      uint32_t r = static_cast<uint32_t>(((g % p) + p) % p);
-      for (int q = 0; q < K; ++q) acc[q] += static_cast<uint64_t>(r) * W[t * K + q];
-    }
-    uint32_t S[kMaxLimbs + 1];
-    uint64_t carry = 0;
-    for (int q = 0; q <= K; ++q) {
-      uint64_t v = acc[q] + carry;
-      S[q] = static_cast<uint32_t>(v);
-      carry = v >> 32;
-    }
-    // q = floor(S / P), corrected by one step either way
-    double qd = floor(limbs_to_double(S, K + 1) / limbs_to_double(P, K));
-    uint64_t qv = qd > 0.0 ? static_cast<uint64_t>(qd) : 0ull;
-    // X = S - qv * P (signed, K+1 limbs)
-    int64_t X[kMaxLimbs + 1];
-    int64_t borrow = 0;
-    for (int q = 0; q <= K; ++q) {
-      uint64_t pq = q < K ? static_cast<uint64_t>(P[q]) * qv : 0ull;
-      // compute in 64-bit with split carries
-      int64_t v = static_cast<int64_t>(S[q]) - static_cast<int64_t>(pq & 0xffffffffull) + borrow;
-      borrow = (v >> 32) - static_cast<int64_t>(pq >> 32);
-      X[q] = v & 0xffffffffll;
-    }
-    // borrow < 0: X negative -> add P;  compare X >= P -> subtract P
-    if (borrow < 0) {
-      int64_t c = 0;
-      for (int q = 0; q <= K; ++q) {
-        int64_t v = X[q] + (q < K ? static_cast<int64_t>(P[q]) : 0) + c;
-        c = v >> 32;
-        X[q] = v & 0xffffffffll;
-      }
-    } else {
-      bool ge = X[K] != 0;
-      if (!ge) {
-        ge = true;
-        for (int q = K - 1; q >= 0; --q) {
-          if (X[q] != static_cast<int64_t>(P[q])) {
-            ge = X[q] > static_cast<int64_t>(P[q]);
-            break;
-          }
-        }
-      }
-      if (ge) {
-        int64_t c = 0;
-        for (int q = 0; q <= K; ++q) {
-          int64_t v = X[q] - (q < K ? static_cast<int64_t>(P[q]) : 0) + c;
-          c = v >> 32;
-          X[q] = v & 0xffffffffll;
-        }
-      }
-    }
-    // centre: X > P/2 -> X - P (magnitude P - X, negative)
-    bool upper = false;
-    {
-      // compare 2X with P
-      uint32_t twoX[kMaxLimbs + 1];
-      uint64_t c = 0;
-      for (int q = 0; q <= K; ++q) {
-        uint64_t v = (static_cast<uint64_t>(X[q]) << 1) + c;
-        twoX[q] = static_cast<uint32_t>(v);
-        c = v >> 32;
-      }
-      upper = twoX[K] != 0 || c != 0;
-      if (!upper) {
-        for (int q = K - 1; q >= 0; --q) {
-          if (twoX[q] != P[q]) {
-            upper = twoX[q] > P[q];
-            break;
-          }
-        }
-      }
-    }
-    uint32_t mag[kMaxLimbs];
-    if (upper) {
-      int64_t c = 0;
-      for (int q = 0; q < K; ++q) {
-        int64_t v = static_cast<int64_t>(P[q]) - X[q] + c;
-        c = v >> 32;
-        mag[q] = static_cast<uint32_t>(v & 0xffffffffll);
-      }
-    } else {
-      for (int q = 0; q < K; ++q) mag[q] = static_cast<uint32_t>(X[q]);
-    }
-    const int eJ = -(jb.srow[i] + jb.scol[j]);
-    const int shift = eJ - ebase;
-    if (shift + 32 * K > 32 * kWin) atomicOr(status, 2);    // window too small
-    win_add(win, mag, K, shift, upper);
-  }
-  bool neg = win_normalize(win);
-  // extract COMPS round-to-nearest doubles from the exact value
-  double out[COMPS];
-  for (int c = 0; c < COMPS; ++c) {
-    double d = win_round(win, ebase);
-    out[c] = neg ? -d : d;
-    // remainder: win (magnitude) - d; it may turn negative
-    win_sub_double(win, d, ebase);
-    bool flip = win_normalize(win);
-    neg = neg ^ flip;
-  }
-  bool bad = false;
-  for (int c = 0; c < COMPS; ++c) {
-    C[e * COMPS + c] = out[c];
-    bad |= !isfinite(out[c]);
-  }
-  if (bad) atomicOr(status, 1);
-}
 
 // ---------------------------------------------------------------------------
 // single-job combine: everything in registers (K limbs known at compile time)
@@ -588,25 +374,20 @@ __device__ __forceinline__ double limbs_double(const uint32_t (&v)[K + 1]) {
   return d;
 }
 
-template <int COMPS, int K>
-__global__ void __launch_bounds__(128)
-combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __restrict__ status) {
-  __shared__ uint32_t sW[(kNumMods + 1) * K];
-  for (int q = threadIdx.x; q < (jb.N + 1) * K; q += blockDim.x) sW[q] = jb.table[q];
-  __syncthreads();
-  int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= static_cast<int64_t>(m) * n) return;
-  const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
+// CRT reconstruction of one job's output (i, j): the centred integer X as
+// sign + K magnitude limbs.  sW: P (K limbs) then the N weights (K limbs each).
+template <int K>
+__device__ __forceinline__ bool crt_reconstruct(const int32_t* __restrict__ Gij, int64_t gplane,
+                                                int N, const uint32_t* sW, int64_t (&mag)[K]) {
   const uint32_t* P = sW;
   const uint32_t* W = sW + K;
   uint64_t acc[K + 1];
 #pragma unroll
   for (int q = 0; q <= K; ++q) acc[q] = 0;
-  const int32_t* Gij = jb.G + static_cast<int64_t>(i) * jb.gpitch + j;
 #pragma unroll 2
-  for (int t = 0; t < jb.N; ++t) {
+  for (int t = 0; t < N; ++t) {
     const unsigned p = static_cast<unsigned>(kModsDev[t]);
-    const int g = Gij[t * jb.gplane];
+    const int g = Gij[t * gplane];
     unsigned r = barrett(static_cast<unsigned>(g), kModMu[t], p);
     if (g < 0) {                 // (g + 2^32) mod p  ->  g mod p
       r = r + p - kMod2p32[t];
@@ -638,8 +419,7 @@ combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __re
     borrow = (v >> 32) - static_cast<int64_t>(pq >> 32);
     X[q] = v & 0xffffffffll;
   }
-  // bring X into [0, P): one correction either way
-  {
+  {  // bring X into [0, P): one correction either way
     bool add = borrow < 0;
     bool ge = X[K] != 0;
     if (!add && !ge) {
@@ -667,7 +447,6 @@ combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __re
   bool upper = false, decided = false;
 #pragma unroll
   for (int q = K - 1; q >= 0; --q) {
-    // compare 2X with P limb by limb from the top (2X limbs computed on the fly)
     const uint64_t twoq = ((static_cast<uint64_t>(X[q]) << 1) & 0xffffffffull) |
                           (q > 0 ? static_cast<uint64_t>(X[q - 1]) >> 31 : 0ull);
     if (!decided && twoq != Pl[q]) {
@@ -676,7 +455,6 @@ combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __re
     }
   }
   if ((static_cast<uint64_t>(X[K - 1]) >> 31) != 0 || X[K] != 0) upper = true;
-  int64_t mag[K];
   if (upper) {
     int64_t c = 0;
 #pragma unroll
@@ -689,7 +467,21 @@ combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __re
 #pragma unroll
     for (int q = 0; q < K; ++q) mag[q] = X[q];
   }
-  bool neg = upper;
+  return upper;
+}
+
+template <int COMPS, int K>
+__global__ void __launch_bounds__(128)
+combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __restrict__ status) {
+  __shared__ uint32_t sW[(kNumMods + 1) * K];
+  for (int q = threadIdx.x; q < (jb.N + 1) * K; q += blockDim.x) sW[q] = jb.table[q];
+  __syncthreads();
+  int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= static_cast<int64_t>(m) * n) return;
+  const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
+  int64_t mag[K];
+  bool neg = crt_reconstruct<K>(jb.G + static_cast<int64_t>(i) * jb.gpitch + j, jb.gplane, jb.N,
+                                sW, mag);
   const int ebase = -(jb.srow[i] + jb.scol[j]);
   double out[COMPS];
 #pragma unroll
@@ -700,6 +492,120 @@ combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __re
   }
   bool bad = false;
 #pragma unroll
+  for (int c = 0; c < COMPS; ++c) {
+    C[e * COMPS + c] = out[c];
+    bad |= !isfinite(out[c]);
+  }
+  if (bad) atomicOr(status, 1);
+}
+
+// ---------------------------------------------------------------------------
+// multi-job combine: per-job CRT in registers, the exact sum in a per-thread
+// shared-memory window laid out [digit][thread] (conflict-free for any
+// per-thread digit index)
+// ---------------------------------------------------------------------------
+
+constexpr int kMTB = 128;     // threads per block
+constexpr int kMWin = 28;     // window digits (896 bits)
+constexpr int kMaxJobs = 16;
+
+template <int COMPS, int K>
+__global__ void __launch_bounds__(kMTB)
+combine_multi_kernel(const CrtJob* __restrict__ jobs, int njobs, int m, int n,
+                     double* __restrict__ C, int* __restrict__ status) {
+  extern __shared__ unsigned char smraw[];
+  int64_t* win = reinterpret_cast<int64_t*>(smraw);                   // [kMWin][kMTB]
+  uint32_t* tabs = reinterpret_cast<uint32_t*>(win + kMWin * kMTB);   // [njobs][(55)*K]
+  const int tstride = (kNumMods + 1) * K;
+  for (int J = 0; J < njobs; ++J)
+    for (int q = threadIdx.x; q < (jobs[J].N + 1) * K; q += blockDim.x)
+      tabs[J * tstride + q] = jobs[J].table[q];
+  __syncthreads();
+  const int tid = threadIdx.x;
+  int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + tid;
+  if (e >= static_cast<int64_t>(m) * n) return;
+  const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
+#define WIN(q) win[(q) * kMTB + tid]
+  for (int q = 0; q < kMWin; ++q) WIN(q) = 0;
+  int ebase = 1 << 30;
+  for (int J = 0; J < njobs; ++J) ebase = min(ebase, -(jobs[J].srow[i] + jobs[J].scol[j]));
+  for (int J = 0; J < njobs; ++J) {
+    const CrtJob& jb = jobs[J];
+    int64_t mag[K];
+    const bool neg = crt_reconstruct<K>(jb.G + static_cast<int64_t>(i) * jb.gpitch + j, jb.gplane,
+                                        jb.N, tabs + J * tstride, mag);
+    const int shift = -(jb.srow[i] + jb.scol[j]) - ebase;
+    const int q0 = shift >> 5, r = shift & 31;
+    if (q0 + K + 1 > kMWin) atomicOr(status, 2);
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+      uint64_t v = static_cast<uint64_t>(mag[p]) << r;
+      int64_t lo = static_cast<int64_t>(v & 0xffffffffull), hi = static_cast<int64_t>(v >> 32);
+      if (neg) {
+        lo = -lo;
+        hi = -hi;
+      }
+      if (q0 + p < kMWin) WIN(q0 + p) += lo;
+      if (q0 + p + 1 < kMWin) WIN(q0 + p + 1) += hi;
+    }
+  }
+  auto normalize = [&]() -> bool {
+    int64_t carry = 0;
+    for (int q = 0; q < kMWin; ++q) {
+      int64_t v = WIN(q) + carry;
+      carry = v >> 32;
+      WIN(q) = v - (carry << 32);
+    }
+    if (carry >= 0) return false;
+    int64_t c = 1;
+    for (int q = 0; q < kMWin; ++q) {
+      int64_t v = (0xffffffffll - WIN(q)) + c;
+      c = v >> 32;
+      WIN(q) = v & 0xffffffffll;
+    }
+    return true;
+  };
+  bool neg = normalize();
+  double out[COMPS];
+  for (int c = 0; c < COMPS; ++c) {
+    // round-to-nearest of the magnitude
+    int top = kMWin - 1;
+    while (top >= 0 && WIN(top) == 0) --top;
+    double d = 0.0;
+    if (top >= 0) {
+      uint64_t hi = static_cast<uint64_t>(WIN(top));
+      uint64_t mid = top >= 1 ? static_cast<uint64_t>(WIN(top - 1)) : 0;
+      uint64_t lo = top >= 2 ? static_cast<uint64_t>(WIN(top - 2)) : 0;
+      bool sticky = false;
+      for (int q = top - 3; q >= 0; --q) sticky |= (WIN(q) != 0);
+      int lz = __clzll(static_cast<long long>(hi)) - 32;
+      unsigned __int128 w = (static_cast<unsigned __int128>(hi) << 64) |
+                            (static_cast<unsigned __int128>(mid) << 32) | lo;
+      w <<= lz;
+      uint64_t top64 = static_cast<uint64_t>(w >> 32);
+      if ((static_cast<uint64_t>(w) & 0xffffffffull) != 0 || sticky) top64 |= 1ull;
+      d = ldexp(__ull2double_rn(top64), 32 * (top - 2) - lz + 32 + ebase);
+    }
+    out[c] = neg ? -d : d;
+    if (d != 0.0) {   // subtract d (a multiple of 2^ebase) from the magnitude
+      unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(d));
+      int be = static_cast<int>((b >> 52) & 0x7ff);
+      unsigned long long mm = b & ((1ull << 52) - 1);
+      if (be > 0) mm |= (1ull << 52);
+      int ee = (be > 0 ? be - 1075 : -1074) - ebase;
+      int tz = __ffsll(static_cast<long long>(mm)) - 1;
+      mm >>= tz;
+      ee += tz;
+      int q0 = ee >> 5, rr = ee & 31;
+      unsigned __int128 ww = static_cast<unsigned __int128>(mm) << rr;
+      for (int u = 0; u < 3; ++u)
+        if (q0 + u < kMWin)
+          WIN(q0 + u) -= static_cast<int64_t>(static_cast<uint32_t>(ww >> (32 * u)));
+    }
+    neg = neg ^ normalize();
+  }
+#undef WIN
+  bool bad = false;
   for (int c = 0; c < COMPS; ++c) {
     C[e * COMPS + c] = out[c];
     bad |= !isfinite(out[c]);
@@ -783,22 +689,46 @@ static cudaError_t combine_single(const CrtJob& jb, int m, int n, double* C, int
   return cudaGetLastError();
 }
 
+template <int COMPS>
+static cudaError_t combine_multi(const void* jobs, int njobs, int K, int m, int n, double* C,
+                                 int* status, unsigned blocks, cudaStream_t s) {
+  const CrtJob* J = static_cast<const CrtJob*>(jobs);
+  const size_t smem = static_cast<size_t>(kMWin) * kMTB * sizeof(int64_t) +
+                      static_cast<size_t>(njobs) * (kNumMods + 1) * K * sizeof(uint32_t);
+  switch (K) {
+#define MPMM_K(KK)                                                                            \
+  case KK:                                                                                    \
+    cudaFuncSetAttribute(combine_multi_kernel<COMPS, KK>,                                     \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
+    combine_multi_kernel<COMPS, KK><<<blocks, kMTB, smem, s>>>(J, njobs, m, n, C, status);    \
+    break;
+    MPMM_K(1) MPMM_K(2) MPMM_K(3) MPMM_K(4) MPMM_K(5) MPMM_K(6) MPMM_K(7) MPMM_K(8) MPMM_K(9)
+    MPMM_K(10) MPMM_K(11) MPMM_K(12)
+#undef MPMM_K
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t oz_combine_launch(int comps, const void* jobs, int njobs, int m, int n, double* C,
                               int* status, cudaStream_t s, const void* host_job) {
   int64_t total = static_cast<int64_t>(m) * n;
   if (total <= 0) return cudaSuccess;
-  unsigned blocks = static_cast<unsigned>((total + 127) / 128);
-  if (njobs == 1 && host_job != nullptr) {
-    const CrtJob& jb = *static_cast<const CrtJob*>(host_job);
-    return comps == 2 ? combine_single<2>(jb, m, n, C, status, blocks, s)
-                      : combine_single<4>(jb, m, n, C, status, blocks, s);
+  if (host_job == nullptr || njobs < 1 || njobs > kMaxJobs) return cudaErrorInvalidValue;
+  const CrtJob* hj = static_cast<const CrtJob*>(host_job);
+  int K = 0;
+  for (int q = 0; q < njobs; ++q) K = hj[q].K > K ? hj[q].K : K;
+  for (int q = 0; q < njobs; ++q)
+    if (hj[q].K != K) return cudaErrorInvalidValue;   // host pads every table to one K
+  if (njobs == 1) {
+    unsigned blocks = static_cast<unsigned>((total + 127) / 128);
+    return comps == 2 ? combine_single<2>(*hj, m, n, C, status, blocks, s)
+                      : combine_single<4>(*hj, m, n, C, status, blocks, s);
   }
-  const CrtJob* J = static_cast<const CrtJob*>(jobs);
-  if (comps == 2)
-    combine_kernel<2><<<blocks, 128, 0, s>>>(J, njobs, m, n, C, status);
-  else
-    combine_kernel<4><<<blocks, 128, 0, s>>>(J, njobs, m, n, C, status);
-  return cudaGetLastError();
+  unsigned blocks = static_cast<unsigned>((total + kMTB - 1) / kMTB);
+  return comps == 2 ? combine_multi<2>(jobs, njobs, K, m, n, C, status, blocks, s)
+                    : combine_multi<4>(jobs, njobs, K, m, n, C, status, blocks, s);
 }
 
 }  // namespace mpmm

@@ -55,13 +55,21 @@ def moduli_count(bits):
     return None
 
 
-@lru_cache(maxsize=None)
-def crt_table(N):
-    """uint32 limbs: P (K limbs) then the N CRT weights W_t = M_t (M_t^-1 mod p_t) mod P."""
+def crt_limbs(N):
     P = 1
     for p in MODULI[:N]:
         P *= p
-    K = (P.bit_length() + 31) // 32
+    return (P.bit_length() + 31) // 32
+
+
+@lru_cache(maxsize=None)
+def crt_table(N, K=None):
+    """uint32 limbs: P (K limbs) then the N CRT weights W_t = M_t (M_t^-1 mod p_t) mod P
+    (K defaults to the limbs P needs; a larger K zero-pads every entry)."""
+    P = 1
+    for p in MODULI[:N]:
+        P *= p
+    K = K or crt_limbs(N)
     words = []
 
     def limbs(x):
@@ -155,28 +163,46 @@ def matmul_exact_tensors(A, B):
     ws = torch.empty(WORKSPACE_BYTES, dtype=torch.uint8, device=dev)
     pad = lambda x: -(-x // 16) * 16  # noqa: E731  (cuBLASLt IMMA alignment)
     mp_, np_, lp = pad(m), pad(n), pad(l)
+    K = max(crt_limbs(N) for _, _, N, _, _, _, _ in jobs)
+    # residues once per operand component range, with the most moduli any
+    # job using that range needs (a job reads the leading planes)
+    need = {}
+    for ra, rb, N, ba, bb, sa, sb in jobs:
+        need[("a", ra)] = max(need.get(("a", ra), 0), N)
+        need[("b", rb)] = max(need.get(("b", rb), 0), N)
+    xmax = max(max(j[3], j[4]) for j in jobs) + 8
+    res = {}
+    alloc = torch.zeros if (mp_, np_, lp) != (m, n, l) else torch.empty
+    for ra, rb, N, ba, bb, sa, sb in jobs:
+        for side, rng, sh in (("a", ra, sa), ("b", rb, sb)):
+            if (side, rng) in res:
+                continue
+            Nr = need[(side, rng)]
+            pow2 = _device_const(("pow2", Nr, xmax), pow2_table(Nr, xmax), dev)
+            dsh = torch.from_numpy(sh).to(dev)
+            if side == "a":
+                R = alloc((Nr, mp_, lp), dtype=torch.int8, device=dev)
+                _cuda.oz_residues_dev(0, comps, rng[0], rng[1], m, l, A.data_ptr(), l,
+                                      dsh.data_ptr(), Nr, pow2.data_ptr(), xmax, R.data_ptr(),
+                                      lp, mp_ * lp, stream)
+            else:
+                R = alloc((Nr, np_, lp), dtype=torch.int8, device=dev)
+                _cuda.oz_residues_dev(1, comps, rng[0], rng[1], l, n, B.data_ptr(), n,
+                                      dsh.data_ptr(), Nr, pow2.data_ptr(), xmax, R.data_ptr(),
+                                      lp, np_ * lp, stream)
+            res[(side, rng)] = (R, dsh)
     keep, recs = [], []
     for ra, rb, N, ba, bb, sa, sb in jobs:
-        xmax = max(ba, bb) + 8
-        pow2 = _device_const(("pow2", N, xmax), pow2_table(N, xmax), dev)
-        table_h, K = crt_table(N)
-        table = _device_const(("crt", N), table_h, dev)
-        dsa = torch.from_numpy(sa).to(dev)
-        dsb = torch.from_numpy(sb).to(dev)
-        alloc = torch.zeros if (mp_, np_, lp) != (m, n, l) else torch.empty
-        RA = alloc((N, mp_, lp), dtype=torch.int8, device=dev)
-        RB = alloc((N, np_, lp), dtype=torch.int8, device=dev)
-        _cuda.oz_residues_dev(0, comps, ra[0], ra[1], m, l, A.data_ptr(), l, dsa.data_ptr(), N,
-                              pow2.data_ptr(), xmax, RA.data_ptr(), lp, mp_ * lp, stream)
-        _cuda.oz_residues_dev(1, comps, rb[0], rb[1], l, n, B.data_ptr(), n, dsb.data_ptr(), N,
-                              pow2.data_ptr(), xmax, RB.data_ptr(), lp, np_ * lp, stream)
+        RA, dsa = res[("a", ra)]
+        RB, dsb = res[("b", rb)]
+        table = _device_const(("crt", N, K), crt_table(N, K)[0], dev)
         G = torch.empty((N, mp_, np_), dtype=torch.int32, device=dev)
         _cuda.int8_gemm_batched_dev(mp_, np_, lp, N, RA.data_ptr(), RB.data_ptr(), G.data_ptr(),
                                     ws.data_ptr(), WORKSPACE_BYTES, stream)
-        del RA, RB
         keep += [G, dsa, dsb]
         recs.append((G.data_ptr(), dsa.data_ptr(), dsb.data_ptr(), table.data_ptr(), N, K,
                      np_, mp_ * np_))
+    del res
     rec = np.zeros(len(recs), dtype=np.dtype([("G", "<u8"), ("sr", "<u8"), ("sc", "<u8"),
                                               ("tb", "<u8"), ("N", "<i4"), ("K", "<i4"),
                                               ("gp", "<i8"), ("gl", "<i8")]))

@@ -278,3 +278,31 @@ def test_row_shards_cover_exactly():
             assert lo % align == 0 or lo == m
     assert shard.panel_bounds(10, 4) == [(0, 4), (4, 8), (8, 10)]
     assert shard.panel_bounds(10, None) == [(0, 10)]
+
+
+# --- tensor mode host tables ----------------------------------------------------
+
+def test_tensor_moduli_and_crt_tables():
+    import math
+    import random
+    from paper_1710_01839_b200 import tensor
+    mods = tensor.MODULI
+    assert len(mods) == 54 and all(math.gcd(a, b) == 1 for i, a in enumerate(mods)
+                                   for b in mods[:i])
+    assert all(p <= 256 for p in mods)
+    assert tensor.moduli_count(300) is not None and tensor.moduli_count(400) is None
+    N = tensor.moduli_count(250)
+    words, K = tensor.crt_table(N)
+    limbs = lambda q: sum(int(words[q * K + t]) << (32 * t) for t in range(K))  # noqa: E731
+    P, W = limbs(0), [limbs(1 + t) for t in range(N)]
+    assert P == math.prod(mods[:N]) and P > 1 << 250
+    rng = random.Random(1)
+    for _ in range(20):
+        x = rng.randrange(-(P // 2), P // 2)
+        r = [x % p for p in mods[:N]]
+        X = sum(ri * wi for ri, wi in zip(r, W)) % P
+        assert (X if X <= P // 2 else X - P) == x
+    padded, K2 = tensor.crt_table(N, K + 2)
+    assert K2 == K + 2 and int(padded[K2 * 1 + K]) == 0
+    pt = tensor.pow2_table(3, 40)
+    assert all(int(pt[i, x]) == pow(2, x, mods[i]) for i in range(3) for x in range(40))
