@@ -43,6 +43,9 @@ extern "C" {
  * within the north_star bound 4 l u (|A||B|)_ij, u = 2^-104; NOT
  * bit-identical to the reference.  DD only. */
 #define MPMM_ALGO_BLOCK_FAST 2
+/* Strassen (reference matmul_strassen, multiply.py:267-338): n_min is the
+ * leaf block size, `cutoff` the recursion threshold. */
+#define MPMM_ALGO_STRASSEN 3
 
 int mpmm_abi_version(void);
 const char *mpmm_last_error(void);
@@ -205,6 +208,56 @@ int mpmm_oz_combine_dev(int comps, const void *jobs, int njobs, int64_t m, int64
 
 /* FP64 roofline micro-benchmark: blocks x threads threads each run 8
  * independent chains of `iters` DFMA (op 0) or DADD (op 1). */
+/* C = A*B by the reference's Strassen recursion (multiply.py:267-338), bit
+ * for bit: a node of size <= cutoff (all of m, l, n) is a leaf, computed by
+ * the blocked kernel with block size leaf_n_min from a zero accumulator;
+ * odd dimensions are zero-padded to even (multiply.py:206-260).  Square
+ * inputs are the reference's algorithm; rectangular m x l x n halves each
+ * dimension (the BASELINE config-3 extension).  Runs level-synchronously
+ * (one batched launch per level and operand shape, one launch for all
+ * leaves), depth first at the top when the scratch would exceed 60% of
+ * free device memory.  stats: optional HOST int64[2] receiving the
+ * reference's operation counts {multiplications, additions}
+ * (multiply.py:322-331).  nonfinite: optional device flag as above. */
+int mpmm_strassen_dev(int comps, int64_t cutoff, int64_t leaf_n_min, int64_t m, int64_t l,
+                      int64_t n, const double *A, int64_t lda, const double *B, int64_t ldb,
+                      double *C, int64_t ldc, int *nonfinite, int64_t *stats, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Multi-GPU runtime (single process).  The library owns, per
+ * device, a compute stream, a communication stream and an NCCL
+ * communicator.  Not needed by the Python package (one process per GPU
+ * over torch.distributed, shard.py); for C/C++ callers.
+ * ------------------------------------------------------------------------- */
+
+/* Create the runtime over `ngpus` devices: devices[0..ngpus) or, when
+ * devices is NULL, 0..ngpus-1.  Error if already initialized. */
+int mpmm_init(int ngpus, const int *devices);
+/* Destroy the communicators and streams (no-op when not initialized). */
+int mpmm_finalize(void);
+/* The runtime's device count (0 when not initialized) and ids. */
+int mpmm_runtime_gpus(int *ngpus, int *devices, int cap);
+/* c (m x n) = a*b from HOST buffers on the runtime's GPUs: C's rows are
+ * split in 64-row-aligned blocks, one per GPU, each GPU receiving its rows
+ * of a directly; b goes to the first GPU and is broadcast by NCCL in
+ * `panels` k-panels (<= 0: automatic) overlapped with the per-panel GEMM.
+ * algo SIMPLE / BLOCK / BLOCK_FAST (n_min) or STRASSEN (n_min = leaf block
+ * size, cutoff; per-GPU rectangular Strassen).  Bitwise independent of the
+ * GPU count and the panel split for SIMPLE/BLOCK.  nonfinite: optional
+ * host int.  device_ms: optional, the max over GPUs of the device time
+ * from the first copy to the last (CUDA events). */
+int mpmm_gemm_multi(int comps, int algo, int64_t n_min, int64_t cutoff, int64_t m, int64_t l,
+                    int64_t n, const double *a, const double *b, double *c, int64_t panels,
+                    int *nonfinite, double *device_ms);
+
+/* Event timers on a stream (TimingPolicy's device clock, timing.py:22-59). */
+int mpmm_timer_create(void **timer);
+int mpmm_timer_start(void *timer, void *stream);
+int mpmm_timer_stop(void *timer, void *stream);
+/* Waits for the stop event; milliseconds between start and stop. */
+int mpmm_timer_elapsed_ms(void *timer, float *ms);
+int mpmm_timer_destroy(void *timer);
+
 int mpmm_fp64_burn_dev(int op, int blocks, int threads, int64_t iters, double *scratch,
                        void *stream);
 

@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmpmm_cuda.so")
 SOURCES = ["gemm_dd.cu", "gemm_qd.cu", "ewise.cu", "verify.cu", "rng.cu", "ozaki.cu", "int8gemm.cpp",
-           "capi.cu", "host_norms.cpp"]
+           "strassen.cpp", "runtime.cpp", "capi.cu", "host_norms.cpp"]
 HEADERS = ["ddqd.cuh", "common.cuh", "kernels.h", "gemm.cuh"]
 
 # -fmad=false: no implicit contraction (the reference is built with
@@ -21,7 +21,7 @@ NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo", "-fmad=false",
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math", "-shared",
-    "-lcublasLt", "-Xlinker", "-rpath,/usr/local/cuda/lib64",
+    "-lcublasLt", "-ldl", "-Xlinker", "-rpath,/usr/local/cuda/lib64",
 ]
 
 

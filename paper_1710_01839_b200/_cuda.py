@@ -69,6 +69,18 @@ _SIGNATURES = {
     "mpmm_oz_combine_dev": [_INT, _VP, _INT, _I64, _I64, _VP, _VP, _VP, _VP],
     "mpmm_exact_check_dev": [_INT, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _VP,
                              _I64, _INT, _VP, _VP],
+    "mpmm_strassen_dev": [_INT, _I64, _I64, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64,
+                          _VP, _VP, _VP],
+    "mpmm_init": [_INT, _VP],
+    "mpmm_finalize": [],
+    "mpmm_runtime_gpus": [ctypes.POINTER(_INT), _VP, _INT],
+    "mpmm_gemm_multi": [_INT, _INT, _I64, _I64, _I64, _I64, _I64, _D, _D, _D, _I64,
+                        ctypes.POINTER(_INT), ctypes.POINTER(ctypes.c_double)],
+    "mpmm_timer_create": [ctypes.POINTER(_VP)],
+    "mpmm_timer_start": [_VP, _VP],
+    "mpmm_timer_stop": [_VP, _VP],
+    "mpmm_timer_elapsed_ms": [_VP, ctypes.POINTER(ctypes.c_float)],
+    "mpmm_timer_destroy": [_VP],
     "mpmm_host_frobenius_norm": [_INT, _D, _I64, _D],
     "mpmm_host_frobenius_rel_diff": [_INT, _D, _D, _I64, _D],
 }
@@ -76,6 +88,7 @@ _SIGNATURES = {
 ALGO_SIMPLE = 0
 ALGO_BLOCK = 1
 ALGO_BLOCK_FAST = 2   # opt-in faithful DD sequence (not bit-identical)
+ALGO_STRASSEN = 3     # mpmm_gemm_multi only
 
 
 def load():
@@ -257,6 +270,71 @@ def ewise_batched_dev(comps, batch, rows, cols, problems, stream=None):
     """``problems``: device pointer to ``batch`` x 14 int64 (see mpmm_cuda.h)."""
     sync_device()
     check(load().mpmm_ewise_batched_dev(comps, batch, rows, cols, problems, stream))
+
+
+def strassen_dev(comps, cutoff, leaf_n_min, m, l, n, A, lda, B, ldb, C, ldc, nonfinite=None,
+                 stats=None, stream=None):
+    """``stats``: optional ctypes int64[2] receiving {multiplications, additions}."""
+    sync_device()
+    check(load().mpmm_strassen_dev(comps, cutoff, leaf_n_min, m, l, n, A, lda, B, ldb, C, ldc,
+                                   nonfinite, stats, stream))
+
+
+def runtime_init(ngpus, devices=None):
+    """Single-process multi-GPU runtime (NCCL communicators owned by the library).
+    torch is imported first so the library binds the NCCL build torch uses."""
+    import torch  # noqa: F401
+    arr = None
+    if devices is not None:
+        arr = (ctypes.c_int * len(devices))(*devices)
+        ngpus = len(devices)
+    check(load().mpmm_init(ngpus, ctypes.cast(arr, ctypes.c_void_p) if arr else None))
+
+
+def runtime_finalize():
+    check(load().mpmm_finalize())
+
+
+def runtime_gpus():
+    n = _INT(0)
+    ids = (ctypes.c_int * 64)()
+    check(load().mpmm_runtime_gpus(ctypes.byref(n), ctypes.cast(ids, ctypes.c_void_p), 64))
+    return list(ids[:n.value])
+
+
+def gemm_multi(comps, algo, n_min, cutoff, a, b, c, panels=0):
+    """c = a*b (host float64 arrays (m,l,comps) / (l,n,comps) / (m,n,comps)) on
+    the runtime's GPUs; returns (nonfinite, device_ms)."""
+    m, l, n = a.shape[0], a.shape[1], b.shape[1]
+    bad, ms = _INT(0), ctypes.c_double(0.0)
+    check(load().mpmm_gemm_multi(comps, algo, n_min, cutoff, m, l, n, _arr(a, comps),
+                                 _arr(b, comps), _arr(c, comps), panels, ctypes.byref(bad),
+                                 ctypes.byref(ms)))
+    return bool(bad.value), ms.value
+
+
+class Timer:
+    """Device event timer (mpmm_timer_*), start/stop on a stream."""
+
+    def __init__(self):
+        self._t = ctypes.c_void_p()
+        check(load().mpmm_timer_create(ctypes.byref(self._t)))
+
+    def start(self, stream=None):
+        check(load().mpmm_timer_start(self._t, stream))
+
+    def stop(self, stream=None):
+        check(load().mpmm_timer_stop(self._t, stream))
+
+    def elapsed_ms(self):
+        ms = ctypes.c_float(0.0)
+        check(load().mpmm_timer_elapsed_ms(self._t, ctypes.byref(ms)))
+        return ms.value
+
+    def __del__(self):
+        if getattr(self, "_t", None) and _lib is not None:
+            _lib.mpmm_timer_destroy(self._t)
+            self._t = None
 
 
 def block_cells_dev(comps, n_min, cell0, cell1, m, l, n, A, lda, B, ldb, C, ldc, stream=None):

@@ -14,6 +14,18 @@
 
 using namespace mpmm;
 
+namespace mpmm {
+cudaError_t strassen_run(int comps, int64_t cutoff, int tile, int64_t m, int64_t l, int64_t n,
+                         const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                         int64_t ldc, int64_t* stats, cudaStream_t stream);
+int rt_init(const int* devs, int ndev, std::string* err);
+int rt_finalize();
+int rt_gpus(int* ids, int cap);
+int rt_gemm_host(int comps, int algo, int tile, int64_t cutoff, int64_t m, int64_t l, int64_t n,
+                 const double* a, const double* b, double* c, int* nonfinite, double* device_ms,
+                 int64_t panels, std::string* err);
+}  // namespace mpmm
+
 namespace {
 
 thread_local std::string g_err;
@@ -81,6 +93,13 @@ cudaError_t host_streams(HostStreams** out) {
     g_hs.device = dev;
     if ((e = cudaStreamCreateWithFlags(&g_hs.copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
     if ((e = cudaStreamCreateWithFlags(&g_hs.comp, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    // keep freed buffers in the stream-ordered pool between calls (the
+    // default threshold 0 unmaps them at every synchronize)
+    cudaMemPool_t pool;
+    if ((e = cudaDeviceGetDefaultMemPool(&pool, dev)) != cudaSuccess) return e;
+    uint64_t keep = UINT64_MAX;
+    if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess)
+      return e;
   }
   *out = &g_hs;
   return cudaSuccess;
@@ -546,6 +565,99 @@ int mpmm_oz_combine_dev(int comps, const void* jobs, int njobs, int64_t m, int64
   cudaError_t e = oz_combine_launch(comps, jobs, njobs, (int)m, (int)n, C, status,
                                     (cudaStream_t)stream, host_jobs);
   return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "combine launch");
+}
+
+int mpmm_strassen_dev(int comps, int64_t cutoff, int64_t leaf_n_min, int64_t m, int64_t l,
+                      int64_t n, const double* A, int64_t lda, const double* B, int64_t ldb,
+                      double* C, int64_t ldc, int* nonfinite, int64_t* stats, void* stream) {
+  if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
+  if (!dims_ok(m, l, n)) return fail(MPMM_ERR_ARG, "bad shape");
+  if (lda < l || ldb < n || ldc < n) return fail(MPMM_ERR_ARG, "leading dimension too small");
+  if (cutoff < 2) return fail(MPMM_ERR_ARG, "Strassen cutoff must be >= 2");
+  if (leaf_n_min < 1) return fail(MPMM_ERR_ARG, "leaf block size must be positive");
+  if (stats) stats[0] = stats[1] = 0;
+  int tile, super;
+  tile_for(leaf_n_min, &tile, &super);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = strassen_run(comps, cutoff, tile, m, l, n, A, lda, B, ldb, C, ldc, stats, s);
+  if (e == cudaSuccess && nonfinite && m > 0 && n > 0)
+    e = nonfinite_launch(comps, C, ldc, (int)m, (int)n, nonfinite, s);
+  return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "strassen");
+}
+
+int mpmm_init(int ngpus, const int* devices) {
+  std::string err;
+  int rc = rt_init(devices, ngpus, &err);
+  return rc == 0 ? MPMM_OK : fail(rc, err);
+}
+
+int mpmm_finalize(void) { return rt_finalize(); }
+
+int mpmm_runtime_gpus(int* ngpus, int* devices, int cap) {
+  *ngpus = rt_gpus(devices, devices ? cap : 0);
+  return MPMM_OK;
+}
+
+int mpmm_gemm_multi(int comps, int algo, int64_t n_min, int64_t cutoff, int64_t m, int64_t l,
+                    int64_t n, const double* a, const double* b, double* c, int64_t panels,
+                    int* nonfinite, double* device_ms) {
+  if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
+  if (!dims_ok(m, l, n)) return fail(MPMM_ERR_ARG, "bad shape");
+  if (algo < MPMM_ALGO_SIMPLE || algo > MPMM_ALGO_STRASSEN) return fail(MPMM_ERR_ARG, "bad algo");
+  if (algo == MPMM_ALGO_BLOCK_FAST && comps != 2)
+    return fail(MPMM_ERR_ARG, "the fast accuracy mode is implemented for DD only");
+  if (algo != MPMM_ALGO_SIMPLE && n_min < 1) return fail(MPMM_ERR_ARG, "block size must be positive");
+  if (algo == MPMM_ALGO_STRASSEN && cutoff < 2) return fail(MPMM_ERR_ARG, "Strassen cutoff must be >= 2");
+  int tile = TILE_16, super = 1;
+  if (algo != MPMM_ALGO_SIMPLE) tile_for(n_min, &tile, &super);
+  std::string err;
+  int rc = rt_gemm_host(comps, algo, tile, cutoff, m, l, n, a, b, c, nonfinite, device_ms, panels,
+                        &err);
+  return rc == 0 ? MPMM_OK : fail(rc, err);
+}
+
+struct MpmmTimer {
+  cudaEvent_t start = nullptr, stop = nullptr;
+};
+
+int mpmm_timer_create(void** timer) {
+  MpmmTimer* t = new MpmmTimer();
+  cudaError_t e = cudaEventCreate(&t->start);
+  if (e == cudaSuccess) e = cudaEventCreate(&t->stop);
+  if (e != cudaSuccess) {
+    if (t->start) cudaEventDestroy(t->start);
+    delete t;
+    return cuda_fail(e, "cudaEventCreate");
+  }
+  *timer = t;
+  return MPMM_OK;
+}
+
+int mpmm_timer_start(void* timer, void* stream) {
+  CU(cudaEventRecord(static_cast<MpmmTimer*>(timer)->start, (cudaStream_t)stream));
+  return MPMM_OK;
+}
+
+int mpmm_timer_stop(void* timer, void* stream) {
+  CU(cudaEventRecord(static_cast<MpmmTimer*>(timer)->stop, (cudaStream_t)stream));
+  return MPMM_OK;
+}
+
+int mpmm_timer_elapsed_ms(void* timer, float* ms) {
+  MpmmTimer* t = static_cast<MpmmTimer*>(timer);
+  CU(cudaEventSynchronize(t->stop));
+  CU(cudaEventElapsedTime(ms, t->start, t->stop));
+  return MPMM_OK;
+}
+
+int mpmm_timer_destroy(void* timer) {
+  MpmmTimer* t = static_cast<MpmmTimer*>(timer);
+  if (t) {
+    cudaEventDestroy(t->start);
+    cudaEventDestroy(t->stop);
+    delete t;
+  }
+  return MPMM_OK;
 }
 
 int mpmm_fp64_burn_dev(int op, int blocks, int threads, int64_t iters, double* scratch,

@@ -142,12 +142,6 @@ def _ewise_view(O, X, Y, sy, Z=None, sz=1, W=None, sw=1):
                     _stream())
 
 
-def _new(rows, cols, comps, device, zero=False):
-    torch = _torch()
-    fn = torch.zeros if zero else torch.empty
-    return fn((rows, cols, comps), dtype=torch.float64, device=device)
-
-
 # ---------------------------------------------------------------------------
 # validation (multiply.py:115-127)
 # ---------------------------------------------------------------------------
@@ -381,126 +375,22 @@ def matmul_strassen(a, b, cutoff=DEFAULT_STRASSEN_CUTOFF, leaf_n_min=DEFAULT_BLO
     return _result(_check_finite(c), home)
 
 
-def _padded(V, rows, cols):
-    """V itself, or a zero-padded rows x cols copy (multiply.py:206-218)."""
-    if V.rows == rows and V.cols == cols:
-        return V
-    t = _new(rows, cols, V.comps, V.base.device, zero=True)
-    src = V.base[V.r0:V.r0 + V.rows, V.c0:V.c0 + V.cols]
-    t[:V.rows, :V.cols].copy_(src)
-    return _View.of(t)
-
-
-class _Node:
-    """One Strassen sub-problem: C (m x n) = A (m x l) * B (l x n)."""
-
-    __slots__ = ("A", "B", "C", "Cp", "P")
-
-    def __init__(self, A, B, C):
-        self.A, self.B, self.C = A, B, C
-        self.Cp = None     # padded C buffer when the level pads
-        self.P = None      # the seven product views
-
-
-def _ptr_table(rows):
-    """int64 device table from a list of equal-length tuples."""
-    torch = _torch()
-    host = torch.tensor(rows, dtype=torch.int64)
-    return host.to(_torch().device("cuda", torch.cuda.current_device()), non_blocking=False)
-
-
-def _ewise_batch(items, rows, cols, comps):
-    """items: (O, X, Y, sy[, Z, sz[, W, sw]]) views, all rows x cols."""
-    if not items:
-        return
-    recs = []
-    for it in items:
-        O, X, Y, sy = it[:4]
-        Z, sz = (it[4], it[5]) if len(it) > 4 else (None, 1)
-        W, sw = (it[6], it[7]) if len(it) > 6 else (None, 1)
-        nops = 1 + (Z is not None) + (W is not None)
-        recs.append((X.ptr, Y.ptr, Z.ptr if Z else 0, W.ptr if W else 0, O.ptr,
-                     X.ld, Y.ld, Z.ld if Z else 0, W.ld if W else 0, O.ld, nops, sy, sz, sw))
-    table = _ptr_table(recs)
-    _cuda.ewise_batched_dev(comps, len(recs), rows, cols, table.data_ptr(), _stream())
-    return table
-
-
 def _strassen_rec(A, B, C, cutoff, leaf_n_min, stats):
-    """Level-synchronous Strassen: every level's operand sums are one
-    batched elementwise launch per operand shape, all 7^d leaves are ONE
-    batched GEMM launch, and the quadrant combinations go bottom-up one
-    batched launch per level.  Per element this is exactly the reference's
-    recursion (multiply.py:293-338): same padding, same operand list, same
-    combination chains, leaves on the blocked kernel from a zero
-    accumulator -- so results are bit-identical to it."""
-    comps, dev = C.comps, C.base.device
-    keep = []                   # device tables/buffers alive until the stream drains
-    levels = []
-    nodes = [_Node(A, B, C)]
-    m, l, n = A.rows, A.cols, B.cols
-    while min(m, l, n) > cutoff:
-        me, le, ne = m + (m & 1), l + (l & 1), n + (n & 1)
-        hm, hl, hn = me // 2, le // 2, ne // 2
-        sums_a, sums_b, children = [], [], []
-        for nd in nodes:
-            Ap, Bp = _padded(nd.A, me, le), _padded(nd.B, le, ne)
-            if (me, ne) != (m, n):
-                nd.Cp = _View.of(_new(me, ne, comps, dev))
-            Cq = nd.Cp if nd.Cp is not None else nd.C
-            a11, a12 = Ap.sub(0, 0, hm, hl), Ap.sub(0, hl, hm, hl)
-            a21, a22 = Ap.sub(hm, 0, hm, hl), Ap.sub(hm, hl, hm, hl)
-            b11, b12 = Bp.sub(0, 0, hl, hn), Bp.sub(0, hn, hl, hn)
-            b21, b22 = Bp.sub(hl, 0, hl, hn), Bp.sub(hl, hn, hl, hn)
-            ta = _new(5 * hm, hl, comps, dev)
-            tb = _new(5 * hl, hn, comps, dev)
-            pt = _new(7 * hm, hn, comps, dev)
-            keep += [Ap, Bp, ta, tb, pt]
-            SA = [_View(ta, q * hm, 0, hm, hl) for q in range(5)]
-            SB = [_View(tb, q * hl, 0, hl, hn) for q in range(5)]
-            # operand sums of multiply.py:313-321, in the reference's order
-            sums_a += [(SA[0], a11, a22, 1), (SA[1], a21, a22, 1), (SA[2], a11, a12, 1),
-                       (SA[3], a21, a11, -1), (SA[4], a12, a22, -1)]
-            sums_b += [(SB[0], b11, b22, 1), (SB[1], b12, b22, -1), (SB[2], b21, b11, -1),
-                       (SB[3], b11, b12, 1), (SB[4], b21, b22, 1)]
-            nd.P = [_View(pt, q * hm, 0, hm, hn) for q in range(7)]
-            operands = ((SA[0], SB[0]), (SA[1], b11), (a11, SB[1]), (a22, SB[2]),
-                        (SA[2], b22), (SA[3], SB[3]), (SA[4], SB[4]))
-            children += [_Node(x, y, p) for (x, y), p in zip(operands, nd.P)]
-            nd.C = (nd.C, Cq)
-            if stats is not None:
-                stats.multiplications += 7
-                stats.additions += 18
-        keep.append(_ewise_batch(sums_a, hm, hl, comps))
-        keep.append(_ewise_batch(sums_b, hl, hn, comps))
-        levels.append((nodes, (m, n), (hm, hn)))
-        nodes = children
-        m, l, n = hm, hl, hn
-    # all leaves: blocked kernel from a zero accumulator (multiply.py:294-298)
-    recs = [(nd.A.ptr, nd.B.ptr, nd.C.ptr, nd.A.ld, nd.B.ld, nd.C.ld) for nd in nodes]
-    table = _ptr_table(recs)
-    keep.append(table)
-    _cuda.gemm_batched_dev(comps, _cuda.ALGO_BLOCK, leaf_n_min, len(recs), m, l, n,
-                           table.data_ptr(), False, None, _stream())
-    # combinations bottom-up (multiply.py:334-337), then crop (:242-260)
-    for lv_nodes, (pm, pn), (hm, hn) in reversed(levels):
-        items = []
-        for nd in lv_nodes:
-            Cout, Cq = nd.C
-            p1, p2, p3, p4, p5, p6, p7 = nd.P
-            items += [(Cq.sub(0, 0, hm, hn), p1, p4, 1, p5, -1, p7, 1),
-                      (Cq.sub(0, hn, hm, hn), p3, p5, 1),
-                      (Cq.sub(hm, 0, hm, hn), p2, p4, 1),
-                      (Cq.sub(hm, hn, hm, hn), p1, p3, 1, p2, -1, p6, 1)]
-        keep.append(_ewise_batch(items, hm, hn, comps))
-        for nd in lv_nodes:
-            Cout, Cq = nd.C
-            if nd.Cp is not None:
-                Cout.base[Cout.r0:Cout.r0 + pm, Cout.c0:Cout.c0 + pn].copy_(
-                    Cq.base[:pm, :pn])
-    # every buffer in `keep` was allocated on, and is only used by, the
-    # current stream, so the caching allocator may recycle it in stream order
-    del keep
+    """The reference's recursion (multiply.py:293-338) through the native
+    driver (csrc/strassen.cpp, mpmm_strassen_dev): level-synchronous --
+    per level one batched elementwise launch per operand shape, ONE batched
+    GEMM launch for all 7^d leaves, one batched launch per level for the
+    quadrant combinations -- with the same padding, operand list,
+    combination chains and zero-accumulator leaves, so results are
+    bit-identical to the reference."""
+    import ctypes
+    counts = (ctypes.c_int64 * 2)()
+    _cuda.strassen_dev(C.comps, cutoff, leaf_n_min, A.rows, A.cols, B.cols, A.ptr, A.ld,
+                       B.ptr, B.ld, C.ptr, C.ld, None, counts if stats is not None else None,
+                       _stream())
+    if stats is not None:
+        stats.multiplications += counts[0]
+        stats.additions += counts[1]
 
 
 # ---------------------------------------------------------------------------
