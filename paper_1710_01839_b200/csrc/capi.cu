@@ -55,6 +55,13 @@ void tile_for(int64_t n_min, int* tile, int* super) {
   // GPU it selects the CTA tile configuration; results never
   // depend on it.  `super` is kept in the ABI for table compatibility (1).
   *super = 1;
+  if (const char* env = std::getenv("MPMM_FORCE_TILE")) {   // experiments only
+    int t = std::atoi(env);
+    if (t >= 0 && t < TILE_COUNT) {
+      *tile = t;
+      return;
+    }
+  }
   if (n_min <= 16) {
     *tile = TILE_16;
   } else if (n_min <= 32) {

@@ -82,9 +82,12 @@ struct TileSmem {
 
 // One CTA computes the BM x BN output tile at (m0, n0) of problem `pr`.
 // NT threads: thread (tx, ty) owns rows ty + r*NTY, cols tx + c*NTX.
+// k-tiles [kt0, kt1) of the tile (kt1 < 0: to the end); accumulate: the
+// accumulator starts at C's value (read through L2).
 template <class Ops, int BM, int BN, int BK, int TM, int TN, int NT>
 __device__ __forceinline__ void gemm_tile(const Prob& pr, int m, int n, int l, int accumulate,
-                                          int m0, int n0, double2* smem, bool& bad) {
+                                          int m0, int n0, double2* smem, bool& bad,
+                                          int kt0 = 0, int kt1 = -1) {
   constexpr int V = Ops::V;
   constexpr int NTX = BN / TN, NTY = BM / TM;
   static_assert(NTX * NTY == NT, "thread tile does not cover the CTA tile");
@@ -108,13 +111,14 @@ __device__ __forceinline__ void gemm_tile(const Prob& pr, int m, int n, int l, i
       bool load = accumulate && i < m && j < n;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
-        double2 x = load ? pr.C[((int64_t)i * pr.ldc + j) * V + v] : make_double2(0.0, 0.0);
+        double2 x = load ? __ldcg(pr.C + ((int64_t)i * pr.ldc + j) * V + v)
+                         : make_double2(0.0, 0.0);
         acc[r][c][2 * v] = x.x;
         acc[r][c][2 * v + 1] = x.y;
       }
     }
 
-  const int ktiles = (l + BK - 1) / BK;
+  const int ktiles = kt1 < 0 ? (l + BK - 1) / BK : kt1;
   auto load = [&](int kt, int st) {
     const int k0 = kt * BK;
 #pragma unroll
@@ -137,12 +141,12 @@ __device__ __forceinline__ void gemm_tile(const Prob& pr, int m, int n, int l, i
     }
   };
 
-  if (ktiles > 0) {
-    load(0, 0);
+  if (ktiles > kt0) {
+    load(kt0, 0);
     cp_async_commit();
   }
-  for (int kt = 0; kt < ktiles; ++kt) {
-    const int st = kt & 1;
+  for (int kt = kt0; kt < ktiles; ++kt) {
+    const int st = (kt - kt0) & 1;
     if (kt + 1 < ktiles) {
       load(kt + 1, st ^ 1);
       cp_async_commit();

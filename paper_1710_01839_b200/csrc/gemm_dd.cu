@@ -7,7 +7,7 @@
 // bit-identical to the reference).
 // Tile configurations (n_min -> tile: capi.cu tile_for):
 //   TILE_16    16x16 CTA tile, 1x1 per thread, 256 threads, 4 CTAs/SM
-//   TILE_32    32x32, 2x2, 256 threads, 2 CTAs/SM
+//   TILE_32    32x32, 2x2, 256 threads, 2 CTAs/SM, k-tiles of 16
 //   TILE_LPT   persistent 64x64 (4x4) tiles in whole waves + 32x32 quarters
 //   TILE_32x64 32x64, 2x2, 512 threads
 //   TILE_64    64x64, 4x4, 256 threads, plain grid
@@ -19,7 +19,7 @@ template <class Ops>
 static cudaError_t dd_blocked(const GemmArgs& g) {
   switch (g.tile) {
     case TILE_16: return launch_tiled<Ops, 16, 16, 16, 1, 1, 4>(g);
-    case TILE_32: return launch_tiled<Ops, 32, 32, 8, 2, 2, 2>(g);
+    case TILE_32: return launch_tiled<Ops, 32, 32, 16, 2, 2, 2>(g);
     case TILE_64: return launch_tiled<Ops, 64, 64, 8, 4, 4, 1>(g);
     case TILE_32x64: return launch_tiled<Ops, 32, 64, 8, 2, 2, 1>(g);
     case TILE_LPT: return launch_lpt<Ops, 64, 64, 8, 4, 4, 1>(g);
@@ -40,7 +40,7 @@ cudaError_t dd_gemm_geometry(int algo, int tile, Geometry* geo) {
       case TILE_16: geo->bm = 16, geo->bn = 16;
         return occupancy_of(gemm_tiled<DDFastOps, 16, 16, 16, 1, 1, 4>, 256, geo);
       case TILE_32: geo->bm = 32, geo->bn = 32;
-        return occupancy_of(gemm_tiled<DDFastOps, 32, 32, 8, 2, 2, 2>, 256, geo);
+        return occupancy_of(gemm_tiled<DDFastOps, 32, 32, 16, 2, 2, 2>, 256, geo);
       case TILE_64: geo->bm = 64, geo->bn = 64;
         return occupancy_of(gemm_tiled<DDFastOps, 64, 64, 8, 4, 4, 1>, 256, geo);
       case TILE_32x64: geo->bm = 32, geo->bn = 64;
@@ -58,7 +58,7 @@ cudaError_t dd_gemm_geometry(int algo, int tile, Geometry* geo) {
     case TILE_16: geo->bm = 16, geo->bn = 16;
       return occupancy_of(gemm_tiled<DDOps, 16, 16, 16, 1, 1, 4>, 256, geo);
     case TILE_32: geo->bm = 32, geo->bn = 32;
-      return occupancy_of(gemm_tiled<DDOps, 32, 32, 8, 2, 2, 2>, 256, geo);
+      return occupancy_of(gemm_tiled<DDOps, 32, 32, 16, 2, 2, 2>, 256, geo);
     case TILE_64: geo->bm = 64, geo->bn = 64;
       return occupancy_of(gemm_tiled<DDOps, 64, 64, 8, 4, 4, 1>, 256, geo);
     case TILE_32x64: geo->bm = 32, geo->bn = 64;
