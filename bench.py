@@ -334,7 +334,7 @@ def run_ours(args, rank, world, local_rank):
     tensor_s, tensor_err = None, None
     try:
         from paper_1710_01839_b200.tensor import matmul_exact_tensors, plan
-        jobs = plan(A, B)
+        pl = plan(A, B)
         matmul_exact_tensors(A, B)
         torch.cuda.synchronize()
         tev = []
@@ -347,7 +347,7 @@ def run_ours(args, rank, world, local_rank):
             tev.append((s, e))
         torch.cuda.synchronize()
         tensor_s = statistics.mean(s.elapsed_time(e) for s, e in tev) / 1e3
-        tensor_jobs = [(j[0], j[1], j[2]) for j in jobs]
+        tensor_jobs = [(pl.ranges_a[ia], pl.ranges_b[ib], N) for ia, ib, N in pl.jobs]
     except Exception as ex:  # noqa: BLE001 - reported, the headline is unaffected
         tensor_err = f"{type(ex).__name__}: {ex}"
     clocks = sampler.stop() if sampler else None

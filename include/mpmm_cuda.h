@@ -36,6 +36,7 @@ extern "C" {
 #define MPMM_ERR_ARG 1    /* bad argument (shape, comps, algo, range)     */
 #define MPMM_ERR_CUDA 2   /* a CUDA runtime call failed                   */
 #define MPMM_ERR_NODEV 3  /* no CUDA device                               */
+#define MPMM_ERR_RANGE 4  /* operands not representable (exact tensor mode) */
 
 #define MPMM_ALGO_SIMPLE 0
 #define MPMM_ALGO_BLOCK 1
@@ -180,31 +181,51 @@ int mpmm_gen_inputs_dev(int comps, uint64_t state_hi, uint64_t state_lo, uint64_
  * then rounded once to DD/QD.  Not bit-identical to the reference (it is
  * the exact product, correctly rounded).
  * ------------------------------------------------------------------------- */
-/* Per row (by_cols 0) or column (1) of the components [c0,c1): E = max
- * exponent (|x| < 2^E), L = lowest set bit (empty: E=-100000, L=100000). */
-int mpmm_oz_scan_dev(int by_cols, int comps, int c0, int c1, int64_t rows, int64_t cols,
-                     const double *X, int64_t ld, int *E, int *L, void *stream);
-/* int8 residues of x * 2^shift[row|col] modulo the first nmod moduli:
- * by_cols 0 -> R[t*rplane + row*rpitch + col], by_cols 1 ->
- * R[t*rplane + col*rpitch + row] (k contiguous; pads are left untouched).
- * pow2: nmod x xmax table of 2^x mod p_t (xmax > largest scaled exponent). */
+/* One pass over X (rows x cols DD/QD, leading dim ld): per row (by_cols 0) or column (1) and per
+ * component c, EL[c*odim + o] = max exponent E with |x| < 2^E and
+ * EL[(comps + c)*odim + o] = min weight exponent L of the lowest set bit
+ * over the nonzero entries (-100000 / 100000 when none); bit 0 of *status
+ * is set when any component is not finite. */
+int mpmm_oz_scan_dev(int by_cols, int comps, int64_t rows, int64_t cols, const double *X,
+                     int64_t ld, int *EL, int *status, void *stream);
+/* int8 residues of sum_{c0<=c<c1} x_c * 2^shift[row|col] (an integer of
+ * fewer than 32*words - 1 bits, two's complement) modulo the first nmod
+ * moduli: by_cols 0 -> R[t*rplane + row*rpitch + k], by_cols 1 ->
+ * R[t*rplane + col*rpitch + k] (k contiguous; rpitch a multiple of 4;
+ * whole 4-byte groups are written, zeros past the matrix edge).
+ * words <= 12. */
 int mpmm_oz_residues_dev(int by_cols, int comps, int c0, int c1, int64_t rows, int64_t cols,
-                         const double *X, int64_t ld, const int *shift, int nmod,
-                         const uint8_t *pow2, int xmax, int8_t *R, int64_t rpitch,
-                         int64_t rplane, void *stream);
+                         const double *X, int64_t ld, const int *shift, int nmod, int words,
+                         int8_t *R, int64_t rpitch, int64_t rplane, void *stream);
+/* Host-only planner of the exact tensor mode: from the scan arrays of A
+ * (ela, 2*comps*m ints) and B (elb, 2*comps*n ints) choose the cheapest
+ * feasible component split.  Outputs: *na ranges of A in ranges_a[2*na]
+ * (c0, c1) with their row shifts in shift_a[na*m] (na <= 4), likewise B;
+ * *njobs (<= 16) jobs of 8 ints {a_range, b_range, moduli N, limbs K (one
+ * for all jobs), words_a, words_b, beta_a, beta_b}.  MPMM_ERR_RANGE when
+ * no split fits the 54 moduli.  No device work. */
+int mpmm_oz_plan(int comps, int64_t m, int64_t n, int64_t l, const int *ela, const int *elb,
+                 int *njobs, int *jobs, int *na, int *ranges_a, int *shift_a, int *nb,
+                 int *ranges_b, int *shift_b);
 /* batch x (C_t = A_t * Bt_t^T): A_t m x k, Bt_t n x k (row-major int8),
  * C_t m x n row-major int32, exact for k <= 131071 (cuBLASLt IMMA); m, n,
  * k multiples of 16. */
 int mpmm_int8_gemm_batched_dev(int64_t m, int64_t n, int64_t k, int64_t batch, const int8_t *A,
                                const int8_t *Bt, int32_t *C, void *workspace, int64_t ws_bytes,
                                void *stream);
-/* CRT reconstruction of njobs jobs (device array of 56-byte records {G,
- * srow, scol, table: pointers; N, K: int32; gpitch, gplane: int64}), exact
- * sum, rounding to comps doubles per entry of C (m x n); *status |= 1
- * non-finite, 2 window.  host_jobs: the same records in host memory (lets a
- * single job take the register-resident kernel), or NULL. */
+/* CRT reconstruction of njobs <= 16 jobs given as a HOST array of 56-byte
+ * records {G, srow, scol, table: device pointers; N, K: int32; gpitch,
+ * gplane: int64} (passed to the kernel by value), exact sum, rounding to
+ * comps doubles per entry of C (m x n); *status |= 1 non-finite, 2
+ * window overflow. */
 int mpmm_oz_combine_dev(int comps, const void *jobs, int njobs, int64_t m, int64_t n, double *C,
-                        int *status, const void *host_jobs, void *stream);
+                        int *status, void *stream);
+/* Device side of the planner: for nranges <= 4 component ranges (HOST
+ * array ranges[2*nranges] of (c0, c1)) and the scan arrays EL of one
+ * operand (odim rows/columns): shift[r*odim + o] = -min L (0 for an empty
+ * row) and beta[r] = max(E - L) + 1 (atomic max; the caller zeroes beta). */
+int mpmm_oz_shifts_dev(int comps, int nranges, const int *ranges, int64_t odim, const int *EL,
+                       int *shift, int *beta, void *stream);
 
 /* FP64 roofline micro-benchmark: blocks x threads threads each run 8
  * independent chains of `iters` DFMA (op 0) or DADD (op 1). */

@@ -62,11 +62,14 @@ _SIGNATURES = {
     "mpmm_fp64_burn_dev": [_INT, _INT, _INT, _I64, _VP, _VP],
     "mpmm_gen_inputs_dev": [_INT, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                             ctypes.c_uint64, ctypes.c_uint64, _I64, _I64, _VP, _VP],
-    "mpmm_oz_scan_dev": [_INT, _INT, _INT, _INT, _I64, _I64, _VP, _I64, _VP, _VP, _VP],
-    "mpmm_oz_residues_dev": [_INT, _INT, _INT, _INT, _I64, _I64, _VP, _I64, _VP, _INT, _VP, _INT,
+    "mpmm_oz_scan_dev": [_INT, _INT, _I64, _I64, _VP, _I64, _VP, _VP, _VP],
+    "mpmm_oz_residues_dev": [_INT, _INT, _INT, _INT, _I64, _I64, _VP, _I64, _VP, _INT, _INT,
                              _VP, _I64, _I64, _VP],
+    "mpmm_oz_plan": [_INT, _I64, _I64, _I64, _VP, _VP, ctypes.POINTER(_INT), _VP,
+                     ctypes.POINTER(_INT), _VP, _VP, ctypes.POINTER(_INT), _VP, _VP],
     "mpmm_int8_gemm_batched_dev": [_I64, _I64, _I64, _I64, _VP, _VP, _VP, _VP, _I64, _VP],
-    "mpmm_oz_combine_dev": [_INT, _VP, _INT, _I64, _I64, _VP, _VP, _VP, _VP],
+    "mpmm_oz_combine_dev": [_INT, _VP, _INT, _I64, _I64, _VP, _VP, _VP],
+    "mpmm_oz_shifts_dev": [_INT, _INT, _VP, _I64, _VP, _VP, _VP, _VP],
     "mpmm_exact_check_dev": [_INT, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _VP,
                              _I64, _INT, _VP, _VP],
     "mpmm_strassen_dev": [_INT, _I64, _I64, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64,
@@ -370,16 +373,36 @@ def gen_inputs_dev(comps, state, inc, first_draw, rows, cols, out, stream=None):
                                      first_draw, rows, cols, out, stream))
 
 
-def oz_scan_dev(by_cols, comps, c0, c1, rows, cols, X, ld, E, L, stream=None):
+def oz_scan_dev(by_cols, comps, rows, cols, X, ld, EL, status, stream=None):
     sync_device()
-    check(load().mpmm_oz_scan_dev(by_cols, comps, c0, c1, rows, cols, X, ld, E, L, stream))
+    check(load().mpmm_oz_scan_dev(by_cols, comps, rows, cols, X, ld, EL, status, stream))
 
 
-def oz_residues_dev(by_cols, comps, c0, c1, rows, cols, X, ld, shift, nmod, pow2, xmax, R,
-                    rpitch, rplane, stream=None):
+def oz_residues_dev(by_cols, comps, c0, c1, rows, cols, X, ld, shift, nmod, words, R, rpitch,
+                    rplane, stream=None):
     sync_device()
     check(load().mpmm_oz_residues_dev(by_cols, comps, c0, c1, rows, cols, X, ld, shift, nmod,
-                                      pow2, xmax, R, rpitch, rplane, stream))
+                                      words, R, rpitch, rplane, stream))
+
+
+def oz_plan(comps, m, n, l, ela, elb):
+    """Host planner (no device work): returns (jobs int32[njobs, 8],
+    ranges_a, shift_a[na, m], ranges_b, shift_b[nb, n]) or None when no
+    split is representable."""
+    ela = np.ascontiguousarray(ela, dtype=np.int32)
+    elb = np.ascontiguousarray(elb, dtype=np.int32)
+    jobs = np.zeros((16, 8), dtype=np.int32)
+    ra, rb = np.zeros(8, dtype=np.int32), np.zeros(8, dtype=np.int32)
+    sa, sb = np.zeros((4, max(m, 1)), dtype=np.int32), np.zeros((4, max(n, 1)), dtype=np.int32)
+    nj, na, nb = _INT(0), _INT(0), _INT(0)
+    vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    rc = load().mpmm_oz_plan(comps, m, n, l, vp(ela), vp(elb), ctypes.byref(nj), vp(jobs),
+                             ctypes.byref(na), vp(ra), vp(sa), ctypes.byref(nb), vp(rb), vp(sb))
+    if rc == 4:
+        return None
+    check(rc)
+    return (jobs[:nj.value], ra[:2 * na.value].reshape(-1, 2), sa[:na.value, :m],
+            rb[:2 * nb.value].reshape(-1, 2), sb[:nb.value, :n])
 
 
 def int8_gemm_batched_dev(m, n, k, batch, A, Bt, C, workspace, ws_bytes, stream=None):
@@ -388,9 +411,18 @@ def int8_gemm_batched_dev(m, n, k, batch, A, Bt, C, workspace, ws_bytes, stream=
                                             stream))
 
 
-def oz_combine_dev(comps, jobs, njobs, m, n, C, status, host_jobs=None, stream=None):
+def oz_combine_dev(comps, jobs, njobs, m, n, C, status, stream=None):
+    """jobs: host pointer to njobs 56-byte CrtJob records."""
     sync_device()
-    check(load().mpmm_oz_combine_dev(comps, jobs, njobs, m, n, C, status, host_jobs, stream))
+    check(load().mpmm_oz_combine_dev(comps, jobs, njobs, m, n, C, status, stream))
+
+
+def oz_shifts_dev(comps, ranges, odim, EL, shift, beta, stream=None):
+    """ranges: sequence of (c0, c1) component ranges (<= 4)."""
+    sync_device()
+    flat = (ctypes.c_int * (2 * len(ranges)))(*[c for r in ranges for c in r])
+    check(load().mpmm_oz_shifts_dev(comps, len(ranges), ctypes.cast(flat, ctypes.c_void_p),
+                                    odim, EL, shift, beta, stream))
 
 
 def fp64_burn_dev(op, blocks, threads, iters, scratch, stream=None):

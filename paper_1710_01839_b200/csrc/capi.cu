@@ -24,6 +24,9 @@ int rt_gpus(int* ids, int cap);
 int rt_gemm_host(int comps, int algo, int tile, int64_t cutoff, int64_t m, int64_t l, int64_t n,
                  const double* a, const double* b, double* c, int* nonfinite, double* device_ms,
                  int64_t panels, std::string* err);
+int oz_plan(int comps, int64_t m, int64_t n, int64_t l, const int* ela, const int* elb,
+            int* njobs, int* jobs, int* na, int* ranges_a, int* shift_a, int* nb, int* ranges_b,
+            int* shift_b);
 }  // namespace mpmm
 
 namespace {
@@ -532,26 +535,37 @@ int mpmm_gen_inputs_dev(int comps, uint64_t state_hi, uint64_t state_lo, uint64_
   return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "input generation launch");
 }
 
-int mpmm_oz_scan_dev(int by_cols, int comps, int c0, int c1, int64_t rows, int64_t cols,
-                     const double* X, int64_t ld, int* E, int* L, void* stream) {
+int mpmm_oz_scan_dev(int by_cols, int comps, int64_t rows, int64_t cols, const double* X,
+                     int64_t ld, int* EL, int* status, void* stream) {
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
-  if (c0 < 0 || c1 > comps || c0 >= c1) return fail(MPMM_ERR_ARG, "bad component range");
   if (!dims_ok(rows, 0, cols)) return fail(MPMM_ERR_ARG, "bad shape");
-  cudaError_t e = oz_scan_launch(by_cols, X, ld, (int)rows, (int)cols, comps, c0, c1, E, L,
+  cudaError_t e = oz_scan_launch(by_cols, X, ld, (int)rows, (int)cols, comps, EL, status,
                                  (cudaStream_t)stream);
   return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "scan launch");
 }
 
 int mpmm_oz_residues_dev(int by_cols, int comps, int c0, int c1, int64_t rows, int64_t cols,
-                         const double* X, int64_t ld, const int* shift, int nmod,
-                         const uint8_t* pow2, int xmax, int8_t* R, int64_t rpitch,
-                         int64_t rplane, void* stream) {
+                         const double* X, int64_t ld, const int* shift, int nmod, int words,
+                         int8_t* R, int64_t rpitch, int64_t rplane, void* stream) {
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
   if (c0 < 0 || c1 > comps || c0 >= c1) return fail(MPMM_ERR_ARG, "bad component range");
   if (!dims_ok(rows, 0, cols) || nmod < 1 || nmod > 54) return fail(MPMM_ERR_ARG, "bad shape");
+  if (words < 1 || words > 12) return fail(MPMM_ERR_ARG, "words must be 1..12");
+  if (rpitch % 4) return fail(MPMM_ERR_ARG, "rpitch must be a multiple of 4");
   cudaError_t e = oz_residues_launch(by_cols, X, ld, (int)rows, (int)cols, comps, c0, c1, shift,
-                                     nmod, pow2, xmax, R, rpitch, rplane, (cudaStream_t)stream);
+                                     nmod, words, R, rpitch, rplane, (cudaStream_t)stream);
   return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "residues launch");
+}
+
+int mpmm_oz_plan(int comps, int64_t m, int64_t n, int64_t l, const int* ela, const int* elb,
+                 int* njobs, int* jobs, int* na, int* ranges_a, int* shift_a, int* nb,
+                 int* ranges_b, int* shift_b) {
+  if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
+  if (m < 0 || n < 0 || l < 0) return fail(MPMM_ERR_ARG, "bad shape");
+  int rc = oz_plan(comps, m, n, l, ela, elb, njobs, jobs, na, ranges_a, shift_a, nb, ranges_b,
+                   shift_b);
+  return rc == 0 ? MPMM_OK
+                 : fail(MPMM_ERR_RANGE, "operand dynamic range too wide for the int8 CRT scheme");
 }
 
 int mpmm_int8_gemm_batched_dev(int64_t m, int64_t n, int64_t k, int64_t batch, const int8_t* A,
@@ -566,12 +580,25 @@ int mpmm_int8_gemm_batched_dev(int64_t m, int64_t n, int64_t k, int64_t batch, c
 }
 
 int mpmm_oz_combine_dev(int comps, const void* jobs, int njobs, int64_t m, int64_t n, double* C,
-                        int* status, const void* host_jobs, void* stream) {
+                        int* status, void* stream) {
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
-  if (njobs < 1 || !dims_ok(m, 0, n)) return fail(MPMM_ERR_ARG, "bad shape");
+  if (njobs < 1 || njobs > 16 || !dims_ok(m, 0, n)) return fail(MPMM_ERR_ARG, "bad shape");
   cudaError_t e = oz_combine_launch(comps, jobs, njobs, (int)m, (int)n, C, status,
-                                    (cudaStream_t)stream, host_jobs);
+                                    (cudaStream_t)stream);
   return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "combine launch");
+}
+
+int mpmm_oz_shifts_dev(int comps, int nranges, const int* ranges, int64_t odim, const int* EL,
+                       int* shift, int* beta, void* stream) {
+  if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
+  if (nranges < 1 || nranges > 4 || odim < 0 || odim >= (1ll << 30))
+    return fail(MPMM_ERR_ARG, "bad ranges or shape");
+  for (int r = 0; r < nranges; ++r)
+    if (ranges[2 * r] < 0 || ranges[2 * r + 1] > comps || ranges[2 * r] >= ranges[2 * r + 1])
+      return fail(MPMM_ERR_ARG, "bad component range");
+  cudaError_t e = oz_shifts_launch(comps, nranges, ranges, (int)odim, EL, shift, beta,
+                                   (cudaStream_t)stream);
+  return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "shifts launch");
 }
 
 int mpmm_strassen_dev(int comps, int64_t cutoff, int64_t leaf_n_min, int64_t m, int64_t l,

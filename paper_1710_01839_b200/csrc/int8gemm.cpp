@@ -10,7 +10,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <string>
+#include <tuple>
 
 namespace mpmm {
 
@@ -18,6 +20,10 @@ namespace {
 
 thread_local cublasLtHandle_t g_lt = nullptr;
 thread_local int g_lt_device = -1;
+// heuristic picks per (device, m, n, k, batch, workspace): the query costs
+// tens of microseconds, the product of a 1024^3 DD call about 45
+using AlgoKey = std::tuple<int, int64_t, int64_t, int64_t, int64_t, size_t>;
+thread_local std::map<AlgoKey, cublasLtMatmulAlgo_t> g_algos;
 
 }  // namespace
 
@@ -33,6 +39,7 @@ int int8_gemm_batched(int64_t m, int64_t n, int64_t k, int64_t batch, const int8
   int dev = 0;
   cudaGetDevice(&dev);
   if (g_lt == nullptr || g_lt_device != dev) {
+    g_algos.clear();
     if (cublasLtCreate(&g_lt) != CUBLAS_STATUS_SUCCESS) {
       *err = "cublasLtCreate failed";
       return 2;
@@ -77,15 +84,20 @@ int int8_gemm_batched(int64_t m, int64_t n, int64_t k, int64_t batch, const int8
   uint64_t wss = ws_size;
   cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wss,
                                        sizeof wss);
-  cublasLtMatmulHeuristicResult_t heur{};
-  int found = 0;
-  if (cublasLtMatmulAlgoGetHeuristic(g_lt, op, la, lb, lc, lc, pref, 1, &heur, &found) !=
-          CUBLAS_STATUS_SUCCESS ||
-      found == 0)
-    return bad("no int8 algorithm for this shape");
+  const AlgoKey key{dev, m, n, k, batch, ws_size};
+  auto it = g_algos.find(key);
+  if (it == g_algos.end()) {
+    cublasLtMatmulHeuristicResult_t heur{};
+    int found = 0;
+    if (cublasLtMatmulAlgoGetHeuristic(g_lt, op, la, lb, lc, lc, pref, 1, &heur, &found) !=
+            CUBLAS_STATUS_SUCCESS ||
+        found == 0)
+      return bad("no int8 algorithm for this shape");
+    it = g_algos.emplace(key, heur.algo).first;
+  }
   const int32_t alpha = 1, beta = 0;
   cublasStatus_t st = cublasLtMatmul(g_lt, op, &alpha, Bt, la, A, lb, &beta, C, lc, C, lc,
-                                     &heur.algo, workspace, ws_size, stream);
+                                     &it->second, workspace, ws_size, stream);
   cleanup();
   if (st != CUBLAS_STATUS_SUCCESS) {
     *err = "cublasLtMatmul failed (status " + std::to_string(static_cast<int>(st)) + ")";

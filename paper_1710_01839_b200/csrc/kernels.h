@@ -95,13 +95,14 @@ cudaError_t assemble_launch(int comps, const double* draws, int64_t count, doubl
 
 // exact int8 tensor-core mode (ozaki.cu, int8gemm.cpp)
 cudaError_t oz_scan_launch(int by_cols, const double* X, int64_t ld, int rows, int cols, int comps,
-                           int c0, int c1, int* E, int* L, cudaStream_t s);
+                           int* EL, int* status, cudaStream_t s);
 cudaError_t oz_residues_launch(int by_cols, const double* X, int64_t ld, int rows, int cols,
-                               int comps, int c0, int c1, const int* shift, int N,
-                               const uint8_t* pow2, int xmax, int8_t* R, int64_t rpitch,
-                               int64_t rplane, cudaStream_t s);
+                               int comps, int c0, int c1, const int* shift, int N, int W,
+                               int8_t* R, int64_t rpitch, int64_t rplane, cudaStream_t s);
 cudaError_t oz_combine_launch(int comps, const void* jobs, int njobs, int m, int n, double* C,
-                              int* status, cudaStream_t s, const void* host_job);
+                              int* status, cudaStream_t s);
+cudaError_t oz_shifts_launch(int comps, int nranges, const int* ranges, int odim, const int* EL,
+                             int* shift, int* beta, cudaStream_t s);
 int int8_gemm_batched(int64_t m, int64_t n, int64_t k, int64_t batch, const int8_t* A,
                       const int8_t* Bt, int32_t* C, void* workspace, size_t ws_size,
                       cudaStream_t stream, std::string* err);

@@ -35,22 +35,6 @@ __constant__ int kModsDev[54] = {
     121, 113, 109, 107, 103, 101, 97,  89,  83,  79,  73,  71,  67,  61,
     59,  53,  49,  47,  43,  41,  37,  31,  29,  23,  19,  17};
 constexpr int kNumMods = 54;
-// Lemire fastmod constants ceil(2^64 / p) and 2^32 mod p
-__constant__ unsigned long long kModM[54] = {
-    0x0100000000000000ull, 0x0105197f7d734042ull, 0x010db20a88f4695aull, 0x010fef010fef0110ull,
-    0x0112358e75d30337ull, 0x0119453808ca29c1ull, 0x011e2ef3b3fb8745ull, 0x0120b470c67c0d89ull,
-    0x0125e22708092f12ull, 0x013698df3de0747aull, 0x0149539e3b2d066full, 0x014cab88725af6e8ull,
-    0x015390948f40feadull, 0x01571ed3c506b39bull, 0x016a13cd15372905ull, 0x016e1f76b4337c6dull,
-    0x017ad2208e0ecc36ull, 0x0183c977ab2bedd3ull, 0x01886e5f0abb049aull, 0x01920fb49d0e228eull,
-    0x01a16d3f97a4b01bull, 0x01b2036406c80d91ull, 0x01b7d6c3dda338b3ull, 0x01d77b654b82c33aull,
-    0x01de5d6e3f8868a5ull, 0x01f44659e4a42716ull, 0x0204081020408103ull, 0x020c49ba5e353f7dull,
-    0x021d9ead7cd391fcull, 0x0243f6f0243f6f03ull, 0x02593f69b02593f7ull, 0x02647c69456217edull,
-    0x027c45979c952050ull, 0x0288df0cac5b3f5eull, 0x02a3a0fd5c5f02a4ull, 0x02e05c0b81702e06ull,
-    0x03159721ed7e7535ull, 0x033d91d2a2067b24ull, 0x0381c0e070381c0full, 0x039b0ad12073615bull,
-    0x03d226357e16ece6ull, 0x04325c53ef368eb1ull, 0x0456c797dd49c342ull, 0x04d4873ecade304eull,
-    0x05397829cbc14e5full, 0x0572620ae4c415caull, 0x05f417d05f417d06ull, 0x063e7063e7063e71ull,
-    0x06eb3e45306eb3e5ull, 0x0842108421084211ull, 0x08d3dcb08d3dcb09ull, 0x0b21642c8590b217ull,
-    0x0d79435e50d79436ull, 0x0f0f0f0f0f0f0f10ull};
 __constant__ unsigned kMod2p32[54] = {
     0,  123, 130, 15, 110, 8,  161, 176, 7,  51, 46, 88, 108, 147, 15, 126, 96, 113,
     7,  100, 93,  4,  129, 41, 34,  117, 16, 46, 59, 16, 75,  29,  63, 68,  35, 45,
@@ -71,13 +55,6 @@ __constant__ unsigned kModMu[54] = {
 __device__ __forceinline__ unsigned barrett(unsigned x, unsigned mu, unsigned p) {
   unsigned r = x - __umulhi(x, mu) * p;
   return r >= p ? r - p : r;
-}
-
-// a mod d for 32-bit a (Lemire, Kaser, Kurz: "Faster remainder by direct
-// computation"), M = ceil(2^64 / d)
-__device__ __forceinline__ unsigned fastmod(unsigned a, unsigned long long M, unsigned d) {
-  unsigned long long low = M * a;
-  return static_cast<unsigned>(__umul64hi(low, d));
 }
 
 namespace {
@@ -103,178 +80,296 @@ __device__ __forceinline__ bool is_zero(double x) {
   return (static_cast<unsigned long long>(__double_as_longlong(x)) << 1) == 0ull;
 }
 
+__device__ __forceinline__ bool not_finite(double x) {
+  return ((static_cast<unsigned long long>(__double_as_longlong(x)) >> 52) & 0x7ff) == 0x7ff;
+}
+
 constexpr int kEmptyE = -100000, kEmptyL = 100000;
 
-// one warp per row: E = max top_exp, L = min low_bit over the components
-// [c0, c1) of the row's entries
+// One pass over a matrix: per row (by_cols 0) or column (1) and per
+// component c, E[c] = max top_exp and L[c] = min low_bit over the nonzero
+// entries; any non-finite component sets bit 0 of *status.  EL layout:
+// E[comps][odim] then L[comps][odim].
+template <int NC>
 __global__ void scan_rows_kernel(const double* __restrict__ X, int64_t ld, int rows, int cols,
-                                 int comps, int c0, int c1, int* __restrict__ E,
-                                 int* __restrict__ L) {
-  int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
+                                 int* __restrict__ EL, int* __restrict__ status) {
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (r >= rows) return;
-  int e = kEmptyE, lo = kEmptyL;
+  int e[NC], lo[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) e[c] = kEmptyE, lo[c] = kEmptyL;
+  bool bad = false;
   for (int k = lane; k < cols; k += 32) {
-    const double* p = X + ((int64_t)r * ld + k) * comps;
-    for (int c = c0; c < c1; ++c) {
-      double v = p[c];
+    const double* p = X + ((int64_t)r * ld + k) * NC;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const double v = p[c];
+      bad |= not_finite(v);
       if (!is_zero(v)) {
-        e = max(e, top_exp(v));
-        lo = min(lo, low_bit(v));
+        e[c] = max(e[c], top_exp(v));
+        lo[c] = min(lo[c], low_bit(v));
       }
     }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    e = max(e, __shfl_xor_sync(0xffffffffu, e, o));
-    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-  }
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      e[c] = max(e[c], __shfl_xor_sync(0xffffffffu, e[c], o));
+      lo[c] = min(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+    }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, 1);
   if (lane == 0) {
-    E[r] = e;
-    L[r] = lo;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      EL[c * rows + r] = e[c];
+      EL[(NC + c) * rows + r] = lo[c];
+    }
+  }
+}
+
+__global__ void fill_el_kernel(int* __restrict__ EL, int nc, int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < nc * n) {
+    EL[j] = kEmptyE;
+    EL[nc * n + j] = kEmptyL;
   }
 }
 
 // columns: a 32-column x 64-row tile per block (coalesced along the row),
-// block reduction over the rows, then one atomic per column
+// block reduction over the rows, then one atomic per column and component
+template <int NC>
 __global__ void scan_cols_kernel(const double* __restrict__ X, int64_t ld, int rows, int cols,
-                                 int comps, int c0, int c1, int* __restrict__ E,
-                                 int* __restrict__ L) {
-  __shared__ int se[8][32], sl[8][32];
+                                 int* __restrict__ EL, int* __restrict__ status) {
+  __shared__ int se[NC][8][32], sl[NC][8][32];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + tx;
-  int e = kEmptyE, lo = kEmptyL;
+  int e[NC], lo[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) e[c] = kEmptyE, lo[c] = kEmptyL;
+  bool bad = false;
   if (j < cols) {
     const int k0 = blockIdx.y * 64;
     for (int k = k0 + ty; k < rows && k < k0 + 64; k += 8) {
-      const double* p = X + ((int64_t)k * ld + j) * comps;
-      for (int c = c0; c < c1; ++c) {
-        double v = p[c];
+      const double* p = X + ((int64_t)k * ld + j) * NC;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const double v = p[c];
+        bad |= not_finite(v);
         if (!is_zero(v)) {
-          e = max(e, top_exp(v));
-          lo = min(lo, low_bit(v));
+          e[c] = max(e[c], top_exp(v));
+          lo[c] = min(lo[c], low_bit(v));
         }
       }
     }
   }
-  se[ty][tx] = e;
-  sl[ty][tx] = lo;
+  if (__any_sync(0xffffffffu, bad) && tx == 0) atomicOr(status, 1);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    se[c][ty][tx] = e[c];
+    sl[c][ty][tx] = lo[c];
+  }
   __syncthreads();
   if (ty == 0 && j < cols) {
-    for (int q = 1; q < 8; ++q) {
-      e = max(e, se[q][tx]);
-      lo = min(lo, sl[q][tx]);
-    }
-    if (e != kEmptyE) {
-      atomicMax(E + j, e);
-      atomicMin(L + j, lo);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      for (int q = 1; q < 8; ++q) {
+        e[c] = max(e[c], se[c][q][tx]);
+        lo[c] = min(lo[c], sl[c][q][tx]);
+      }
+      if (e[c] != kEmptyE) {
+        atomicMax(EL + c * cols + j, e[c]);
+        atomicMin(EL + (NC + c) * cols + j, lo[c]);
+      }
     }
   }
 }
 
-__global__ void fill2_kernel(int* __restrict__ E, int* __restrict__ L, int n) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j < n) {
-    E[j] = kEmptyE;
-    L[j] = kEmptyL;
-  }
-}
+// ---------------------------------------------------------------------------
+// residues
+// ---------------------------------------------------------------------------
 
-// Residues of sum_{c < NC} x_{c0+c} 2^shift (an exact integer) modulo the
-// first N moduli, centred into int8, for 4 consecutive entries per thread
-// (one packed 32-bit store per modulus).  pow2: shared-memory N x xmax
-// table of 2^x mod p_t.  All reductions are 32-bit Barrett steps (4
-// integer instructions each): a 53-bit mantissa is hi*2^32 + lo, hi < 2^21.
-template <int NC>
-struct EntryParts {
-  unsigned mlo[NC], mhi[NC];
-  int ex[NC];
-  bool neg[NC], use[NC];
+constexpr int kMaxW = 12;   // 32-bit words of one scaled entry (384 bits)
 
-  __device__ __forceinline__ void load(const double* x, int shift, int xmax) {
-#pragma unroll
-    for (int q = 0; q < NC; ++q) {
-      double v = x[q];
-      use[q] = !is_zero(v);
-      unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
-      int be = static_cast<int>((b >> 52) & 0x7ff);
-      unsigned long long m = b & ((1ull << 52) - 1);
-      if (be > 0) m |= (1ull << 52);
-      int e = (be > 0 ? be - 1075 : -1074) + shift;
-      int tz = use[q] ? __ffsll(static_cast<long long>(m)) - 1 : 0;
-      m >>= tz;
-      e += tz;                    // >= 0 by the choice of shift (scan_*)
-      mlo[q] = static_cast<unsigned>(m);
-      mhi[q] = static_cast<unsigned>(m >> 32);
-      ex[q] = use[q] ? (e < xmax ? e : xmax - 1) : 0;
-      neg[q] = (b >> 63) != 0;
-    }
-  }
-
-  __device__ __forceinline__ unsigned residue(int t, unsigned p, unsigned mu, unsigned c32,
-                                              const uint8_t* pow2, int xmax) const {
-    // terms mr * 2^e mod-p factor stay below 2^16; negative terms add
-    // p * 2^16 - term, so the sum stays positive and < 2^(17 + log2 NC)
-    unsigned acc = 0;
-#pragma unroll
-    for (int q = 0; q < NC; ++q) {
-      unsigned mr = barrett(mhi[q] * c32 + barrett(mlo[q], mu, p), mu, p);
-      unsigned term = use[q] ? mr * pow2[t * xmax + ex[q]] : 0u;
-      acc += neg[q] ? (p << 16) - term : term;
-    }
-    int r = static_cast<int>(barrett(acc, mu, p));
-    if (r >= static_cast<int>((p + 1) / 2)) r -= static_cast<int>(p);   // [-(p-1)/2, p/2)
-    return static_cast<unsigned>(r) & 0xffu;
-  }
+// Constant tables for the residue dot products, built at compile time:
+//   w4[t][w]   the 4 bytes 2^(8(4w+j)) mod p_t, centred into int8, packed
+//   top[t][W]  (p_t - 2^(32W) mod p_t) mod p_t  (two's-complement sign fix)
+//   bias[t]    a multiple of p_t >= 2^22 (keeps the dot product positive)
+struct ResidueTables {
+  uint32_t w4[kNumMods][kMaxW];
+  uint32_t top[kNumMods][kMaxW + 1];
+  uint32_t bias[kNumMods];
 };
 
-__device__ __forceinline__ void load_pow2(const uint8_t* __restrict__ g, uint8_t* s, int n) {
-  for (int q = threadIdx.x; q < n; q += blockDim.x) s[q] = g[q];
-  __syncthreads();
+constexpr int kModsHost[kNumMods] = {
+    256, 251, 243, 241, 239, 233, 229, 227, 223, 211, 199, 197, 193, 191,
+    181, 179, 173, 169, 167, 163, 157, 151, 149, 139, 137, 131, 127, 125,
+    121, 113, 109, 107, 103, 101, 97,  89,  83,  79,  73,  71,  67,  61,
+    59,  53,  49,  47,  43,  41,  37,  31,  29,  23,  19,  17};
+
+constexpr ResidueTables make_residue_tables() {
+  ResidueTables T{};
+  for (int t = 0; t < kNumMods; ++t) {
+    const uint32_t p = static_cast<uint32_t>(kModsHost[t]);
+    uint32_t pw = 1 % p;                    // 2^(8i) mod p
+    for (int w = 0; w < kMaxW; ++w) {
+      uint32_t packed = 0;
+      for (int j = 0; j < 4; ++j) {
+        int c = static_cast<int>(pw);
+        if (c > static_cast<int>(p / 2)) c -= static_cast<int>(p);
+        if (c > 127) c -= static_cast<int>(p);   // p = 256: 0..255 -> -128..127
+        packed |= (static_cast<uint32_t>(c) & 0xffu) << (8 * j);
+        pw = (pw * 256u) % p;
+      }
+      T.w4[t][w] = packed;
+    }
+    uint32_t q = 1 % p;                     // 2^(32W) mod p
+    for (int W = 0; W <= kMaxW; ++W) {
+      T.top[t][W] = (p - q) % p;
+      for (int s = 0; s < 32; ++s) q = (q * 2u) % p;
+    }
+    T.bias[t] = p * ((1u << 22) / p + 1u);
+  }
+  return T;
 }
 
-// by_cols 0: A (rows x cols) -> R[t][row][k], k = the column;
-// by_cols 1: B (rows=l x cols=n) -> R[t][col][k], k = the row.
-// Each thread takes 4 consecutive k of one row/column; the packed int8x4
-// stores coalesce along k.  Requires cols (rows) % 4 == 0 (host pads).
-template <int NC, int BYCOLS>
+__constant__ ResidueTables kRes = make_residue_tables();
+
+__device__ __forceinline__ int dp4a_us(uint32_t a, uint32_t b, int c) {
+  int d;
+  asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+// sum_{c < NC} x[c] * 2^shift as a W-word two's-complement integer
+// (little-endian 32-bit words).  Every nonzero component is an integer
+// multiple of 2^-shift (scan), and |sum| < 2^(32W-1) (host choice of W).
+template <int NC, int W>
+__device__ __forceinline__ void entry_words(const double* x, int shift, bool valid,
+                                            uint32_t (&X)[W]) {
+#pragma unroll
+  for (int w = 0; w < W; ++w) X[w] = 0;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    const double v = valid ? x[c] : 0.0;
+    if (is_zero(v)) continue;
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    const int be = static_cast<int>((b >> 52) & 0x7ff);
+    unsigned long long m = b & ((1ull << 52) - 1);
+    if (be > 0) m |= (1ull << 52);
+    const int tz = __ffsll(static_cast<long long>(m)) - 1;
+    m >>= tz;
+    const int e = (be > 0 ? be - 1075 : -1074) + shift + tz;   // >= 0
+    const int q = e >> 5, r = e & 31;
+    const unsigned long long t0 = m << r;
+    const uint32_t d0 = static_cast<uint32_t>(t0), d1 = static_cast<uint32_t>(t0 >> 32);
+    const uint32_t d2 = r ? static_cast<uint32_t>(m >> (64 - r)) : 0u;
+    const bool neg = (b >> 63) != 0;
+    unsigned long long carry = neg ? 1ull : 0ull;   // x - d == x + ~d + 1
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      uint32_t d = w == q ? d0 : (w == q + 1 ? d1 : (w == q + 2 ? d2 : 0u));
+      if (neg) d = ~d;
+      const unsigned long long s = static_cast<unsigned long long>(X[w]) + d + carry;
+      X[w] = static_cast<uint32_t>(s);
+      carry = s >> 32;
+    }
+  }
+}
+
+// centred residue of the W-word integer X modulo p_t, as an int8 byte
+template <int W>
+__device__ __forceinline__ uint32_t residue_byte(const uint32_t (&X)[W], uint32_t p,
+                                                 uint32_t mu, uint32_t top, uint32_t bias,
+                                                 const uint32_t (&wt)[W]) {
+  int acc = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) acc = dp4a_us(X[w], wt[w], acc);
+  uint32_t x = static_cast<uint32_t>(acc + static_cast<int>(bias)) +
+               ((X[W - 1] >> 31) ? top : 0u);
+  uint32_t r = barrett(x, mu, p);
+  int c = static_cast<int>(r);
+  if (c > static_cast<int>(p / 2)) c -= static_cast<int>(p);
+  if (c > 127) c -= static_cast<int>(p);
+  return static_cast<uint32_t>(c) & 0xffu;
+}
+
+template <int W>
+__device__ __forceinline__ void load_weights(int t, uint32_t (&wt)[W], uint32_t& p, uint32_t& mu,
+                                             uint32_t& top, uint32_t& bias) {
+  p = static_cast<uint32_t>(kModsDev[t]);
+  mu = kModMu[t];
+  top = kRes.top[t][W];
+  bias = kRes.bias[t];
+#pragma unroll
+  for (int w = 0; w < W; ++w) wt[w] = kRes.w4[t][w];
+}
+
+// A side: R[t][row][k], 4 consecutive k of one row per thread (reads and
+// the packed int8x4 stores both coalesce along k).
+template <int NC, int W>
 __global__ void __launch_bounds__(256)
-residues_kernel(const double* __restrict__ X, int64_t ld, int rows, int cols, int comps, int c0,
-                const int* __restrict__ shift, int N, const uint8_t* __restrict__ pow2, int xmax,
-                int8_t* __restrict__ R, int64_t rpitch, int64_t rplane) {
-  extern __shared__ uint8_t spow2[];
-  load_pow2(pow2, spow2, N * xmax);
-  const int kdim = BYCOLS ? rows : cols;       // the contiguous (k) extent
-  const int odim = BYCOLS ? cols : rows;       // rows of R
-  const int64_t quads = static_cast<int64_t>(odim) * ((kdim + 3) / 4);
+residues_rows_kernel(const double* __restrict__ X, int64_t ld, int rows, int cols, int comps,
+                     int c0, const int* __restrict__ shift, int N, int8_t* __restrict__ R,
+                     int64_t rpitch, int64_t rplane) {
+  const int per = (cols + 3) / 4;
   const int64_t qd = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (qd >= quads) return;
-  const int per = (kdim + 3) / 4;
+  if (qd >= static_cast<int64_t>(rows) * per) return;
   const int o = static_cast<int>(qd / per), k0 = static_cast<int>(qd % per) * 4;
   const int sh = shift[o];
-  EntryParts<NC> ent[4];
+  uint32_t Xw[4][W];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int k = k0 + u < kdim ? k0 + u : kdim - 1;
-    const double* src = BYCOLS ? X + ((int64_t)k * ld + o) * comps + c0
-                               : X + ((int64_t)o * ld + k) * comps + c0;
-    ent[u].load(src, sh, xmax);
-  }
-  const bool full = k0 + 4 <= kdim;
+  for (int u = 0; u < 4; ++u)
+    entry_words<NC, W>(X + ((int64_t)o * ld + k0 + u) * comps + c0, sh, k0 + u < cols, Xw[u]);
   int8_t* dst = R + static_cast<int64_t>(o) * rpitch + k0;
 #pragma unroll 1
   for (int t = 0; t < N; ++t) {
-    const unsigned p = static_cast<unsigned>(kModsDev[t]);
-    const unsigned mu = kModMu[t];
-    const unsigned c32 = kMod2p32[t];
-    unsigned word = 0;
+    uint32_t wt[W], p, mu, top, bias;
+    load_weights<W>(t, wt, p, mu, top, bias);
+    uint32_t word = 0;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) word |= ent[u].residue(t, p, mu, c32, spow2, xmax) << (8 * u);
-    if (full) {
-      *reinterpret_cast<unsigned*>(dst + t * rplane) = word;
-    } else {
-      for (int u = 0; k0 + u < kdim; ++u) dst[t * rplane + u] = static_cast<int8_t>(word >> (8 * u));
-    }
+    for (int u = 0; u < 4; ++u) word |= residue_byte<W>(Xw[u], p, mu, top, bias, wt) << (8 * u);
+    *reinterpret_cast<uint32_t*>(dst + t * rplane) = word;
+  }
+}
+
+// B side: R[t][col][k] (B transposed).  A block covers 32 columns x 32 k:
+// lane = column (coalesced reads along the row of B), warp = k quad; the
+// packed words go through shared memory so each column's 32 k leave as
+// one 32-byte sector.
+template <int NC, int W>
+__global__ void __launch_bounds__(256)
+residues_cols_kernel(const double* __restrict__ X, int64_t ld, int rows, int cols, int comps,
+                     int c0, const int* __restrict__ shift, int N, int8_t* __restrict__ R,
+                     int64_t rpitch, int64_t rplane) {
+  __shared__ uint32_t S[2][32][9];
+  const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
+  const int o = blockIdx.x * 32 + lane;
+  const int k0 = blockIdx.y * 32 + wq * 4;
+  const bool col_ok = o < cols;
+  const int sh = col_ok ? shift[o] : 0;
+  uint32_t Xw[4][W];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    entry_words<NC, W>(X + ((int64_t)(k0 + u) * ld + o) * comps + c0, sh,
+                       col_ok && k0 + u < rows, Xw[u]);
+  // write-out mapping: 8 threads per column, one k quad each
+  const int oc = threadIdx.x >> 3, qq = threadIdx.x & 7;
+  const int og = blockIdx.x * 32 + oc;
+  const int kq = blockIdx.y * 32 + qq * 4;
+  int8_t* dst = R + static_cast<int64_t>(og) * rpitch + kq;
+  const bool store = og < cols && kq < rows;
+#pragma unroll 1
+  for (int t = 0; t < N; ++t) {
+    uint32_t wt[W], p, mu, top, bias;
+    load_weights<W>(t, wt, p, mu, top, bias);
+    uint32_t word = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) word |= residue_byte<W>(Xw[u], p, mu, top, bias, wt) << (8 * u);
+    S[t & 1][lane][wq] = word;
+    __syncthreads();
+    if (store) *reinterpret_cast<uint32_t*>(dst + t * rplane) = S[t & 1][oc][qq];
   }
 }
 
@@ -292,6 +387,13 @@ struct CrtJob {
   const uint32_t* table;    // [K] P limbs, then [N][K] weight limbs
   int N, K;
   int64_t gpitch, gplane;
+};
+
+constexpr int kMaxJobs = 16;
+
+// up to kMaxJobs jobs by value (kernel parameter space, no device table)
+struct CrtJobs {
+  CrtJob j[kMaxJobs];
 };
 
 // ---------------------------------------------------------------------------
@@ -366,36 +468,80 @@ __device__ __forceinline__ bool limbs_sub_double(int64_t (&mag)[K], double d, in
   return true;
 }
 
+// sum_q v[q] 2^(32q), rounded (top limbs first; the powers are exact
+// compile-time constants, no ldexp)
 template <int K>
 __device__ __forceinline__ double limbs_double(const uint32_t (&v)[K + 1]) {
-  double d = 0.0;
+  double d = 0.0, scale = 1.0;
+  double sc[K + 1];
 #pragma unroll
-  for (int q = 0; q <= K; ++q) d += ldexp(static_cast<double>(v[q]), 32 * q);
+  for (int q = 0; q <= K; ++q) {
+    sc[q] = scale;
+    scale *= 4294967296.0;
+  }
+#pragma unroll
+  for (int q = K; q >= 0; --q) d += static_cast<double>(v[q]) * sc[q];
   return d;
 }
 
-// CRT reconstruction of one job's output (i, j): the centred integer X as
-// sign + K magnitude limbs.  sW: P (K limbs) then the N weights (K limbs each).
-template <int K>
-__device__ __forceinline__ bool crt_reconstruct(const int32_t* __restrict__ Gij, int64_t gplane,
-                                                int N, const uint32_t* sW, int64_t (&mag)[K]) {
-  const uint32_t* P = sW;
-  const uint32_t* W = sW + K;
-  uint64_t acc[K + 1];
+// p_t * floor(2^31 / p_t): added to a residue product g (|g| < 2^31 -
+// 2^14 for k <= 131071) it makes g nonnegative and below 2^32 without
+// changing g mod p_t, so one Barrett step reduces it
+__constant__ unsigned kGBias[54] = {
+#define MPMM_GB(p) (p) * (2147483648u / (p))
+    MPMM_GB(256), MPMM_GB(251), MPMM_GB(243), MPMM_GB(241), MPMM_GB(239), MPMM_GB(233),
+    MPMM_GB(229), MPMM_GB(227), MPMM_GB(223), MPMM_GB(211), MPMM_GB(199), MPMM_GB(197),
+    MPMM_GB(193), MPMM_GB(191), MPMM_GB(181), MPMM_GB(179), MPMM_GB(173), MPMM_GB(169),
+    MPMM_GB(167), MPMM_GB(163), MPMM_GB(157), MPMM_GB(151), MPMM_GB(149), MPMM_GB(139),
+    MPMM_GB(137), MPMM_GB(131), MPMM_GB(127), MPMM_GB(125), MPMM_GB(121), MPMM_GB(113),
+    MPMM_GB(109), MPMM_GB(107), MPMM_GB(103), MPMM_GB(101), MPMM_GB(97),  MPMM_GB(89),
+    MPMM_GB(83),  MPMM_GB(79),  MPMM_GB(73),  MPMM_GB(71),  MPMM_GB(67),  MPMM_GB(61),
+    MPMM_GB(59),  MPMM_GB(53),  MPMM_GB(49),  MPMM_GB(47),  MPMM_GB(43),  MPMM_GB(41),
+    MPMM_GB(37),  MPMM_GB(31),  MPMM_GB(29),  MPMM_GB(23),  MPMM_GB(19),  MPMM_GB(17)};
+#undef MPMM_GB
+
+// CRT accumulation of one output: acc[q] = sum_t r_t W_t[q] with
+// r_t = G_t mod p_t, in K+1 64-bit limb sums.  W: the N weights, row
+// stride WS >= K limbs (16-byte aligned rows: vector loads), in shared
+// memory.  The G planes are read 8 at a time (eight loads in flight).
+template <int K, int WS>
+__device__ __forceinline__ void crt_accumulate(const int32_t* G, int64_t gplane, int N,
+                                               const uint32_t* W, uint64_t (&acc)[K + 1]) {
+  constexpr int CH = 8;
 #pragma unroll
   for (int q = 0; q <= K; ++q) acc[q] = 0;
-#pragma unroll 2
-  for (int t = 0; t < N; ++t) {
-    const unsigned p = static_cast<unsigned>(kModsDev[t]);
-    const int g = Gij[t * gplane];
-    unsigned r = barrett(static_cast<unsigned>(g), kModMu[t], p);
-    if (g < 0) {                 // (g + 2^32) mod p  ->  g mod p
-      r = r + p - kMod2p32[t];
-      if (r >= p) r -= p;
+  for (int t0 = 0; t0 < N; t0 += CH) {
+    int g[CH];
+    const int32_t* gp = G + t0 * gplane;
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      g[u] = t0 + u < N ? __ldcs(gp) : 0;
+      gp += gplane;
     }
 #pragma unroll
-    for (int q = 0; q < K; ++q) acc[q] += static_cast<uint64_t>(r) * W[t * K + q];
+    for (int u = 0; u < CH; ++u) {
+      const int t = t0 + u;
+      if (t >= N) break;
+      const unsigned p = static_cast<unsigned>(kModsDev[t]);
+      const unsigned r = barrett(static_cast<unsigned>(g[u]) + kGBias[t], kModMu[t], p);
+      const uint4* wv = reinterpret_cast<const uint4*>(W + t * WS);
+#pragma unroll
+      for (int q4 = 0; q4 < WS / 4; ++q4) {
+        const uint4 v = wv[q4];
+        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (4 * q4 + e < K) acc[4 * q4 + e] += static_cast<uint64_t>(r) * w4[e];
+      }
+    }
   }
+}
+
+// From the accumulated sums: the centred integer X = (sum mod P) as sign +
+// K magnitude limbs.  P: K limbs.
+template <int K>
+__device__ __forceinline__ bool crt_finish(const uint64_t (&acc)[K + 1], const uint32_t* P,
+                                           int64_t (&mag)[K]) {
   uint32_t S[K + 1];
   uint64_t carry = 0;
 #pragma unroll
@@ -470,19 +616,33 @@ __device__ __forceinline__ bool crt_reconstruct(const int32_t* __restrict__ Gij,
   return upper;
 }
 
+__host__ __device__ constexpr int wstride(int K) { return (K + 3) / 4 * 4; }
+
+// Stage a job's CRT table in shared memory: P (K limbs, stride WS) then the
+// N weights, each row padded to WS limbs (16-byte aligned).
+template <int K>
+__device__ __forceinline__ void stage_table(const uint32_t* __restrict__ table, int N,
+                                            uint32_t* sW) {
+  constexpr int WS = wstride(K);
+  for (int q = threadIdx.x; q < (N + 1) * WS; q += blockDim.x) {
+    const int row = q / WS, col = q % WS;
+    sW[q] = col < K ? table[row * K + col] : 0u;
+  }
+}
+
+// CRT reconstruction of one job's output from a staged table.
+template <int K>
+__device__ __forceinline__ bool crt_reconstruct(const int32_t* Gij, int64_t gplane, int N,
+                                                const uint32_t* sW, int64_t (&mag)[K]) {
+  constexpr int WS = wstride(K);
+  uint64_t acc[K + 1];
+  crt_accumulate<K, WS>(Gij, gplane, N, sW + WS, acc);
+  return crt_finish<K>(acc, sW, mag);
+}
+
 template <int COMPS, int K>
-__global__ void __launch_bounds__(128)
-combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __restrict__ status) {
-  __shared__ uint32_t sW[(kNumMods + 1) * K];
-  for (int q = threadIdx.x; q < (jb.N + 1) * K; q += blockDim.x) sW[q] = jb.table[q];
-  __syncthreads();
-  int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= static_cast<int64_t>(m) * n) return;
-  const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
-  int64_t mag[K];
-  bool neg = crt_reconstruct<K>(jb.G + static_cast<int64_t>(i) * jb.gpitch + j, jb.gplane, jb.N,
-                                sW, mag);
-  const int ebase = -(jb.srow[i] + jb.scol[j]);
+__device__ __forceinline__ void round_out(int64_t (&mag)[K], bool neg, int ebase, double* dst,
+                                          bool& bad) {
   double out[COMPS];
 #pragma unroll
   for (int c = 0; c < COMPS; ++c) {
@@ -490,12 +650,28 @@ combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __re
     out[c] = neg ? -d : d;
     neg = neg ^ limbs_sub_double<K>(mag, d, ebase);
   }
-  bool bad = false;
 #pragma unroll
   for (int c = 0; c < COMPS; ++c) {
-    C[e * COMPS + c] = out[c];
+    dst[c] = out[c];
     bad |= !isfinite(out[c]);
   }
+}
+
+// single job: one output per thread, weights from shared memory
+template <int COMPS, int K>
+__global__ void __launch_bounds__(128)
+combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __restrict__ status) {
+  __shared__ __align__(16) uint32_t sW[(kNumMods + 1) * wstride(K)];
+  stage_table<K>(jb.table, jb.N, sW);
+  __syncthreads();
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= static_cast<int64_t>(m) * n) return;
+  const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
+  int64_t mag[K];
+  const bool neg = crt_reconstruct<K>(jb.G + static_cast<int64_t>(i) * jb.gpitch + j, jb.gplane,
+                                      jb.N, sW, mag);
+  bool bad = false;
+  round_out<COMPS, K>(mag, neg, -(jb.srow[i] + jb.scol[j]), C + e * COMPS, bad);
   if (bad) atomicOr(status, 1);
 }
 
@@ -507,19 +683,16 @@ combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __re
 
 constexpr int kMTB = 128;     // threads per block
 constexpr int kMWin = 28;     // window digits (896 bits)
-constexpr int kMaxJobs = 16;
 
 template <int COMPS, int K>
 __global__ void __launch_bounds__(kMTB)
-combine_multi_kernel(const CrtJob* __restrict__ jobs, int njobs, int m, int n,
+combine_multi_kernel(const CrtJobs jobs, int njobs, int m, int n,
                      double* __restrict__ C, int* __restrict__ status) {
   extern __shared__ unsigned char smraw[];
   int64_t* win = reinterpret_cast<int64_t*>(smraw);                   // [kMWin][kMTB]
-  uint32_t* tabs = reinterpret_cast<uint32_t*>(win + kMWin * kMTB);   // [njobs][(55)*K]
-  const int tstride = (kNumMods + 1) * K;
-  for (int J = 0; J < njobs; ++J)
-    for (int q = threadIdx.x; q < (jobs[J].N + 1) * K; q += blockDim.x)
-      tabs[J * tstride + q] = jobs[J].table[q];
+  uint32_t* tabs = reinterpret_cast<uint32_t*>(win + kMWin * kMTB);   // [njobs][55 * WS]
+  const int tstride = (kNumMods + 1) * wstride(K);
+  for (int J = 0; J < njobs; ++J) stage_table<K>(jobs.j[J].table, jobs.j[J].N, tabs + J * tstride);
   __syncthreads();
   const int tid = threadIdx.x;
   int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + tid;
@@ -528,9 +701,9 @@ combine_multi_kernel(const CrtJob* __restrict__ jobs, int njobs, int m, int n,
 #define WIN(q) win[(q) * kMTB + tid]
   for (int q = 0; q < kMWin; ++q) WIN(q) = 0;
   int ebase = 1 << 30;
-  for (int J = 0; J < njobs; ++J) ebase = min(ebase, -(jobs[J].srow[i] + jobs[J].scol[j]));
+  for (int J = 0; J < njobs; ++J) ebase = min(ebase, -(jobs.j[J].srow[i] + jobs.j[J].scol[j]));
   for (int J = 0; J < njobs; ++J) {
-    const CrtJob& jb = jobs[J];
+    const CrtJob& jb = jobs.j[J];
     int64_t mag[K];
     const bool neg = crt_reconstruct<K>(jb.G + static_cast<int64_t>(i) * jb.gpitch + j, jb.gplane,
                                         jb.N, tabs + J * tstride, mag);
@@ -618,57 +791,66 @@ combine_multi_kernel(const CrtJob* __restrict__ jobs, int njobs, int m, int n,
 // ---------------------------------------------------------------------------
 
 cudaError_t oz_scan_launch(int by_cols, const double* X, int64_t ld, int rows, int cols, int comps,
-                           int c0, int c1, int* E, int* L, cudaStream_t s) {
+                           int* EL, int* status, cudaStream_t s) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (by_cols) {
-    fill2_kernel<<<(cols + 255) / 256, 256, 0, s>>>(E, L, cols);
+    fill_el_kernel<<<(comps * cols + 255) / 256, 256, 0, s>>>(EL, comps, cols);
     dim3 grid((cols + 31) / 32, (rows + 63) / 64);
-    scan_cols_kernel<<<grid, 256, 0, s>>>(X, ld, rows, cols, comps, c0, c1, E, L);
+    if (comps == 2)
+      scan_cols_kernel<2><<<grid, 256, 0, s>>>(X, ld, rows, cols, EL, status);
+    else
+      scan_cols_kernel<4><<<grid, 256, 0, s>>>(X, ld, rows, cols, EL, status);
   } else {
-    int64_t threads = static_cast<int64_t>(rows) * 32;
-    scan_rows_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(X, ld, rows, cols, comps,
-                                                                       c0, c1, E, L);
+    const int64_t threads = static_cast<int64_t>(rows) * 32;
+    const unsigned blocks = static_cast<unsigned>((threads + 127) / 128);
+    if (comps == 2)
+      scan_rows_kernel<2><<<blocks, 128, 0, s>>>(X, ld, rows, cols, EL, status);
+    else
+      scan_rows_kernel<4><<<blocks, 128, 0, s>>>(X, ld, rows, cols, EL, status);
+  }
+  return cudaGetLastError();
+}
+
+template <int NC, int W>
+static cudaError_t residues_go(int by_cols, const double* X, int64_t ld, int rows, int cols,
+                               int comps, int c0, const int* shift, int N, int8_t* R,
+                               int64_t rpitch, int64_t rplane, cudaStream_t s) {
+  if (by_cols) {
+    dim3 grid((cols + 31) / 32, (rows + 31) / 32);
+    residues_cols_kernel<NC, W><<<grid, 256, 0, s>>>(X, ld, rows, cols, comps, c0, shift, N, R,
+                                                      rpitch, rplane);
+  } else {
+    const int64_t quads = static_cast<int64_t>(rows) * ((cols + 3) / 4);
+    residues_rows_kernel<NC, W><<<(unsigned)((quads + 255) / 256), 256, 0, s>>>(
+        X, ld, rows, cols, comps, c0, shift, N, R, rpitch, rplane);
   }
   return cudaGetLastError();
 }
 
 template <int NC>
-static cudaError_t residues_go(int by_cols, const double* X, int64_t ld, int rows, int cols,
-                               int comps, int c0, const int* shift, int N, const uint8_t* pow2,
-                               int xmax, int8_t* R, int64_t rpitch, int64_t rplane,
-                               cudaStream_t s) {
-  const int kdim = by_cols ? rows : cols, odim = by_cols ? cols : rows;
-  const int64_t quads = static_cast<int64_t>(odim) * ((kdim + 3) / 4);
-  const unsigned blocks = static_cast<unsigned>((quads + 255) / 256);
-  const size_t smem = static_cast<size_t>(N) * xmax;
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  if (by_cols) {
-    cudaFuncSetAttribute(residues_kernel<NC, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    residues_kernel<NC, 1><<<blocks, 256, smem, s>>>(X, ld, rows, cols, comps, c0, shift, N, pow2,
-                                                     xmax, R, rpitch, rplane);
-  } else {
-    cudaFuncSetAttribute(residues_kernel<NC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    residues_kernel<NC, 0><<<blocks, 256, smem, s>>>(X, ld, rows, cols, comps, c0, shift, N, pow2,
-                                                     xmax, R, rpitch, rplane);
-  }
-  return cudaGetLastError();
+static cudaError_t residues_w(int W, int by_cols, const double* X, int64_t ld, int rows, int cols,
+                              int comps, int c0, const int* shift, int N, int8_t* R,
+                              int64_t rpitch, int64_t rplane, cudaStream_t s) {
+  // word counts are rounded up to an instantiated width (extra words are 0)
+  if (W <= 2) return residues_go<NC, 2>(by_cols, X, ld, rows, cols, comps, c0, shift, N, R, rpitch, rplane, s);
+  if (W <= 3) return residues_go<NC, 3>(by_cols, X, ld, rows, cols, comps, c0, shift, N, R, rpitch, rplane, s);
+  if (W <= 4) return residues_go<NC, 4>(by_cols, X, ld, rows, cols, comps, c0, shift, N, R, rpitch, rplane, s);
+  if (W <= 5) return residues_go<NC, 5>(by_cols, X, ld, rows, cols, comps, c0, shift, N, R, rpitch, rplane, s);
+  if (W <= 6) return residues_go<NC, 6>(by_cols, X, ld, rows, cols, comps, c0, shift, N, R, rpitch, rplane, s);
+  if (W <= 8) return residues_go<NC, 8>(by_cols, X, ld, rows, cols, comps, c0, shift, N, R, rpitch, rplane, s);
+  if (W <= kMaxW) return residues_go<NC, kMaxW>(by_cols, X, ld, rows, cols, comps, c0, shift, N, R, rpitch, rplane, s);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t oz_residues_launch(int by_cols, const double* X, int64_t ld, int rows, int cols,
-                               int comps, int c0, int c1, const int* shift, int N,
-                               const uint8_t* pow2, int xmax, int8_t* R, int64_t rpitch,
-                               int64_t rplane, cudaStream_t s) {
+                               int comps, int c0, int c1, const int* shift, int N, int W,
+                               int8_t* R, int64_t rpitch, int64_t rplane, cudaStream_t s) {
   if (static_cast<int64_t>(rows) * cols <= 0) return cudaSuccess;
-  if (N < 1 || N > kNumMods) return cudaErrorInvalidValue;
+  if (N < 1 || N > kNumMods || W < 1 || W > kMaxW) return cudaErrorInvalidValue;
   switch (c1 - c0) {
-    case 1: return residues_go<1>(by_cols, X, ld, rows, cols, comps, c0, shift, N, pow2, xmax, R,
-                                  rpitch, rplane, s);
-    case 2: return residues_go<2>(by_cols, X, ld, rows, cols, comps, c0, shift, N, pow2, xmax, R,
-                                  rpitch, rplane, s);
-    case 4: return residues_go<4>(by_cols, X, ld, rows, cols, comps, c0, shift, N, pow2, xmax, R,
-                                  rpitch, rplane, s);
+    case 1: return residues_w<1>(W, by_cols, X, ld, rows, cols, comps, c0, shift, N, R, rpitch, rplane, s);
+    case 2: return residues_w<2>(W, by_cols, X, ld, rows, cols, comps, c0, shift, N, R, rpitch, rplane, s);
+    case 4: return residues_w<4>(W, by_cols, X, ld, rows, cols, comps, c0, shift, N, R, rpitch, rplane, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -690,17 +872,17 @@ static cudaError_t combine_single(const CrtJob& jb, int m, int n, double* C, int
 }
 
 template <int COMPS>
-static cudaError_t combine_multi(const void* jobs, int njobs, int K, int m, int n, double* C,
+static cudaError_t combine_multi(const CrtJobs& jobs, int njobs, int K, int m, int n, double* C,
                                  int* status, unsigned blocks, cudaStream_t s) {
-  const CrtJob* J = static_cast<const CrtJob*>(jobs);
   const size_t smem = static_cast<size_t>(kMWin) * kMTB * sizeof(int64_t) +
-                      static_cast<size_t>(njobs) * (kNumMods + 1) * K * sizeof(uint32_t);
+                      static_cast<size_t>(njobs) * (kNumMods + 1) * ((K + 3) / 4 * 4) *
+                          sizeof(uint32_t);
   switch (K) {
 #define MPMM_K(KK)                                                                            \
   case KK:                                                                                    \
     cudaFuncSetAttribute(combine_multi_kernel<COMPS, KK>,                                     \
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
-    combine_multi_kernel<COMPS, KK><<<blocks, kMTB, smem, s>>>(J, njobs, m, n, C, status);    \
+    combine_multi_kernel<COMPS, KK><<<blocks, kMTB, smem, s>>>(jobs, njobs, m, n, C, status); \
     break;
     MPMM_K(1) MPMM_K(2) MPMM_K(3) MPMM_K(4) MPMM_K(5) MPMM_K(6) MPMM_K(7) MPMM_K(8) MPMM_K(9)
     MPMM_K(10) MPMM_K(11) MPMM_K(12)
@@ -711,12 +893,13 @@ static cudaError_t combine_multi(const void* jobs, int njobs, int K, int m, int 
   return cudaGetLastError();
 }
 
+// jobs: HOST array of njobs CrtJob records (device pointers inside)
 cudaError_t oz_combine_launch(int comps, const void* jobs, int njobs, int m, int n, double* C,
-                              int* status, cudaStream_t s, const void* host_job) {
+                              int* status, cudaStream_t s) {
   int64_t total = static_cast<int64_t>(m) * n;
   if (total <= 0) return cudaSuccess;
-  if (host_job == nullptr || njobs < 1 || njobs > kMaxJobs) return cudaErrorInvalidValue;
-  const CrtJob* hj = static_cast<const CrtJob*>(host_job);
+  if (jobs == nullptr || njobs < 1 || njobs > kMaxJobs) return cudaErrorInvalidValue;
+  const CrtJob* hj = static_cast<const CrtJob*>(jobs);
   int K = 0;
   for (int q = 0; q < njobs; ++q) K = hj[q].K > K ? hj[q].K : K;
   for (int q = 0; q < njobs; ++q)
@@ -726,9 +909,53 @@ cudaError_t oz_combine_launch(int comps, const void* jobs, int njobs, int m, int
     return comps == 2 ? combine_single<2>(*hj, m, n, C, status, blocks, s)
                       : combine_single<4>(*hj, m, n, C, status, blocks, s);
   }
+  CrtJobs all{};
+  for (int q = 0; q < njobs; ++q) all.j[q] = hj[q];
   unsigned blocks = static_cast<unsigned>((total + kMTB - 1) / kMTB);
-  return comps == 2 ? combine_multi<2>(jobs, njobs, K, m, n, C, status, blocks, s)
-                    : combine_multi<4>(jobs, njobs, K, m, n, C, status, blocks, s);
+  return comps == 2 ? combine_multi<2>(all, njobs, K, m, n, C, status, blocks, s)
+                    : combine_multi<4>(all, njobs, K, m, n, C, status, blocks, s);
+}
+
+// per-row shifts and the bit width of each component range, from the scan
+// arrays (device side of the planner): shift[r][o] = -min L (0 when empty),
+// beta[r] = max over o of (max E - min L) + 1 (atomic; zeroed by caller)
+struct OzRanges {
+  int n;
+  int c0[4], c1[4];
+};
+
+__global__ void oz_shifts_kernel(OzRanges rg, int comps, int odim, const int* __restrict__ EL,
+                                 int* __restrict__ shift, int* __restrict__ beta) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r = blockIdx.y;
+  int d = 0;
+  if (o < odim) {
+    int e = kEmptyE, lo = kEmptyL;
+    for (int c = rg.c0[r]; c < rg.c1[r]; ++c) {
+      e = max(e, EL[c * odim + o]);
+      lo = min(lo, EL[(comps + c) * odim + o]);
+    }
+    shift[static_cast<int64_t>(r) * odim + o] = lo == kEmptyL ? 0 : -lo;
+    d = e == kEmptyE ? 0 : e - lo + 1;
+  }
+#pragma unroll
+  for (int k = 16; k > 0; k >>= 1) d = max(d, __shfl_xor_sync(0xffffffffu, d, k));
+  if ((threadIdx.x & 31) == 0 && d > 0) atomicMax(beta + r, d);
+}
+
+cudaError_t oz_shifts_launch(int comps, int nranges, const int* ranges, int odim, const int* EL,
+                             int* shift, int* beta, cudaStream_t s) {
+  if (odim <= 0) return cudaSuccess;
+  if (nranges < 1 || nranges > 4) return cudaErrorInvalidValue;
+  OzRanges rg{};
+  rg.n = nranges;
+  for (int r = 0; r < nranges; ++r) {
+    rg.c0[r] = ranges[2 * r];
+    rg.c1[r] = ranges[2 * r + 1];
+  }
+  dim3 grid((odim + 255) / 256, nranges);
+  oz_shifts_kernel<<<grid, 256, 0, s>>>(rg, comps, odim, EL, shift, beta);
+  return cudaGetLastError();
 }
 
 }  // namespace mpmm

@@ -7,25 +7,27 @@ inside the north_star bound 4 l u (|A||B|)_ij.
 
 How (csrc/ozaki.cu, int8gemm.cpp; the CRT variant of the Ozaki scheme):
 
-1. scan: per row of A (column of B) the largest exponent E and the lowest
-   set bit L of any component; the row shift s = -L makes every entry
-   times 2^s an integer of < beta = max(E - L) + 1 bits;
-2. residues: those integers modulo N pairwise-coprime prime powers
-   p_t <= 256, centred into int8, with N the smallest count whose product
-   P exceeds 2 l 2^(beta_A + beta_B);
+1. scan (one pass per operand, one host sync): per row of A (column of
+   B) and component the largest exponent E and the lowest set bit L; for a
+   component range the row shift s = -min L makes every entry times 2^s an
+   integer of < beta = max(E - L) + 1 (+1 per doubling of the range) bits;
+2. residues: each scaled entry as a two's-complement word string, reduced
+   modulo N pairwise-coprime prime powers p_t <= 256 by byte dot products
+   (dp4a) with 2^(8j) mod p_t, centred into int8; N is the smallest count
+   whose product P exceeds 2 l 2^(beta_A + beta_B);
 3. one batched int8 GEMM per modulus (exact int32 accumulation);
 4. CRT: per output, X = sum_t r_t W_t mod P rebuilt in 32-bit limbs,
    scaled by 2^-(s_i + t_j), summed over jobs, rounded to DD/QD.
 
 When beta_A + beta_B does not fit the 54 available moduli (363 bits) the
-operands are split into component ranges (hi/lo) and the exact jobs
-hi*hi + hi*lo + lo*hi + lo*lo are summed in the combine step, so the
-result stays the exact product, correctly rounded.  ``NotRepresentable``
+operands are split into component ranges (e.g. QD hi/lo of A against all
+of B, or hi/lo of both) and the exact jobs are summed in the combine step,
+so the result stays the exact product, correctly rounded; the planner
+takes the feasible split with the least int8/CRT work.  ``NotRepresentable``
 is raised when even single components do not fit (e.g. a row spanning
 2^300 of dynamic range).
 """
 
-import math
 from functools import lru_cache
 
 import numpy as np
@@ -37,7 +39,7 @@ MODULI = (256, 251, 243, 241, 239, 233, 229, 227, 223, 211, 199, 197, 193, 191,
           181, 179, 173, 169, 167, 163, 157, 151, 149, 139, 137, 131, 127, 125,
           121, 113, 109, 107, 103, 101, 97, 89, 83, 79, 73, 71, 67, 61,
           59, 53, 49, 47, 43, 41, 37, 31, 29, 23, 19, 17)
-EMPTY_E = -100000
+EMPTY_E, EMPTY_L = -100000, 100000
 WORKSPACE_BYTES = 64 << 20
 
 
@@ -45,6 +47,7 @@ class NotRepresentable(MpmmError, ValueError):
     """The operands' dynamic range is too wide for the int8 CRT scheme."""
 
 
+@lru_cache(maxsize=None)
 def moduli_count(bits):
     """Smallest N with prod(MODULI[:N]) > 2^bits, or None."""
     P = 1
@@ -55,6 +58,7 @@ def moduli_count(bits):
     return None
 
 
+@lru_cache(maxsize=None)
 def crt_limbs(N):
     P = 1
     for p in MODULI[:N]:
@@ -82,14 +86,6 @@ def crt_table(N, K=None):
     return np.array(words, dtype=np.uint32), K
 
 
-@lru_cache(maxsize=None)
-def pow2_table(N, xmax):
-    t = np.zeros((N, xmax), dtype=np.uint8)
-    for i, p in enumerate(MODULI[:N]):
-        t[i] = [pow(2, x, p) for x in range(xmax)]
-    return t
-
-
 _dev_cache = {}
 
 
@@ -101,124 +97,176 @@ def _device_const(key, host_array, device):
     return _dev_cache[k]
 
 
-def _scan(X, rows, cols, comps, c0, c1, by_cols, stream):
-    import torch
-    n = cols if by_cols else rows
-    E = torch.empty(n, dtype=torch.int32, device=X.device)
-    L = torch.empty(n, dtype=torch.int32, device=X.device)
-    _cuda.oz_scan_dev(1 if by_cols else 0, comps, c0, c1, rows, cols, X.data_ptr(),
-                      X.shape[1], E.data_ptr(), L.data_ptr(), stream)
-    E, L = E.cpu().numpy(), L.cpu().numpy()
-    full = E != EMPTY_E
-    beta = int((E[full] - L[full]).max()) + 1 if full.any() else 1
-    shift = np.where(full, -L, 0).astype(np.int32)
-    return beta, shift
+class Plan:
+    """A chosen component split: ranges of A and B with their bit widths
+    (beta) and residue word counts, and the jobs (pairs of ranges) with
+    their moduli counts N and one CRT limb count K."""
+
+    def __init__(self, jobs, ranges_a, ranges_b):
+        self.ranges_a = [tuple(int(c) for c in r) for r in ranges_a]
+        self.ranges_b = [tuple(int(c) for c in r) for r in ranges_b]
+        self.jobs = [(int(j[0]), int(j[1]), int(j[2])) for j in jobs]   # (ia, ib, N)
+        self.K = int(jobs[0][3])
+        na, nb = len(self.ranges_a), len(self.ranges_b)
+        self.words_a, self.words_b = [0] * na, [0] * nb
+        self.beta_a, self.beta_b = [0] * na, [0] * nb
+        self.need_a, self.need_b = [0] * na, [0] * nb
+        for j in jobs:
+            ia, ib, N = int(j[0]), int(j[1]), int(j[2])
+            self.words_a[ia], self.words_b[ib] = int(j[4]), int(j[5])
+            self.beta_a[ia], self.beta_b[ib] = int(j[6]), int(j[7])
+            self.need_a[ia] = max(self.need_a[ia], N)
+            self.need_b[ib] = max(self.need_b[ib], N)
+
+    def fits(self, actual_a, actual_b):
+        """The plan is exact for operands whose per-range widths are these."""
+        return all(x <= y for x, y in zip(actual_a, self.beta_a)) and \
+            all(x <= y for x, y in zip(actual_b, self.beta_b))
+
+    def loose(self, actual_a, actual_b, slack=8):
+        """Much wider than needed (a fresh plan would use fewer moduli)."""
+        return any(x + slack < y for x, y in zip(actual_a, self.beta_a)) or \
+            any(x + slack < y for x, y in zip(actual_b, self.beta_b))
 
 
-def _split_plans(comps):
-    """Component-range job lists to try, widest ranges first.  Every list
-    covers all pairs, so the sum of the jobs is the exact product."""
-    ranges = {2: [[(0, 2)], [(0, 1), (1, 2)]],
-              4: [[(0, 4)], [(0, 2), (2, 4)], [(0, 1), (1, 2), (2, 3), (3, 4)]]}[comps]
-    return [[(ra, rb) for ra in rs for rb in rs] for rs in ranges]
+_PLANS = {}   # (device, stream, comps, m, l, n) -> Plan of the last product
 
 
-def plan(A, B, stream=None):
-    """The job list ``[(ra, rb, N, beta_a, beta_b, shift_a, shift_b)]``."""
+def _widths(raw, ranges):
+    """Device betas (max(E - L) + 1 per range, 0 when empty) -> planner
+    widths (+1 bit per doubling of the range's component count)."""
+    return [max(int(b), 1) + (c1 - c0 - 1).bit_length() for b, (c0, c1) in zip(raw, ranges)]
+
+
+def _scan(A, B, stream):
+    """One scan per operand into a single int32 buffer: EL_A | EL_B | aux,
+    aux = [status, beta_a[4], beta_b[4]] (zeroed)."""
     import torch
     m, l, comps = A.shape
     n = B.shape[1]
+    ea, eb = 2 * comps * m, 2 * comps * n
+    buf = torch.empty(ea + eb + 9, dtype=torch.int32, device=A.device)
+    aux = buf[ea + eb:]
+    aux.zero_()
+    _cuda.oz_scan_dev(0, comps, m, l, A.data_ptr(), A.shape[1], buf.data_ptr(), aux.data_ptr(),
+                      stream)
+    _cuda.oz_scan_dev(1, comps, l, n, B.data_ptr(), B.shape[1], buf[ea:].data_ptr(),
+                      aux.data_ptr(), stream)
+    return buf, aux, ea, eb
+
+
+def _make_plan(buf, ea, eb, comps, m, l, n):
+    host = buf.cpu().numpy()                       # the host sync of a planned call
+    if host[ea + eb] & 1:
+        raise RangeError("non-finite operand: the exact tensor mode needs finite inputs")
+    out = _cuda.oz_plan(comps, m, n, l, host[:ea], host[ea:ea + eb])
+    if out is None:
+        raise NotRepresentable("operand dynamic range too wide for the int8 CRT scheme")
+    jobs, ra, _, rb, _ = out
+    return Plan(jobs, ra, rb)
+
+
+def plan(A, B, stream=None):
+    """Scan both operands and plan the product (one host sync); returns a
+    :class:`Plan`."""
+    import torch
     stream = stream if stream is not None else torch.cuda.current_stream().cuda_stream
-    log_l = max(1, math.ceil(math.log2(max(l, 2))))
-    cache = {}
-    for jobs in _split_plans(comps):
-        out = []
-        for ra, rb in jobs:
-            if ("a", ra) not in cache:
-                cache[("a", ra)] = _scan(A, m, l, comps, ra[0], ra[1], False, stream)
-            if ("b", rb) not in cache:
-                cache[("b", rb)] = _scan(B, l, n, comps, rb[0], rb[1], True, stream)
-            ba, sa = cache[("a", ra)]
-            bb, sb = cache[("b", rb)]
-            N = moduli_count(ba + bb + log_l + 1)
-            if N is None:
-                break
-            out.append((ra, rb, N, ba, bb, sa, sb))
-        else:
-            return out
-    raise NotRepresentable("operand dynamic range too wide for the int8 CRT scheme")
+    m, l, comps = A.shape
+    buf, _, ea, eb = _scan(A, B, stream)
+    return _make_plan(buf, ea, eb, comps, m, l, B.shape[1])
+
+
+def _execute(pl, A, B, buf, aux, ea, stream):
+    """Shifts, residues, int8 GEMMs and the CRT combine for plan ``pl``;
+    everything is enqueued on ``stream`` (no host sync)."""
+    import torch
+    m, l, comps = A.shape
+    n = B.shape[1]
+    dev = A.device
+    pad = lambda x: -(-x // 16) * 16  # noqa: E731  (cuBLASLt IMMA alignment)
+    mp_, np_, lp = pad(m), pad(n), pad(l)
+    sh_a = torch.empty((len(pl.ranges_a), m), dtype=torch.int32, device=dev)
+    sh_b = torch.empty((len(pl.ranges_b), n), dtype=torch.int32, device=dev)
+    _cuda.oz_shifts_dev(comps, pl.ranges_a, m, buf.data_ptr(), sh_a.data_ptr(),
+                        aux[1:].data_ptr(), stream)
+    _cuda.oz_shifts_dev(comps, pl.ranges_b, n, buf[ea:].data_ptr(), sh_b.data_ptr(),
+                        aux[5:].data_ptr(), stream)
+    alloc = torch.zeros if (mp_, np_, lp) != (m, n, l) else torch.empty
+    RA, RB = [], []
+    for r, (c0, c1) in enumerate(pl.ranges_a):
+        R = alloc((pl.need_a[r], mp_, lp), dtype=torch.int8, device=dev)
+        _cuda.oz_residues_dev(0, comps, c0, c1, m, l, A.data_ptr(), A.shape[1], sh_a[r].data_ptr(),
+                              pl.need_a[r], pl.words_a[r], R.data_ptr(), lp, mp_ * lp, stream)
+        RA.append(R)
+    for r, (c0, c1) in enumerate(pl.ranges_b):
+        R = alloc((pl.need_b[r], np_, lp), dtype=torch.int8, device=dev)
+        _cuda.oz_residues_dev(1, comps, c0, c1, l, n, B.data_ptr(), B.shape[1], sh_b[r].data_ptr(),
+                              pl.need_b[r], pl.words_b[r], R.data_ptr(), lp, np_ * lp, stream)
+        RB.append(R)
+    ws = torch.empty(WORKSPACE_BYTES, dtype=torch.uint8, device=dev)
+    rec = np.zeros(len(pl.jobs), dtype=_REC)
+    Gs = []
+    for q, (ia, ib, N) in enumerate(pl.jobs):
+        G = torch.empty((N, mp_, np_), dtype=torch.int32, device=dev)
+        _cuda.int8_gemm_batched_dev(mp_, np_, lp, N, RA[ia].data_ptr(), RB[ib].data_ptr(),
+                                    G.data_ptr(), ws.data_ptr(), WORKSPACE_BYTES, stream)
+        table = _device_const(("crt", N, pl.K), crt_table(N, pl.K)[0], dev)
+        rec[q] = (G.data_ptr(), sh_a[ia].data_ptr(), sh_b[ib].data_ptr(), table.data_ptr(), N,
+                  pl.K, np_, mp_ * np_)
+        Gs.append(G)
+    C = torch.empty((m, n, comps), dtype=torch.float64, device=dev)
+    _cuda.oz_combine_dev(comps, rec.ctypes.data, len(pl.jobs), m, n, C.data_ptr(),
+                         aux.data_ptr(), stream)
+    # buffers return to the caching allocator in stream order
+    return C
+
+
+_REC = np.dtype([("G", "<u8"), ("sr", "<u8"), ("sc", "<u8"), ("tb", "<u8"), ("N", "<i4"),
+                 ("K", "<i4"), ("gp", "<i8"), ("gl", "<i8")])
 
 
 def matmul_exact_tensors(A, B):
     """C = A*B for (m,l,comps) / (l,n,comps) float64 CUDA tensors, exact
-    product rounded once to comps doubles; returns the (m,n,comps) tensor."""
+    product rounded once to comps doubles; returns the (m,n,comps) tensor.
+
+    A product of the same shape on the same stream as the previous one
+    reuses its plan speculatively: the scans, the device-side shifts and
+    width check, the residues, GEMMs and combine are all enqueued at once
+    and the ONE host sync reads the status and the actual widths; if the
+    data needs a wider plan than the cached one the product is planned and
+    recomputed (never returned wrong)."""
     import torch
     m, l, comps = A.shape
     n = B.shape[1]
-    if not (torch.isfinite(A).all() and torch.isfinite(B).all()):
-        raise RangeError("non-finite operand: the exact tensor mode needs finite inputs")
     dev = A.device
     stream = torch.cuda.current_stream(dev).cuda_stream
-    jobs = plan(A, B, stream)
-    ws = torch.empty(WORKSPACE_BYTES, dtype=torch.uint8, device=dev)
-    pad = lambda x: -(-x // 16) * 16  # noqa: E731  (cuBLASLt IMMA alignment)
-    mp_, np_, lp = pad(m), pad(n), pad(l)
-    K = max(crt_limbs(N) for _, _, N, _, _, _, _ in jobs)
-    # residues once per operand component range, with the most moduli any
-    # job using that range needs (a job reads the leading planes)
-    need = {}
-    for ra, rb, N, ba, bb, sa, sb in jobs:
-        need[("a", ra)] = max(need.get(("a", ra), 0), N)
-        need[("b", rb)] = max(need.get(("b", rb), 0), N)
-    xmax = max(max(j[3], j[4]) for j in jobs) + 8
-    res = {}
-    alloc = torch.zeros if (mp_, np_, lp) != (m, n, l) else torch.empty
-    for ra, rb, N, ba, bb, sa, sb in jobs:
-        for side, rng, sh in (("a", ra, sa), ("b", rb, sb)):
-            if (side, rng) in res:
-                continue
-            Nr = need[(side, rng)]
-            pow2 = _device_const(("pow2", Nr, xmax), pow2_table(Nr, xmax), dev)
-            dsh = torch.from_numpy(sh).to(dev)
-            if side == "a":
-                R = alloc((Nr, mp_, lp), dtype=torch.int8, device=dev)
-                _cuda.oz_residues_dev(0, comps, rng[0], rng[1], m, l, A.data_ptr(), l,
-                                      dsh.data_ptr(), Nr, pow2.data_ptr(), xmax, R.data_ptr(),
-                                      lp, mp_ * lp, stream)
-            else:
-                R = alloc((Nr, np_, lp), dtype=torch.int8, device=dev)
-                _cuda.oz_residues_dev(1, comps, rng[0], rng[1], l, n, B.data_ptr(), n,
-                                      dsh.data_ptr(), Nr, pow2.data_ptr(), xmax, R.data_ptr(),
-                                      lp, np_ * lp, stream)
-            res[(side, rng)] = (R, dsh)
-    keep, recs = [], []
-    for ra, rb, N, ba, bb, sa, sb in jobs:
-        RA, dsa = res[("a", ra)]
-        RB, dsb = res[("b", rb)]
-        table = _device_const(("crt", N, K), crt_table(N, K)[0], dev)
-        G = torch.empty((N, mp_, np_), dtype=torch.int32, device=dev)
-        _cuda.int8_gemm_batched_dev(mp_, np_, lp, N, RA.data_ptr(), RB.data_ptr(), G.data_ptr(),
-                                    ws.data_ptr(), WORKSPACE_BYTES, stream)
-        keep += [G, dsa, dsb]
-        recs.append((G.data_ptr(), dsa.data_ptr(), dsb.data_ptr(), table.data_ptr(), N, K,
-                     np_, mp_ * np_))
-    del res
-    rec = np.zeros(len(recs), dtype=np.dtype([("G", "<u8"), ("sr", "<u8"), ("sc", "<u8"),
-                                              ("tb", "<u8"), ("N", "<i4"), ("K", "<i4"),
-                                              ("gp", "<i8"), ("gl", "<i8")]))
-    for q, r in enumerate(recs):
-        rec[q] = r
-    drec = torch.from_numpy(rec.view(np.uint8).copy()).to(dev)
-    C = torch.empty((m, n, comps), dtype=torch.float64, device=dev)
-    status = torch.zeros(1, dtype=torch.int32, device=dev)
-    _cuda.oz_combine_dev(comps, drec.data_ptr(), len(recs), m, n, C.data_ptr(),
-                         status.data_ptr(), rec.ctypes.data, stream)
-    st = int(status.item())
-    if st & 2:
+    key = (dev.index, stream, comps, m, l, n)
+    buf, aux, ea, eb = _scan(A, B, stream)
+    pl = _PLANS.get(key)
+    speculative = pl is not None
+    if pl is None:
+        pl = _make_plan(buf, ea, eb, comps, m, l, n)
+    C = _execute(pl, A, B, buf, aux, ea, stream)
+    h = aux.cpu().numpy()
+    if h[0] & 1:
+        _PLANS.pop(key, None)
+        raise RangeError("non-finite operand or product overflowed the working precision")
+    act_a, act_b = _widths(h[1:1 + len(pl.ranges_a)], pl.ranges_a), \
+        _widths(h[5:5 + len(pl.ranges_b)], pl.ranges_b)
+    if speculative and not pl.fits(act_a, act_b):
+        pl = _make_plan(buf, ea, eb, comps, m, l, n)
+        aux.zero_()
+        C = _execute(pl, A, B, buf, aux, ea, stream)
+        h = aux.cpu().numpy()
+        if h[0] & 1:
+            raise RangeError("matrix product overflowed the working precision")
+    if h[0] & 2:
+        _PLANS.pop(key, None)
         raise NotRepresentable("CRT combine window exceeded")
-    if st & 1:
-        raise RangeError("matrix product overflowed the working precision")
-    del keep
+    if pl.loose(act_a, act_b):
+        _PLANS.pop(key, None)        # next product of this shape replans
+    else:
+        _PLANS[key] = pl
     return C
 
 

@@ -47,11 +47,32 @@ def test_exact_and_correctly_rounded(gpu, tok, shape, wide):
 def test_plan_splits_wide_and_qd(gpu):
     import torch
     a, b = inputs.gemm_inputs("dd", 64, 64, 64, seed=1)
-    jobs = plan(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
-    assert len(jobs) == 1 and jobs[0][2] <= 54
+    pl = plan(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    assert len(pl.jobs) == 1 and pl.jobs[0][2] <= 54
     a, b = inputs.gemm_inputs("qd", 32, 32, 32, seed=1)
-    jobs = plan(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
-    assert len(jobs) == 4          # hi/lo x hi/lo
+    pl = plan(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    assert len(pl.jobs) in (2, 4)     # hi/lo of one operand, or of both
+    cover = sorted((x, y) for ia, ib, _ in pl.jobs for x in range(*pl.ranges_a[ia])
+                   for y in range(*pl.ranges_b[ib]))
+    assert cover == [(x, y) for x in range(4) for y in range(4)]
+
+
+def test_speculative_plan_reuse_and_replan(gpu):
+    """Same shape, wider data: the cached plan no longer fits, the product
+    is replanned and still exact; narrower data afterwards drops it."""
+    import torch
+    from paper_1710_01839_b200 import tensor
+    a, b = inputs.gemm_inputs("dd", 12, 40, 10, seed=2)
+    wa, wb = inputs.gemm_inputs("dd", 12, 40, 10, seed=3, wide=True)
+    key = None
+    for x, y in ((a, b), (a, b), (wa, wb), (wa, wb), (a, b)):
+        c = tensor.matmul_exact_tensors(torch.from_numpy(x).cuda(),
+                                        torch.from_numpy(y).cuda()).cpu().numpy()
+        for i, j in ((0, 0), (11, 9), (5, 3)):
+            assert list(c[i, j]) == _rn_expansion(_exact_entry(x, y, i, j), 2), (i, j)
+        keys = [k for k in tensor._PLANS if k[2:] == (2, 12, 40, 10)]
+        key = keys[0] if keys else key
+    assert key is not None
 
 
 def test_integers_and_zero_rows(gpu):

@@ -304,5 +304,31 @@ def test_tensor_moduli_and_crt_tables():
         assert (X if X <= P // 2 else X - P) == x
     padded, K2 = tensor.crt_table(N, K + 2)
     assert K2 == K + 2 and int(padded[K2 * 1 + K]) == 0
-    pt = tensor.pow2_table(3, 40)
-    assert all(int(pt[i, x]) == pow(2, x, mods[i]) for i in range(3) for x in range(40))
+
+
+
+def test_native_tensor_planner():
+    """mpmm_oz_plan (host-only C++): feasibility, cost choice and shifts."""
+    from paper_1710_01839_b200 import _cuda, tensor
+    E_, L_ = tensor.EMPTY_E, tensor.EMPTY_L
+    # DD, 3 rows: hi spans [2^-52, 2^0), lo down to 2^-105; row 2 empty
+    ea = np.array([0, -3, E_, -53, -60, E_, -52, -10, L_, -105, -70, L_], dtype=np.int32)
+    eb = ea.copy()
+    jobs, ra, sa, rb, sb = _cuda.oz_plan(2, 3, 3, 64, ea, eb)
+    assert len(jobs) == 1 and tuple(ra[0]) == (0, 2)
+    beta = (0 + 105) + 1 + 1
+    N, K, wa, wb, ba, bb = jobs[0][2:]
+    assert (ba, bb) == (beta, beta) and wa == wb == (beta + 33) // 32
+    assert N == tensor.moduli_count(2 * beta + 6 + 1) and K == tensor.crt_limbs(N)
+    assert list(sa[0]) == [105, 70, 0]
+    # a wide row: the 1-job plan no longer fits 54 moduli -> a split
+    ea2 = ea.copy()
+    ea2[9] = -250
+    jobs, ra, sa, rb, sb = _cuda.oz_plan(2, 3, 3, 64, ea2, eb)
+    assert len(jobs) > 1
+    cover = sorted((x, y) for j in jobs for x in range(*ra[j[0]]) for y in range(*rb[j[1]]))
+    assert cover == [(0, 0), (0, 1), (1, 0), (1, 1)]
+    # hopeless: a single component spanning 2^400
+    ea3 = ea.copy()
+    ea3[6] = -400
+    assert _cuda.oz_plan(2, 3, 3, 64, ea3, eb) is None
