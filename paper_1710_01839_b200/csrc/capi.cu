@@ -4,10 +4,12 @@
 // selected by backend.py:28-56): the eight range kernels keep their
 // argument meaning on host pointers, and device-resident whole-GEMM /
 // elementwise entry points serve the multiply/predict/tune layers.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/mpmm_cuda.h"
 #include "kernels.h"
@@ -207,18 +209,38 @@ int host_rows_gemm(int comps, int algo, int64_t n_min, int64_t rows, int64_t l, 
   int64_t want = l >= 1024 ? 8 : (l >= 256 ? l / 128 : 1);
   if (const char* env = std::getenv("MPMM_HOST_PANELS")) {   // tuning knob
     int64_t v = std::atoll(env);
-    if (v >= 1 && v <= 8) want = v < l ? v : (l > 0 ? l : 1);
+    if (v >= 1 && v <= 32) want = v < l ? v : (l > 0 ? l : 1);
   }
-  const int64_t step = (l + want - 1) / want;
+  // panel bounds: a short first panel (its H2D is the exposed one), the
+  // rest of k in want - 1 equal panels
+  std::vector<int64_t> kb{0};
+  if (l > 0) {
+    const int64_t step = (l + want - 1) / want;
+    const int64_t first = want > 1 ? std::max<int64_t>(std::min<int64_t>(16, l), step / 4) : l;
+    kb.push_back(first);
+    const int64_t rest = l - first, np = want > 1 ? want - 1 : 0;
+    for (int64_t q = 1; q <= np && rest > 0; ++q) {
+      const int64_t b1 = first + (rest * q + np - 1) / np;
+      if (b1 > kb.back()) kb.push_back(b1 < l ? b1 : l);
+    }
+    if (kb.back() != l) kb.push_back(l);
+  }
   int tile = TILE_16, super = 1;
   if (algo != ALGO_SIMPLE) tile_for(n_min, &tile, &super);
-  Event ev[8];
-  int p = 0;
-  const int64_t split = rows >= 256 ? ((rows / 2 + 63) / 64) * 64 : rows;  // D2H overlap
-  Event top;
-  CU(top.make());
-  for (int64_t k0 = 0; k0 < l || (l == 0 && p == 0); k0 += step, ++p) {
-    const int64_t k1 = (k0 + step < l) ? k0 + step : l;
+  // The last panel runs in row slices so each slice's D2H (copy stream)
+  // overlaps the next slice's GEMM; only the last slice's copy is exposed.
+  int64_t nslice = rows >= 1024 ? 8 : (rows >= 512 ? 4 : (rows >= 256 ? 2 : 1));
+  if (const char* env = std::getenv("MPMM_HOST_TAIL")) {     // tuning knob
+    int64_t v = std::atoll(env);
+    if (v >= 1 && v <= 8) nslice = v;
+  }
+  int64_t srows = ((rows + nslice - 1) / nslice + 63) / 64 * 64;
+  const int npan = l > 0 ? static_cast<int>(kb.size()) - 1 : 1;
+  std::vector<Event> ev(static_cast<size_t>(npan));
+  std::vector<Event> sl(static_cast<size_t>(nslice));
+  int64_t copied = 0;   // rows of C already queued for D2H
+  for (int p = 0; p < npan; ++p) {
+    const int64_t k0 = l > 0 ? kb[p] : 0, k1 = l > 0 ? kb[p + 1] : 0;
     if (l > 0) {
       CU(cudaMemcpy2DAsync(dA.p + k0 * comps, l * el, a_rows + k0 * comps, l * el,
                            (k1 - k0) * el, rows, cudaMemcpyHostToDevice, hs->copy));
@@ -230,28 +252,26 @@ int host_rows_gemm(int comps, int algo, int64_t n_min, int64_t rows, int64_t l, 
     CU(cudaStreamWaitEvent(hs->comp, ev[p].e, 0));
     const bool last = (k1 >= l);
     const int acc = (accumulate_c || p > 0) ? 1 : 0;
-    // the finite check only needs the final values: flag the last panel.
-    // The last panel runs in two row halves so the top half's D2H (on the
-    // copy stream) overlaps the bottom half's GEMM.
-    const int64_t parts[2][2] = {{0, last ? split : rows}, {last ? split : rows, rows}};
-    for (int h = 0; h < 2; ++h) {
-      const int64_t q0 = parts[h][0], q1 = parts[h][1];
-      if (q1 <= q0) continue;
+    // the finite check only needs the final values: flag the last panel
+    const int64_t sstep = last ? srows : rows;
+    for (int64_t q0 = 0, si = 0; q0 < rows; q0 += sstep, ++si) {
+      const int64_t q1 = q0 + sstep < rows ? q0 + sstep : rows;
       GemmArgs g{algo, tile, (int)(q1 - q0), (int)n, (int)(k1 - k0),
                  dA.p + (q0 * l + k0) * comps, l, dB.p + k0 * n * comps, n,
                  dC.p + q0 * n * comps, n, acc, last ? dflag : nullptr, hs->comp};
       CU(gemm(comps, g));
-      if (last && h == 0 && split < rows) {
-        CU(cudaEventRecord(top.e, hs->comp));
-        CU(cudaStreamWaitEvent(hs->copy, top.e, 0));
-        CU(cudaMemcpyAsync(c_rows, dC.p, split * n * el, cudaMemcpyDeviceToHost, hs->copy));
+      if (last && q1 < rows) {   // this slice is final: copy it out under the next one
+        CU(sl[si].make());
+        CU(cudaEventRecord(sl[si].e, hs->comp));
+        CU(cudaStreamWaitEvent(hs->copy, sl[si].e, 0));
+        CU(cudaMemcpyAsync(c_rows + q0 * n * comps, dC.p + q0 * n * comps,
+                           (q1 - q0) * n * el, cudaMemcpyDeviceToHost, hs->copy));
+        copied = q1;
       }
     }
-    if (l == 0) break;
   }
-  const int64_t rest0 = (split < rows && l > 0) ? split : 0;
-  CU(cudaMemcpyAsync(c_rows + rest0 * n * comps, dC.p + rest0 * n * comps,
-                     (rows - rest0) * n * el, cudaMemcpyDeviceToHost, hs->comp));
+  CU(cudaMemcpyAsync(c_rows + copied * n * comps, dC.p + copied * n * comps,
+                     (rows - copied) * n * el, cudaMemcpyDeviceToHost, hs->comp));
   CU(cudaStreamSynchronize(hs->copy));
   if (dflag) {
     CU(cudaMemcpyAsync(nonfinite_host, dflag, sizeof(int), cudaMemcpyDeviceToHost, hs->comp));
