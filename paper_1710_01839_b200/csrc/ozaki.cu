@@ -500,14 +500,30 @@ __constant__ unsigned kGBias[54] = {
     MPMM_GB(37),  MPMM_GB(31),  MPMM_GB(29),  MPMM_GB(23),  MPMM_GB(19),  MPMM_GB(17)};
 #undef MPMM_GB
 
+// CRT table row layout in shared memory (32-bit words): the low KD limbs
+// of W_t as doubles (padded to an even count), then the other K - KD limbs
+// as uint32 (padded to 4): every row is a whole number of 16-byte vectors.
+// All limbs on the FP64 pipe measured best (DD 1024^3 combine: 101 us; 111
+// with half the limbs as integer multiply-adds, 114 with all of them).
+__host__ __device__ constexpr int kd_limbs(int K) { return K; }
+__host__ __device__ constexpr int kd_even(int K) { return (kd_limbs(K) + 1) / 2 * 2; }
+__host__ __device__ constexpr int ki_pad(int K) { return (K - kd_limbs(K) + 3) / 4 * 4; }
+__host__ __device__ constexpr int row_words(int K) { return 2 * kd_even(K) + ki_pad(K); }
+__host__ __device__ constexpr int pwords(int K) { return (K + 3) / 4 * 4; }
+
 // CRT accumulation of one output: acc[q] = sum_t r_t W_t[q] with
-// r_t = G_t mod p_t, in K+1 64-bit limb sums.  W: the N weights, row
-// stride WS >= K limbs (16-byte aligned rows: vector loads), in shared
-// memory.  The G planes are read 8 at a time (eight loads in flight).
-template <int K, int WS>
+// r_t = G_t mod p_t, in K+1 64-bit limb sums.  The low KD limbs run on
+// the FP64 pipe -- r_t W_t[q] < 2^40 and sums over <= 54 moduli < 2^46
+// are exact in binary64 -- and any others as 32x32->64-bit integer
+// multiply-adds.  The G planes are read 8 at
+// a time (eight loads in flight).
+template <int K>
 __device__ __forceinline__ void crt_accumulate(const int32_t* G, int64_t gplane, int N,
                                                const uint32_t* W, uint64_t (&acc)[K + 1]) {
-  constexpr int CH = 8;
+  constexpr int CH = 8, KD = kd_limbs(K), KE = kd_even(K), RW = row_words(K);
+  double a[KD];
+#pragma unroll
+  for (int q = 0; q < KD; ++q) a[q] = 0.0;
 #pragma unroll
   for (int q = 0; q <= K; ++q) acc[q] = 0;
   for (int t0 = 0; t0 < N; t0 += CH) {
@@ -524,17 +540,28 @@ __device__ __forceinline__ void crt_accumulate(const int32_t* G, int64_t gplane,
       if (t >= N) break;
       const unsigned p = static_cast<unsigned>(kModsDev[t]);
       const unsigned r = barrett(static_cast<unsigned>(g[u]) + kGBias[t], kModMu[t], p);
-      const uint4* wv = reinterpret_cast<const uint4*>(W + t * WS);
+      const double rd = static_cast<double>(r);
+      const uint32_t* row = W + t * RW;
+      const double2* wd = reinterpret_cast<const double2*>(row);
 #pragma unroll
-      for (int q4 = 0; q4 < WS / 4; ++q4) {
-        const uint4 v = wv[q4];
+      for (int q2 = 0; q2 < KE / 2; ++q2) {
+        const double2 v = wd[q2];
+        if (2 * q2 < KD) a[2 * q2] = __fma_rn(rd, v.x, a[2 * q2]);
+        if (2 * q2 + 1 < KD) a[2 * q2 + 1] = __fma_rn(rd, v.y, a[2 * q2 + 1]);
+      }
+      const uint4* wi = reinterpret_cast<const uint4*>(row + 2 * KE);
+#pragma unroll
+      for (int q4 = 0; q4 < ki_pad(K) / 4; ++q4) {
+        const uint4 v = wi[q4];
         const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-          if (4 * q4 + e < K) acc[4 * q4 + e] += static_cast<uint64_t>(r) * w4[e];
+          if (KD + 4 * q4 + e < K) acc[KD + 4 * q4 + e] += static_cast<uint64_t>(r) * w4[e];
       }
     }
   }
+#pragma unroll
+  for (int q = 0; q < KD; ++q) acc[q] = static_cast<uint64_t>(a[q]);
 }
 
 // From the accumulated sums: the centred integer X = (sum mod P) as sign +
@@ -616,17 +643,31 @@ __device__ __forceinline__ bool crt_finish(const uint64_t (&acc)[K + 1], const u
   return upper;
 }
 
-__host__ __device__ constexpr int wstride(int K) { return (K + 3) / 4 * 4; }
+// Shared-memory CRT table of one job: P (K uint32 limbs, padded to a
+// 16-byte multiple) then the N weight rows (layout above).
+template <int K>
+struct StagedTable {
+  static constexpr int WORDS = pwords(K) + row_words(K) * kNumMods;   // uint32 words
+};
 
-// Stage a job's CRT table in shared memory: P (K limbs, stride WS) then the
-// N weights, each row padded to WS limbs (16-byte aligned).
 template <int K>
 __device__ __forceinline__ void stage_table(const uint32_t* __restrict__ table, int N,
                                             uint32_t* sW) {
-  constexpr int WS = wstride(K);
-  for (int q = threadIdx.x; q < (N + 1) * WS; q += blockDim.x) {
-    const int row = q / WS, col = q % WS;
-    sW[q] = col < K ? table[row * K + col] : 0u;
+  constexpr int PW = pwords(K), RW = row_words(K), KD = kd_limbs(K), KE = kd_even(K);
+  for (int q = threadIdx.x; q < PW; q += blockDim.x) sW[q] = q < K ? table[q] : 0u;
+  for (int q = threadIdx.x; q < N * RW; q += blockDim.x) {
+    const int row = q / RW, col = q % RW;
+    uint32_t* dst = sW + PW + row * RW;
+    const uint32_t* src = table + (row + 1) * K;
+    if (col < 2 * KE) {            // double limbs, written as their two halves
+      const int d = col / 2;
+      const double v = d < KD ? static_cast<double>(src[d]) : 0.0;
+      const unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(v));
+      dst[col] = static_cast<uint32_t>(col % 2 ? bits >> 32 : bits);
+    } else {
+      const int li = KD + (col - 2 * KE);
+      dst[col] = li < K ? src[li] : 0u;
+    }
   }
 }
 
@@ -634,9 +675,8 @@ __device__ __forceinline__ void stage_table(const uint32_t* __restrict__ table, 
 template <int K>
 __device__ __forceinline__ bool crt_reconstruct(const int32_t* Gij, int64_t gplane, int N,
                                                 const uint32_t* sW, int64_t (&mag)[K]) {
-  constexpr int WS = wstride(K);
   uint64_t acc[K + 1];
-  crt_accumulate<K, WS>(Gij, gplane, N, sW + WS, acc);
+  crt_accumulate<K>(Gij, gplane, N, sW + pwords(K), acc);
   return crt_finish<K>(acc, sW, mag);
 }
 
@@ -657,11 +697,87 @@ __device__ __forceinline__ void round_out(int64_t (&mag)[K], bool neg, int ebase
   }
 }
 
+// Correctly rounded DD (hi, lo) of sign * mag * 2^ebase from the top 128
+// bits of the magnitude plus a sticky bit: hi = RN(x) from the window; the
+// remainder x - hi = R 2^E + delta (|R| < 2^76, 0 <= delta < 2^E) is
+// rounded again when its integer part keeps >= 55 bits, so the sticky bits
+// below the window cannot reach the rounding position.  Returns false
+// (use the exact limb path) otherwise -- rare: x - hi cancels to within
+// 2^54 ulps of the window's last bit.
+template <int K>
+__device__ __forceinline__ bool round_dd_fast(const int64_t (&mag)[K], bool neg, int ebase,
+                                              double& hi, double& lo) {
+  int top = -1;
+#pragma unroll
+  for (int q = 0; q < K; ++q)
+    if (mag[q] != 0) top = q;
+  if (top < 0) {
+    hi = lo = 0.0;
+    return true;
+  }
+  // limbs top-4 .. top; after normalisation the 128-bit window W holds the
+  // top 128 bits of the magnitude exactly (the fifth limb fills the bits
+  // the shift frees), everything below is the sticky bit
+  uint32_t w[5] = {0, 0, 0, 0, 0};
+  bool sticky = false;
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    const uint32_t v = static_cast<uint32_t>(mag[q]);
+#pragma unroll
+    for (int u = 0; u < 5; ++u)
+      if (q == top - 4 + u) w[u] = v;
+    if (q < top - 4) sticky |= v != 0;
+  }
+  using u128 = unsigned __int128;
+  const int lz = __clz(w[4]);
+  u128 W = (static_cast<u128>(w[4]) << 96) | (static_cast<u128>(w[3]) << 64) |
+           (static_cast<u128>(w[2]) << 32) | w[1];
+  if (lz) {
+    W = (W << lz) | (w[0] >> (32 - lz));
+    sticky |= (w[0] << lz) != 0;
+  } else {
+    sticky |= w[0] != 0;
+  }
+  const int E = 32 * (top - 3) - lz + ebase;          // weight of W's bit 0
+  const uint64_t t = static_cast<uint64_t>(W >> 64), b = static_cast<uint64_t>(W);
+  const double h = __ull2double_rn(t | static_cast<uint64_t>((b != 0) | sticky));
+  // R = W - H with H = h at the window's scale (h is an integer in [2^63, 2^64])
+  bool rneg;
+  u128 Rm;
+  if (h == 18446744073709551616.0) {                 // rounded up to 2^64
+    rneg = true;
+    Rm = (~W) + 1;                                    // 2^128 - W
+  } else {
+    const u128 H = static_cast<u128>(static_cast<uint64_t>(h)) << 64;
+    rneg = H > W;
+    Rm = rneg ? H - W : W - H;
+  }
+  bool st2 = sticky;
+  if (rneg && sticky) Rm -= 1;                        // -(|R| - delta): integer part |R| - 1
+  if (Rm == 0) {
+    if (st2) return false;
+    hi = ldexp(neg ? -h : h, E + 64);
+    lo = 0.0;
+    return true;
+  }
+  const uint64_t rh = static_cast<uint64_t>(Rm >> 64), rl = static_cast<uint64_t>(Rm);
+  const int bl = rh ? 128 - __clzll(static_cast<long long>(rh))
+                    : 64 - __clzll(static_cast<long long>(rl));
+  if (bl < 55) return false;
+  const u128 Mn = Rm << (128 - bl);
+  const uint64_t mt = static_cast<uint64_t>(Mn >> 64), mb = static_cast<uint64_t>(Mn);
+  const double l = __ull2double_rn(mt | static_cast<uint64_t>((mb != 0) | st2));
+  const bool lneg = neg ^ rneg;
+  hi = ldexp(neg ? -h : h, E + 64);
+  lo = ldexp(lneg ? -l : l, E + bl - 64);
+  return true;
+}
+
 // single job: one output per thread, weights from shared memory
 template <int COMPS, int K>
 __global__ void __launch_bounds__(128)
 combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __restrict__ status) {
-  __shared__ __align__(16) uint32_t sW[(kNumMods + 1) * wstride(K)];
+  __shared__ __align__(16) uint32_t sW[StagedTable<K>::WORDS];
   stage_table<K>(jb.table, jb.N, sW);
   __syncthreads();
   const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -671,7 +787,19 @@ combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __re
   const bool neg = crt_reconstruct<K>(jb.G + static_cast<int64_t>(i) * jb.gpitch + j, jb.gplane,
                                       jb.N, sW, mag);
   bool bad = false;
-  round_out<COMPS, K>(mag, neg, -(jb.srow[i] + jb.scol[j]), C + e * COMPS, bad);
+  const int ebase = -(jb.srow[i] + jb.scol[j]);
+  if constexpr (COMPS == 2) {
+    double hi, lo;
+    if (round_dd_fast<K>(mag, neg, ebase, hi, lo)) {
+      C[e * 2] = hi;
+      C[e * 2 + 1] = lo;
+      bad = !isfinite(hi) || !isfinite(lo);
+    } else {
+      round_out<COMPS, K>(mag, neg, ebase, C + e * COMPS, bad);
+    }
+  } else {
+    round_out<COMPS, K>(mag, neg, ebase, C + e * COMPS, bad);
+  }
   if (bad) atomicOr(status, 1);
 }
 
@@ -690,8 +818,8 @@ combine_multi_kernel(const CrtJobs jobs, int njobs, int m, int n,
                      double* __restrict__ C, int* __restrict__ status) {
   extern __shared__ unsigned char smraw[];
   int64_t* win = reinterpret_cast<int64_t*>(smraw);                   // [kMWin][kMTB]
-  uint32_t* tabs = reinterpret_cast<uint32_t*>(win + kMWin * kMTB);   // [njobs][55 * WS]
-  const int tstride = (kNumMods + 1) * wstride(K);
+  uint32_t* tabs = reinterpret_cast<uint32_t*>(win + kMWin * kMTB);   // [njobs][WORDS]
+  const int tstride = StagedTable<K>::WORDS;
   for (int J = 0; J < njobs; ++J) stage_table<K>(jobs.j[J].table, jobs.j[J].N, tabs + J * tstride);
   __syncthreads();
   const int tid = threadIdx.x;
@@ -875,7 +1003,7 @@ template <int COMPS>
 static cudaError_t combine_multi(const CrtJobs& jobs, int njobs, int K, int m, int n, double* C,
                                  int* status, unsigned blocks, cudaStream_t s) {
   const size_t smem = static_cast<size_t>(kMWin) * kMTB * sizeof(int64_t) +
-                      static_cast<size_t>(njobs) * (kNumMods + 1) * ((K + 3) / 4 * 4) *
+                      static_cast<size_t>(njobs) * (pwords(K) + row_words(K) * kNumMods) *
                           sizeof(uint32_t);
   switch (K) {
 #define MPMM_K(KK)                                                                            \

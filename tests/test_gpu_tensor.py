@@ -106,3 +106,21 @@ def test_cfg1_every_entry_and_speed(gpu, wide):
     print(f"tensor mode DD 1024^3 wide={wide}: max ratio {worst:.3e} (mirror {worst_ref:.3e}), "
           f"{t*1e3:.3f} ms, {2*1024**3/t/1e9:.1f} G 2mnl/s")
     assert worst <= worst_ref and worst <= 1e-3
+
+
+@pytest.mark.parametrize("tok,wide", [("dd", False), ("dd", True), ("qd", False)])
+def test_every_entry_correctly_rounded(gpu, tok, wide):
+    """All entries (not a sample) against exact rational arithmetic: the
+    DD fast rounding path (128-bit window + sticky) and the limb paths must
+    both give the nearest expansion."""
+    prec = mp.PrecisionSpec.parse(tok)
+    m, l, n = (16, 24, 12) if tok == "dd" else (6, 8, 5)
+    a, b = inputs.gemm_inputs(tok, m, l, n, seed=11, wide=wide)
+    # cancellation-heavy rows: the remainder after hi can be tiny
+    a[0, :, :] = a[1, :, :]
+    a[0, ::2, :] *= -1
+    c = matmul_exact(M(a, prec), M(b, prec)).data
+    for i in range(m):
+        for j in range(n):
+            want = _rn_expansion(_exact_entry(a, b, i, j), prec.comps)
+            assert list(c[i, j]) == want, (i, j)
