@@ -96,8 +96,10 @@ class WaveModel:
 def wave_model(comps, n_min):
     g = _cuda.gemm_geometry(comps, _cuda.ALGO_BLOCK, n_min)
     tile, _ = _cuda.tile_for_nmin(n_min)
+    # only the DD tile set has a persistent largest-first kernel (the QD
+    # configurations are all plain grids, csrc/gemm_qd.cu)
     return WaveModel(g["tile_m"], g["tile_n"], max(1, g["ctas_per_sm"]), g["sm_count"],
-                     balanced=(tile == TILE_LPT))
+                     balanced=(tile == TILE_LPT and comps == 2))
 
 
 TILE_LPT = 4   # csrc/kernels.h enum Tile

@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Summarise `ncu --page raw --csv` exports into profiles/ncu_summary.json.
 
-usage: tools/ncu_summary.py <prec>=<raw.csv>[:<note>] ...
+usage: tools/ncu_summary.py <key>=<raw.csv>[#<kernel row>][:<note>] ...
 """
 import csv
 import json
@@ -24,14 +24,18 @@ KEYS = {
     "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum": "dfma",
     "sass__inst_executed_local_loads": "local_loads",
     "Kernel Name": "kernel",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
+    "smsp__inst_executed.sum": "warp_instructions",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "alu_pipe_pct",
+    "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed": "fmaheavy_pipe_pct",
 }
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ms": 1e-3, "us": 1e-6,
         "ns": 1e-9, "s": 1.0}
 
 
-def parse(path):
+def parse(path, row=0):
     rows = list(csv.reader(open(path)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units, vals = rows[0], rows[1], rows[2 + row]
     out = {}
     for i, h in enumerate(hdr):
         if h in KEYS:
@@ -54,7 +58,8 @@ def main():
     for arg in sys.argv[1:]:
         prec, _, rest = arg.partition("=")
         path, _, note = rest.partition(":")
-        d = parse(path)
+        path, _, row = path.partition("#")
+        d = parse(path, int(row) if row else 0)
         d["source"] = os.path.basename(path)
         d["note"] = note
         summary[prec] = d
