@@ -82,12 +82,10 @@ struct TileSmem {
 
 // One CTA computes the BM x BN output tile at (m0, n0) of problem `pr`.
 // NT threads: thread (tx, ty) owns rows ty + r*NTY, cols tx + c*NTX.
-// k-tiles [kt0, kt1) of the tile (kt1 < 0: to the end); accumulate: the
-// accumulator starts at C's value (read through L2).
+// accumulate: the accumulator starts at C's value (read through L2).
 template <class Ops, int BM, int BN, int BK, int TM, int TN, int NT>
 __device__ __forceinline__ void gemm_tile(const Prob& pr, int m, int n, int l, int accumulate,
-                                          int m0, int n0, double2* smem, bool& bad,
-                                          int kt0 = 0, int kt1 = -1) {
+                                          int m0, int n0, double2* smem, bool& bad) {
   constexpr int V = Ops::V;
   constexpr int NTX = BN / TN, NTY = BM / TM;
   static_assert(NTX * NTY == NT, "thread tile does not cover the CTA tile");
@@ -118,7 +116,7 @@ __device__ __forceinline__ void gemm_tile(const Prob& pr, int m, int n, int l, i
       }
     }
 
-  const int ktiles = kt1 < 0 ? (l + BK - 1) / BK : kt1;
+  const int ktiles = (l + BK - 1) / BK;
   auto load = [&](int kt, int st) {
     const int k0 = kt * BK;
 #pragma unroll
@@ -141,12 +139,12 @@ __device__ __forceinline__ void gemm_tile(const Prob& pr, int m, int n, int l, i
     }
   };
 
-  if (ktiles > kt0) {
-    load(kt0, 0);
+  if (ktiles > 0) {
+    load(0, 0);
     cp_async_commit();
   }
-  for (int kt = kt0; kt < ktiles; ++kt) {
-    const int st = (kt - kt0) & 1;
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int st = kt & 1;
     if (kt + 1 < ktiles) {
       load(kt + 1, st ^ 1);
       cp_async_commit();
