@@ -225,6 +225,50 @@ _REC = np.dtype([("G", "<u8"), ("sr", "<u8"), ("sc", "<u8"), ("tb", "<u8"), ("N"
                  ("K", "<i4"), ("gp", "<i8"), ("gl", "<i8")])
 
 
+class _Replay:
+    """The whole device side of one product (scans, shifts, residues, int8
+    GEMMs, combine) captured as a CUDA graph for fixed operand addresses:
+    repeated products of the same operands pay one graph launch instead of
+    ~15 host-side launches.  The data are read afresh at every replay, and
+    the widths it reports are checked against the plan as on the eager path."""
+
+    def __init__(self, pl, A, B):
+        import torch
+        self.pl = pl
+        self.ptrs = (A.data_ptr(), B.data_ptr())
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            stream = torch.cuda.current_stream().cuda_stream
+            buf, aux, ea, _ = _scan(A, B, stream)
+            self.C = _execute(pl, A, B, buf, aux, ea, stream)
+        self.aux = aux
+
+    def run(self):
+        self.graph.replay()
+        return self.aux.cpu().numpy()
+
+
+_REPLAYS = {}        # key -> _Replay
+_LAST_PTRS = {}      # key -> operand addresses of the previous product
+GRAPH_MAX_BYTES = 1 << 30     # intermediates a cached graph may keep alive
+
+
+def _graph_bytes(pl, m, l, n):
+    pad = lambda x: -(-x // 16) * 16  # noqa: E731
+    g = sum(N for _, _, N in pl.jobs) * pad(m) * pad(n) * 4
+    r = (sum(pl.need_a) * pad(m) + sum(pl.need_b) * pad(n)) * pad(l)
+    return g + r
+
+
+def _check(h, pl):
+    if h[0] & 1:
+        raise RangeError("non-finite operand or product overflowed the working precision")
+    if h[0] & 2:
+        raise NotRepresentable("CRT combine window exceeded")
+    return (_widths(h[1:1 + len(pl.ranges_a)], pl.ranges_a),
+            _widths(h[5:5 + len(pl.ranges_b)], pl.ranges_b))
+
+
 def matmul_exact_tensors(A, B):
     """C = A*B for (m,l,comps) / (l,n,comps) float64 CUDA tensors, exact
     product rounded once to comps doubles; returns the (m,n,comps) tensor.
@@ -234,13 +278,25 @@ def matmul_exact_tensors(A, B):
     width check, the residues, GEMMs and combine are all enqueued at once
     and the ONE host sync reads the status and the actual widths; if the
     data needs a wider plan than the cached one the product is planned and
-    recomputed (never returned wrong)."""
+    recomputed (never returned wrong).  When the same operands come back
+    (same addresses) the device side replays as one CUDA graph."""
     import torch
     m, l, comps = A.shape
     n = B.shape[1]
     dev = A.device
     stream = torch.cuda.current_stream(dev).cuda_stream
     key = (dev.index, stream, comps, m, l, n)
+    ptrs = (A.data_ptr(), B.data_ptr())
+    rp = _REPLAYS.get(key)
+    if rp is not None and rp.ptrs == ptrs:
+        try:
+            act = _check(rp.run(), rp.pl)
+            if rp.pl.fits(*act) and not rp.pl.loose(*act):
+                return rp.C.clone()
+        except (RangeError, NotRepresentable):
+            pass                      # redo eagerly: same error, or the exact reason
+        _REPLAYS.pop(key, None)
+        _PLANS.pop(key, None)
     buf, aux, ea, eb = _scan(A, B, stream)
     pl = _PLANS.get(key)
     speculative = pl is not None
@@ -248,25 +304,27 @@ def matmul_exact_tensors(A, B):
         pl = _make_plan(buf, ea, eb, comps, m, l, n)
     C = _execute(pl, A, B, buf, aux, ea, stream)
     h = aux.cpu().numpy()
-    if h[0] & 1:
+    try:
+        act_a, act_b = _check(h, pl)
+    except RangeError:
         _PLANS.pop(key, None)
-        raise RangeError("non-finite operand or product overflowed the working precision")
-    act_a, act_b = _widths(h[1:1 + len(pl.ranges_a)], pl.ranges_a), \
-        _widths(h[5:5 + len(pl.ranges_b)], pl.ranges_b)
+        raise
     if speculative and not pl.fits(act_a, act_b):
         pl = _make_plan(buf, ea, eb, comps, m, l, n)
         aux.zero_()
         C = _execute(pl, A, B, buf, aux, ea, stream)
-        h = aux.cpu().numpy()
-        if h[0] & 1:
-            raise RangeError("matrix product overflowed the working precision")
-    if h[0] & 2:
-        _PLANS.pop(key, None)
-        raise NotRepresentable("CRT combine window exceeded")
+        act_a, act_b = _check(aux.cpu().numpy(), pl)
     if pl.loose(act_a, act_b):
         _PLANS.pop(key, None)        # next product of this shape replans
-    else:
-        _PLANS[key] = pl
+        _LAST_PTRS.pop(key, None)
+        return C
+    _PLANS[key] = pl
+    if _LAST_PTRS.get(key) == ptrs and _graph_bytes(pl, m, l, n) <= GRAPH_MAX_BYTES:
+        try:
+            _REPLAYS[key] = _Replay(pl, A, B)
+        except RuntimeError:
+            _REPLAYS.pop(key, None)   # capture not possible here: stay eager
+    _LAST_PTRS[key] = ptrs
     return C
 
 

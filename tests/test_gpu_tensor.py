@@ -124,3 +124,25 @@ def test_every_entry_correctly_rounded(gpu, tok, wide):
         for j in range(n):
             want = _rn_expansion(_exact_entry(a, b, i, j), prec.comps)
             assert list(c[i, j]) == want, (i, j)
+
+
+def test_graph_replay_same_operands_and_in_place_change(gpu):
+    """Same operands three times: the third product replays the captured
+    graph; then the operands change in place (same addresses, wider data):
+    the replay's width check sends it back to the eager path, still exact."""
+    import torch
+    from paper_1710_01839_b200 import tensor
+    a, b = inputs.gemm_inputs("dd", 12, 40, 10, seed=5)
+    wa, wb = inputs.gemm_inputs("dd", 12, 40, 10, seed=6, wide=True)
+    A, B = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    outs = [tensor.matmul_exact_tensors(A, B).cpu().numpy() for _ in range(4)]
+    assert any(k[2:] == (2, 12, 40, 10) for k in tensor._REPLAYS)
+    for c in outs[1:]:
+        assert np.array_equal(c, outs[0])
+    for i, j in ((0, 0), (11, 9)):
+        assert list(outs[-1][i, j]) == _rn_expansion(_exact_entry(a, b, i, j), 2)
+    A.copy_(torch.from_numpy(wa))
+    B.copy_(torch.from_numpy(wb))
+    c = tensor.matmul_exact_tensors(A, B).cpu().numpy()
+    for i, j in ((0, 0), (11, 9), (4, 4)):
+        assert list(c[i, j]) == _rn_expansion(_exact_entry(wa, wb, i, j), 2), (i, j)
