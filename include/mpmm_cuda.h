@@ -37,6 +37,7 @@ extern "C" {
 #define MPMM_ERR_CUDA 2   /* a CUDA runtime call failed                   */
 #define MPMM_ERR_NODEV 3  /* no CUDA device                               */
 #define MPMM_ERR_RANGE 4  /* operands not representable (exact tensor mode) */
+#define MPMM_ERR_NONFINITE 5 /* non-finite operand or result (exact tensor mode) */
 
 #define MPMM_ALGO_SIMPLE 0
 #define MPMM_ALGO_BLOCK 1
@@ -197,6 +198,21 @@ int mpmm_oz_scan_dev(int by_cols, int comps, int64_t rows, int64_t cols, const d
 int mpmm_oz_residues_dev(int by_cols, int comps, int c0, int c1, int64_t rows, int64_t cols,
                          const double *X, int64_t ld, const int *shift, int nmod, int words,
                          int8_t *R, int64_t rpitch, int64_t rplane, void *stream);
+/* The exact tensor mode in one call: C = A*B (device pointers, dense C with
+ * ldc == n) as the exact product rounded once to comps doubles, on the
+ * int8 tensor cores.  Synchronous (returns after the product, whose status
+ * it reads).  The plan is cached per (device, stream, shape) and reused
+ * speculatively with a device-side width check (recomputed when it does
+ * not fit); intermediates up to 1 GiB stay cached, and a call with the same
+ * A/B/C addresses as the previous one replays the whole device side as a
+ * CUDA graph.  MPMM_ERR_NONFINITE for non-finite operands or an
+ * overflowing result, MPMM_ERR_RANGE when the operands' dynamic range does
+ * not fit the 54 moduli. */
+int mpmm_gemm_exact_dev(int comps, int64_t m, int64_t l, int64_t n, const double *A,
+                        int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc,
+                        void *stream);
+/* Free every cached exact-mode plan, workspace and graph. */
+int mpmm_exact_release(void);
 /* Host-only planner of the exact tensor mode: from the scan arrays of A
  * (ela, 2*comps*m ints) and B (elb, 2*comps*n ints) choose the cheapest
  * feasible component split.  Outputs: *na ranges of A in ranges_a[2*na]

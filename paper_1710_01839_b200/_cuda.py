@@ -67,6 +67,8 @@ _SIGNATURES = {
                              _VP, _I64, _I64, _VP],
     "mpmm_oz_plan": [_INT, _I64, _I64, _I64, _VP, _VP, ctypes.POINTER(_INT), _VP,
                      ctypes.POINTER(_INT), _VP, _VP, ctypes.POINTER(_INT), _VP, _VP],
+    "mpmm_gemm_exact_dev": [_INT, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _VP],
+    "mpmm_exact_release": [],
     "mpmm_int8_gemm_batched_dev": [_I64, _I64, _I64, _I64, _VP, _VP, _VP, _VP, _I64, _VP],
     "mpmm_oz_combine_dev": [_INT, _VP, _INT, _I64, _I64, _VP, _VP, _VP],
     "mpmm_oz_shifts_dev": [_INT, _INT, _VP, _I64, _VP, _VP, _VP, _VP],
@@ -383,6 +385,21 @@ def oz_residues_dev(by_cols, comps, c0, c1, rows, cols, X, ld, shift, nmod, word
     sync_device()
     check(load().mpmm_oz_residues_dev(by_cols, comps, c0, c1, rows, cols, X, ld, shift, nmod,
                                       words, R, rpitch, rplane, stream))
+
+
+def gemm_exact_dev(comps, m, l, n, A, lda, B, ldb, C, ldc, stream=None):
+    """Returns 0, or MPMM_ERR_RANGE (4) / MPMM_ERR_NONFINITE (5) with the
+    message in last_error(); raises on other failures."""
+    sync_device()
+    rc = load().mpmm_gemm_exact_dev(comps, m, l, n, A, lda, B, ldb, C, ldc, stream)
+    if rc in (4, 5):
+        return rc
+    check(rc)
+    return 0
+
+
+def last_error():
+    return load().mpmm_last_error().decode(errors="replace")
 
 
 def oz_plan(comps, m, n, l, ela, elb):

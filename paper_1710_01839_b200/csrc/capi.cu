@@ -26,9 +26,10 @@ int rt_gpus(int* ids, int cap);
 int rt_gemm_host(int comps, int algo, int tile, int64_t cutoff, int64_t m, int64_t l, int64_t n,
                  const double* a, const double* b, double* c, int* nonfinite, double* device_ms,
                  int64_t panels, std::string* err);
-int oz_plan(int comps, int64_t m, int64_t n, int64_t l, const int* ela, const int* elb,
-            int* njobs, int* jobs, int* na, int* ranges_a, int* shift_a, int* nb, int* ranges_b,
-            int* shift_b);
+int exact_gemm(int comps, int64_t m, int64_t l, int64_t n, const double* A, int64_t lda,
+               const double* B, int64_t ldb, double* C, int64_t ldc, cudaStream_t s,
+               std::string* err);
+void exact_release();
 }  // namespace mpmm
 
 namespace {
@@ -105,13 +106,7 @@ cudaError_t host_streams(HostStreams** out) {
     g_hs.device = dev;
     if ((e = cudaStreamCreateWithFlags(&g_hs.copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
     if ((e = cudaStreamCreateWithFlags(&g_hs.comp, cudaStreamNonBlocking)) != cudaSuccess) return e;
-    // keep freed buffers in the stream-ordered pool between calls (the
-    // default threshold 0 unmaps them at every synchronize)
-    cudaMemPool_t pool;
-    if ((e = cudaDeviceGetDefaultMemPool(&pool, dev)) != cudaSuccess) return e;
-    uint64_t keep = UINT64_MAX;
-    if ((e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep)) != cudaSuccess)
-      return e;
+    if ((e = retain_default_pool()) != cudaSuccess) return e;
   }
   *out = &g_hs;
   return cudaSuccess;
@@ -350,6 +345,20 @@ int host_ewise(int comps, int sign, const double* x, const double* y, double* ou
 
 }  // namespace
 
+namespace mpmm {
+
+cudaError_t retain_default_pool() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  cudaMemPool_t pool;
+  if (e == cudaSuccess) e = cudaDeviceGetDefaultMemPool(&pool, dev);
+  uint64_t keep = UINT64_MAX;
+  if (e == cudaSuccess) e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  return e;
+}
+
+}  // namespace mpmm
+
 extern "C" {
 
 int mpmm_abi_version(void) { return MPMM_ABI_VERSION; }
@@ -586,6 +595,28 @@ int mpmm_oz_plan(int comps, int64_t m, int64_t n, int64_t l, const int* ela, con
                    shift_b);
   return rc == 0 ? MPMM_OK
                  : fail(MPMM_ERR_RANGE, "operand dynamic range too wide for the int8 CRT scheme");
+}
+
+int mpmm_gemm_exact_dev(int comps, int64_t m, int64_t l, int64_t n, const double* A,
+                        int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
+                        void* stream) {
+  if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
+  if (!dims_ok(m, l, n)) return fail(MPMM_ERR_ARG, "bad shape");
+  if (lda < l || ldb < n || ldc < n) return fail(MPMM_ERR_ARG, "leading dimension too small");
+  std::string err;
+  const int rc = exact_gemm(comps, m, l, n, A, lda, B, ldb, C, ldc, (cudaStream_t)stream, &err);
+  switch (rc) {
+    case 0: return MPMM_OK;
+    case 1: return fail(MPMM_ERR_ARG, err);
+    case 4: return fail(MPMM_ERR_RANGE, err);
+    case 5: return fail(MPMM_ERR_NONFINITE, err);
+    default: return fail(MPMM_ERR_CUDA, err);
+  }
+}
+
+int mpmm_exact_release(void) {
+  exact_release();
+  return MPMM_OK;
 }
 
 int mpmm_int8_gemm_batched_dev(int64_t m, int64_t n, int64_t k, int64_t batch, const int8_t* A,

@@ -1,0 +1,507 @@
+// exact.cpp -- native driver of the exact tensor mode (mpmm_gemm_exact_dev).
+//
+// C = A*B for DD/QD device matrices, the exact product rounded once, on
+// the int8 tensor cores (ozaki.cu documents the scheme).  Per call:
+//   scans of A and B -> [first product of a shape on a stream: host sync,
+//   oz_plan] -> device-side shifts and widths -> residues -> batched int8
+//   GEMMs (cuBLASLt) -> CRT combine -> ONE host read of the status and the
+//   actual widths.
+// A plan is cached per (device, stream, comps, m, l, n) and reused
+// speculatively; if the actual widths exceed it the product is planned
+// and recomputed, so a result is never returned from a plan that does not
+// fit.  Intermediates live in a per-key workspace kept across calls (when
+// under kKeepBytes); with the same operand/result addresses the whole
+// device side is replayed as one captured CUDA graph.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "kernels.h"
+
+namespace mpmm {
+
+namespace {
+
+constexpr int kMods[54] = {256, 251, 243, 241, 239, 233, 229, 227, 223, 211, 199, 197, 193, 191,
+                           181, 179, 173, 169, 167, 163, 157, 151, 149, 139, 137, 131, 127, 125,
+                           121, 113, 109, 107, 103, 101, 97,  89,  83,  79,  73,  71,  67,  61,
+                           59,  53,  49,  47,  43,  41,  37,  31,  29,  23,  19,  17};
+constexpr size_t kKeepBytes = size_t{1} << 30;   // workspace a cache entry may keep
+constexpr size_t kLtWorkspace = size_t{64} << 20;
+
+// ---------------------------------------------------------------------------
+// CRT tables: P = prod p_t (K limbs) then W_t = (P / p_t) * inv(P / p_t mod p_t)
+// (each < P, K limbs), as uint32 little-endian limbs
+// ---------------------------------------------------------------------------
+
+using Limbs = std::vector<uint32_t>;
+
+void mul_small(Limbs& x, uint32_t f) {
+  uint64_t c = 0;
+  for (auto& w : x) {
+    const uint64_t v = static_cast<uint64_t>(w) * f + c;
+    w = static_cast<uint32_t>(v);
+    c = v >> 32;
+  }
+  if (c) x.push_back(static_cast<uint32_t>(c));
+}
+
+uint32_t div_small(Limbs& x, uint32_t d) {   // x /= d, returns x mod d
+  uint64_t r = 0;
+  for (size_t i = x.size(); i-- > 0;) {
+    const uint64_t v = (r << 32) | x[i];
+    x[i] = static_cast<uint32_t>(v / d);
+    r = v % d;
+  }
+  return static_cast<uint32_t>(r);
+}
+
+uint32_t inv_mod(uint32_t a, uint32_t p) {   // a^-1 mod p, gcd(a, p) = 1
+  int64_t t = 0, nt = 1, r = p, nr = a % p;
+  while (nr) {
+    const int64_t q = r / nr;
+    std::tie(t, nt) = std::make_tuple(nt, t - q * nt);
+    std::tie(r, nr) = std::make_tuple(nr, r - q * nr);
+  }
+  return static_cast<uint32_t>(t < 0 ? t + p : t);
+}
+
+std::vector<uint32_t> crt_table(int N, int K) {
+  Limbs P{1};
+  for (int t = 0; t < N; ++t) mul_small(P, kMods[t]);
+  std::vector<uint32_t> out(static_cast<size_t>(N + 1) * K, 0u);
+  for (int q = 0; q < K && q < static_cast<int>(P.size()); ++q) out[q] = P[q];
+  for (int t = 0; t < N; ++t) {
+    Limbs M = P;
+    div_small(M, kMods[t]);
+    Limbs Mc = M;
+    const uint32_t mr = div_small(Mc, kMods[t]);   // M mod p_t
+    mul_small(M, inv_mod(mr, kMods[t]));           // < P: no reduction
+    for (int q = 0; q < K && q < static_cast<int>(M.size()); ++q)
+      out[static_cast<size_t>(t + 1) * K + q] = M[q];
+  }
+  return out;
+}
+
+// device copies of the tables, per (device, N, K); never freed
+std::mutex g_tab_mu;
+std::map<std::tuple<int, int, int>, uint32_t*> g_tables;
+
+cudaError_t device_table(int dev, int N, int K, const uint32_t** out) {
+  std::lock_guard<std::mutex> lock(g_tab_mu);
+  auto key = std::make_tuple(dev, N, K);
+  auto it = g_tables.find(key);
+  if (it == g_tables.end()) {
+    const std::vector<uint32_t> host = crt_table(N, K);
+    uint32_t* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, host.size() * sizeof(uint32_t));
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpy(d, host.data(), host.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+    it = g_tables.emplace(key, d).first;
+  }
+  *out = it->second;
+  return cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------
+// plans and workspaces
+// ---------------------------------------------------------------------------
+
+struct Plan {
+  int njobs = 0, na = 0, nb = 0, K = 0;
+  int jobs[kOzMaxJobs][8];     // a_range, b_range, N, K, words_a, words_b, beta_a, beta_b
+  int ranges_a[8], ranges_b[8];
+  int beta_a[4], beta_b[4], words_a[4], words_b[4], need_a[4], need_b[4];
+  bool from(const int* J, int nj, int na_, const int* ra, int nb_, const int* rb) {
+    njobs = nj;
+    na = na_;
+    nb = nb_;
+    std::memcpy(jobs, J, sizeof(int) * 8 * nj);
+    std::memcpy(ranges_a, ra, sizeof(int) * 2 * na);
+    std::memcpy(ranges_b, rb, sizeof(int) * 2 * nb);
+    for (int x = 0; x < 4; ++x) need_a[x] = need_b[x] = 0;
+    K = J[3];
+    for (int j = 0; j < nj; ++j) {
+      const int* q = J + 8 * j;
+      beta_a[q[0]] = q[6];
+      beta_b[q[1]] = q[7];
+      words_a[q[0]] = q[4];
+      words_b[q[1]] = q[5];
+      need_a[q[0]] = need_a[q[0]] > q[2] ? need_a[q[0]] : q[2];
+      need_b[q[1]] = need_b[q[1]] > q[2] ? need_b[q[1]] : q[2];
+    }
+    return true;
+  }
+  static int width(int raw, int c0, int c1) {   // planner's beta from a device width
+    int b = raw > 1 ? raw : 1;
+    for (int k = c1 - c0 - 1; k > 0; k >>= 1) ++b;
+    return b;
+  }
+  bool fits(const int* aux) const {   // aux[1..4] widths of A's ranges, aux[5..8] of B's
+    for (int x = 0; x < na; ++x)
+      if (width(aux[1 + x], ranges_a[2 * x], ranges_a[2 * x + 1]) > beta_a[x]) return false;
+    for (int y = 0; y < nb; ++y)
+      if (width(aux[5 + y], ranges_b[2 * y], ranges_b[2 * y + 1]) > beta_b[y]) return false;
+    return true;
+  }
+  bool loose(const int* aux) const {  // much wider than needed: replan next time
+    for (int x = 0; x < na; ++x)
+      if (width(aux[1 + x], ranges_a[2 * x], ranges_a[2 * x + 1]) + 8 < beta_a[x]) return true;
+    for (int y = 0; y < nb; ++y)
+      if (width(aux[5 + y], ranges_b[2 * y], ranges_b[2 * y + 1]) + 8 < beta_b[y]) return true;
+    return false;
+  }
+};
+
+int64_t pad16(int64_t x) { return (x + 15) / 16 * 16; }
+
+// Device buffers of one product: scan arrays + aux, shifts, residues,
+// residue products, cuBLASLt workspace.  One cudaMallocAsync block.
+struct Workspace {
+  char* base = nullptr;
+  size_t bytes = 0;
+  int* el = nullptr;           // EL_A | EL_B | aux[9]
+  int* aux = nullptr;
+  int* sh_a = nullptr;         // [na][m]
+  int* sh_b = nullptr;         // [nb][n]
+  int8_t* ra[4] = {};
+  int8_t* rb[4] = {};
+  int32_t* g[kOzMaxJobs] = {};
+  void* lt = nullptr;
+  bool padded_zeroed = false;
+};
+
+struct Entry {
+  int* aux_host = nullptr;                 // pinned: status + widths
+  int* el_host = nullptr;                  // pinned: scan arrays for the planner
+  cudaStream_t side = nullptr;             // capture stream (the caller's may be legacy)
+  bool planned = false;
+  Plan plan;
+  Workspace ws;
+  bool keep = false;                       // workspace kept across calls
+  const void* last[3] = {nullptr, nullptr, nullptr};
+  cudaGraphExec_t graph = nullptr;         // replay for ptrs == graph_ptrs
+  const void* graph_ptrs[3] = {nullptr, nullptr, nullptr};
+};
+
+using Key = std::tuple<int, uintptr_t, int, int64_t, int64_t, int64_t>;
+std::mutex g_mu;
+std::map<Key, std::unique_ptr<Entry>> g_entries;
+
+size_t workspace_bytes(const Plan& pl, int comps, int64_t m, int64_t l, int64_t n) {
+  const int64_t mp = pad16(m), np = pad16(n), lp = pad16(l);
+  size_t b = static_cast<size_t>(2 * comps * (m + n) + 16) * 4 + 256;
+  b += static_cast<size_t>((pl.na * m + pl.nb * n) * 4 + 512);
+  for (int x = 0; x < pl.na; ++x) b += static_cast<size_t>(pl.need_a[x] * mp * lp) + 256;
+  for (int y = 0; y < pl.nb; ++y) b += static_cast<size_t>(pl.need_b[y] * np * lp) + 256;
+  for (int j = 0; j < pl.njobs; ++j) b += static_cast<size_t>(pl.jobs[j][2] * mp * np) * 4 + 256;
+  return b + kLtWorkspace;
+}
+
+void free_workspace(Workspace& ws, cudaStream_t s) {
+  if (ws.base) cudaFreeAsync(ws.base, s);
+  ws = Workspace{};
+}
+
+cudaError_t make_workspace(Workspace& ws, const Plan* pl, int comps, int64_t m, int64_t l,
+                           int64_t n, cudaStream_t s) {
+  // without a plan: only the scan part (the planning call)
+  const size_t elb = static_cast<size_t>(2 * comps * (m + n) + 16) * 4;
+  size_t bytes = pl ? workspace_bytes(*pl, comps, m, l, n) : elb + 256;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws.base), bytes, s);
+  if (e != cudaSuccess) return e;
+  ws.bytes = bytes;
+  size_t off = 0;
+  auto take = [&](size_t nb) {
+    char* p = ws.base + off;
+    off += (nb + 255) / 256 * 256;
+    return p;
+  };
+  ws.el = reinterpret_cast<int*>(take(elb));
+  ws.aux = ws.el + 2 * comps * (m + n);
+  if (!pl) return cudaSuccess;
+  const int64_t mp = pad16(m), np = pad16(n), lp = pad16(l);
+  ws.sh_a = reinterpret_cast<int*>(take(static_cast<size_t>(pl->na * m) * 4));
+  ws.sh_b = reinterpret_cast<int*>(take(static_cast<size_t>(pl->nb * n) * 4));
+  for (int x = 0; x < pl->na; ++x)
+    ws.ra[x] = reinterpret_cast<int8_t*>(take(static_cast<size_t>(pl->need_a[x] * mp * lp)));
+  for (int y = 0; y < pl->nb; ++y)
+    ws.rb[y] = reinterpret_cast<int8_t*>(take(static_cast<size_t>(pl->need_b[y] * np * lp)));
+  for (int j = 0; j < pl->njobs; ++j)
+    ws.g[j] = reinterpret_cast<int32_t*>(take(static_cast<size_t>(pl->jobs[j][2] * mp * np) * 4));
+  ws.lt = take(kLtWorkspace);
+  return cudaSuccess;
+}
+
+// scans (stream-ordered, no sync)
+cudaError_t enqueue_scans(int comps, int64_t m, int64_t l, int64_t n, const double* A, int64_t lda,
+                          const double* B, int64_t ldb, Workspace& ws, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(ws.aux, 0, 9 * sizeof(int), s);
+  if (e == cudaSuccess)
+    e = oz_scan_launch(0, A, lda, (int)m, (int)l, comps, ws.el, ws.aux, s);
+  if (e == cudaSuccess)
+    e = oz_scan_launch(1, B, ldb, (int)l, (int)n, comps, ws.el + 2 * comps * m, ws.aux, s);
+  return e;
+}
+
+// everything after the scans (stream-ordered, no sync, no allocation)
+cudaError_t enqueue_product(const Plan& pl, int comps, int64_t m, int64_t l, int64_t n,
+                            const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                            int64_t ldc, Workspace& ws, int dev, cudaStream_t s,
+                            std::string* err) {
+  const int64_t mp = pad16(m), np = pad16(n), lp = pad16(l);
+  if (ldc != n) {
+    *err = "the exact mode writes a dense C (ldc == n)";
+    return cudaErrorInvalidValue;
+  }
+  cudaError_t e = oz_shifts_launch(comps, pl.na, pl.ranges_a, (int)m, ws.el, ws.sh_a, ws.aux + 1, s);
+  if (e == cudaSuccess)
+    e = oz_shifts_launch(comps, pl.nb, pl.ranges_b, (int)n, ws.el + 2 * comps * m, ws.sh_b,
+                         ws.aux + 5, s);
+  for (int x = 0; x < pl.na && e == cudaSuccess; ++x)
+    e = oz_residues_launch(0, A, lda, (int)m, (int)l, comps, pl.ranges_a[2 * x],
+                           pl.ranges_a[2 * x + 1], ws.sh_a + x * m, pl.need_a[x], pl.words_a[x],
+                           ws.ra[x], lp, mp * lp, s);
+  for (int y = 0; y < pl.nb && e == cudaSuccess; ++y)
+    e = oz_residues_launch(1, B, ldb, (int)l, (int)n, comps, pl.ranges_b[2 * y],
+                           pl.ranges_b[2 * y + 1], ws.sh_b + y * n, pl.need_b[y], pl.words_b[y],
+                           ws.rb[y], lp, np * lp, s);
+  if (e != cudaSuccess) return e;
+  CrtJob jobs[kOzMaxJobs];
+  for (int j = 0; j < pl.njobs; ++j) {
+    const int* q = pl.jobs[j];
+    if (int8_gemm_batched(mp, np, lp, q[2], ws.ra[q[0]], ws.rb[q[1]], ws.g[j], ws.lt,
+                          kLtWorkspace, s, err) != 0)
+      return cudaErrorUnknown;
+    const uint32_t* tab = nullptr;
+    if ((e = device_table(dev, q[2], pl.K, &tab)) != cudaSuccess) return e;
+    jobs[j] = CrtJob{ws.g[j], ws.sh_a + q[0] * m, ws.sh_b + q[1] * n, tab, q[2], pl.K, np,
+                     mp * np};
+  }
+  return oz_combine_launch(comps, jobs, pl.njobs, (int)m, (int)n, C, ws.aux, s);
+}
+
+}  // namespace
+
+// 0 ok; 1 bad argument; 2 CUDA error; 4 not representable; 5 non-finite
+int exact_gemm(int comps, int64_t m, int64_t l, int64_t n, const double* A, int64_t lda,
+               const double* B, int64_t ldb, double* C, int64_t ldc, cudaStream_t s,
+               std::string* err) {
+  if (m == 0 || n == 0) return 0;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    *err = cudaGetErrorString(e);
+    return 2;
+  }
+  if ((e = retain_default_pool()) != cudaSuccess) {
+    *err = cudaGetErrorString(e);
+    return 2;
+  }
+  if (l > 131071) {
+    *err = "inner dimension too large for exact int32 residue products";
+    return 1;
+  }
+  // table uploads (synchronous) must not happen inside a capture: warm them
+  const Key key{dev, reinterpret_cast<uintptr_t>(s), comps, m, l, n};
+  std::unique_lock<std::mutex> lock(g_mu);
+  auto& slot = g_entries[key];
+  if (!slot) {
+    std::unique_ptr<Entry> ne(new Entry());
+    const size_t elb = static_cast<size_t>(2 * comps * (m + n) + 16) * sizeof(int);
+    if ((e = cudaMallocHost(reinterpret_cast<void**>(&ne->aux_host), 16 * sizeof(int))) !=
+            cudaSuccess ||
+        (e = cudaMallocHost(reinterpret_cast<void**>(&ne->el_host), elb)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&ne->side, cudaStreamNonBlocking)) != cudaSuccess) {
+      *err = cudaGetErrorString(e);
+      return 2;
+    }
+    slot = std::move(ne);
+  }
+  Entry& en = *slot;
+  lock.unlock();
+  auto cuda_err = [&](cudaError_t ce) {
+    if (err->empty()) *err = cudaGetErrorString(ce);
+    return 2;
+  };
+  const void* ptrs[3] = {A, B, C};
+  const bool same = ptrs[0] == en.last[0] && ptrs[1] == en.last[1] && ptrs[2] == en.last[2];
+  // 1. graph replay for the same addresses
+  if (en.graph && same && std::memcmp(en.graph_ptrs, ptrs, sizeof ptrs) == 0) {
+    if ((e = cudaGraphLaunch(en.graph, s)) != cudaSuccess) return cuda_err(e);
+    if ((e = cudaMemcpyAsync(en.aux_host, en.ws.aux, 9 * sizeof(int), cudaMemcpyDeviceToHost,
+                             s)) != cudaSuccess)
+      return cuda_err(e);
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_err(e);
+    const int* h = en.aux_host;
+    if (!(h[0] & 1) && !(h[0] & 2) && en.plan.fits(h) && !en.plan.loose(h)) return 0;
+    cudaGraphExecDestroy(en.graph);      // fall through to the eager path
+    en.graph = nullptr;
+    en.planned = false;
+  }
+  // 2. eager: scans, then plan (sync) or the cached plan (speculative)
+  const bool speculative = en.planned;
+  Workspace scratch;
+  Workspace* ws = &en.ws;
+  if (speculative && !en.ws.base) {          // plan kept, workspace released last time
+    if ((e = make_workspace(en.ws, &en.plan, comps, m, l, n, s)) != cudaSuccess)
+      return cuda_err(e);
+  }
+  if (!speculative) {
+    if (en.ws.base) free_workspace(en.ws, s);
+    if ((e = make_workspace(scratch, nullptr, comps, m, l, n, s)) != cudaSuccess)
+      return cuda_err(e);
+    ws = &scratch;
+  }
+  if ((e = enqueue_scans(comps, m, l, n, A, lda, B, ldb, *ws, s)) != cudaSuccess)
+    return cuda_err(e);
+  auto replan = [&](Workspace& from) -> int {
+    const size_t elb = static_cast<size_t>(2 * comps * (m + n) + 9) * 4;
+    cudaError_t ce = cudaMemcpyAsync(en.el_host, from.el, elb, cudaMemcpyDeviceToHost, s);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+    if (ce != cudaSuccess) return cuda_err(ce);
+    if (en.el_host[2 * comps * (m + n)] & 1) {
+      *err = "non-finite operand: the exact tensor mode needs finite inputs";
+      return 5;
+    }
+    int J[kOzMaxJobs * 8], nj = 0, na = 0, nb = 0, ra[8], rb[8];
+    if (oz_plan(comps, m, n, l, en.el_host, en.el_host + 2 * comps * m, &nj, J, &na, ra,
+                nullptr, &nb, rb, nullptr) != 0) {
+      *err = "operand dynamic range too wide for the int8 CRT scheme";
+      return 4;
+    }
+    en.plan.from(J, nj, na, ra, nb, rb);
+    en.planned = true;
+    return 0;
+  };
+  int rc = 0;
+  if (!speculative) {
+    if ((rc = replan(scratch)) != 0) {
+      free_workspace(scratch, s);
+      en.planned = false;
+      return rc;
+    }
+    if ((e = make_workspace(en.ws, &en.plan, comps, m, l, n, s)) != cudaSuccess)
+      return cuda_err(e);
+    // the scan results move to the product's workspace
+    const size_t elb = static_cast<size_t>(2 * comps * (m + n) + 9) * 4;
+    if ((e = cudaMemcpyAsync(en.ws.el, scratch.el, elb, cudaMemcpyDeviceToDevice, s)) !=
+        cudaSuccess)
+      return cuda_err(e);
+    free_workspace(scratch, s);
+    en.keep = en.ws.bytes <= kKeepBytes;
+  }
+  const int64_t mp = pad16(m), np = pad16(n), lp = pad16(l);
+  auto zero_pads = [&]() -> cudaError_t {
+    if (en.ws.padded_zeroed || (mp == m && np == n && lp == l)) return cudaSuccess;
+    for (int x = 0; x < en.plan.na; ++x) {
+      cudaError_t ce = cudaMemsetAsync(en.ws.ra[x], 0, static_cast<size_t>(en.plan.need_a[x] *
+                                                                             mp * lp), s);
+      if (ce != cudaSuccess) return ce;
+    }
+    for (int y = 0; y < en.plan.nb; ++y) {
+      cudaError_t ce = cudaMemsetAsync(en.ws.rb[y], 0, static_cast<size_t>(en.plan.need_b[y] *
+                                                                             np * lp), s);
+      if (ce != cudaSuccess) return ce;
+    }
+    en.ws.padded_zeroed = true;
+    return cudaSuccess;
+  };
+  if ((e = zero_pads()) != cudaSuccess) return cuda_err(e);
+  if ((e = enqueue_product(en.plan, comps, m, l, n, A, lda, B, ldb, C, ldc, en.ws, dev, s, err)) !=
+      cudaSuccess)
+    return cuda_err(e);
+  if ((e = cudaMemcpyAsync(en.aux_host, en.ws.aux, 9 * sizeof(int), cudaMemcpyDeviceToHost,
+                           s)) != cudaSuccess)
+    return cuda_err(e);
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_err(e);
+  int h[9];
+  std::memcpy(h, en.aux_host, sizeof h);
+  if (speculative && !(h[0] & 1) && !en.plan.fits(h)) {
+    // the cached plan is too narrow for these operands: plan and redo
+    if ((rc = replan(en.ws)) != 0) return rc;
+    free_workspace(en.ws, s);
+    if ((e = make_workspace(en.ws, &en.plan, comps, m, l, n, s)) != cudaSuccess)
+      return cuda_err(e);
+    if ((e = enqueue_scans(comps, m, l, n, A, lda, B, ldb, en.ws, s)) != cudaSuccess ||
+        (e = zero_pads()) != cudaSuccess ||
+        (e = enqueue_product(en.plan, comps, m, l, n, A, lda, B, ldb, C, ldc, en.ws, dev, s,
+                             err)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(en.aux_host, en.ws.aux, 9 * sizeof(int), cudaMemcpyDeviceToHost,
+                             s)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(s)) != cudaSuccess)
+      return cuda_err(e);
+    std::memcpy(h, en.aux_host, sizeof h);
+    en.keep = en.ws.bytes <= kKeepBytes;
+  }
+  if (h[0] & 1) {
+    en.planned = false;
+    *err = "non-finite operand or product overflowed the working precision";
+    rc = 5;
+  } else if (h[0] & 2) {
+    en.planned = false;
+    *err = "CRT combine window exceeded";
+    rc = 4;
+  } else if (en.plan.loose(h)) {
+    en.planned = false;          // much narrower data now: replan next time
+  }
+  // 3. a graph for the next product with the same addresses, captured on
+  // the entry's own stream (the caller's may be the legacy stream)
+  if (rc == 0 && en.planned && en.keep && same && !en.graph) {
+    cudaGraph_t g = nullptr;
+    cudaEvent_t ready = nullptr;
+    if (cudaEventCreateWithFlags(&ready, cudaEventDisableTiming) == cudaSuccess &&
+        cudaEventRecord(ready, s) == cudaSuccess &&
+        cudaStreamWaitEvent(en.side, ready, 0) == cudaSuccess &&
+        cudaStreamBeginCapture(en.side, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      cudaError_t ce = enqueue_scans(comps, m, l, n, A, lda, B, ldb, en.ws, en.side);
+      std::string cerr;
+      if (ce == cudaSuccess)
+        ce = enqueue_product(en.plan, comps, m, l, n, A, lda, B, ldb, C, ldc, en.ws, dev,
+                             en.side, &cerr);
+      cudaError_t ee = cudaStreamEndCapture(en.side, &g);
+      if (ce == cudaSuccess && ee == cudaSuccess && g != nullptr &&
+          cudaGraphInstantiate(&en.graph, g, 0) == cudaSuccess) {
+        std::memcpy(en.graph_ptrs, ptrs, sizeof ptrs);
+      } else {
+        en.graph = nullptr;
+      }
+      if (g) cudaGraphDestroy(g);
+    }
+    if (ready) cudaEventDestroy(ready);
+    cudaGetLastError();
+  }
+  std::memcpy(en.last, ptrs, sizeof ptrs);
+  if (!en.keep || !en.planned) {
+    if (en.graph) {
+      cudaGraphExecDestroy(en.graph);
+      en.graph = nullptr;
+    }
+    free_workspace(en.ws, s);
+  }
+  return rc;
+}
+
+// Drop every cached plan, workspace and graph (device memory back to the pool).
+void exact_release() {
+  std::lock_guard<std::mutex> lock(g_mu);
+  for (auto& kv : g_entries) {
+    Entry& en = *kv.second;
+    if (en.graph) cudaGraphExecDestroy(en.graph);
+    free_workspace(en.ws, reinterpret_cast<cudaStream_t>(std::get<1>(kv.first)));
+    if (en.aux_host) cudaFreeHost(en.aux_host);
+    if (en.el_host) cudaFreeHost(en.el_host);
+    if (en.side) cudaStreamDestroy(en.side);
+  }
+  g_entries.clear();
+}
+
+}  // namespace mpmm

@@ -99,13 +99,32 @@ cudaError_t oz_scan_launch(int by_cols, const double* X, int64_t ld, int rows, i
 cudaError_t oz_residues_launch(int by_cols, const double* X, int64_t ld, int rows, int cols,
                                int comps, int c0, int c1, const int* shift, int N, int W,
                                int8_t* R, int64_t rpitch, int64_t rplane, cudaStream_t s);
+// One CRT job of the combine (56 bytes; tensor.py / exact.cpp build them).
+struct CrtJob {
+  const int32_t* G;         // [N][.][gpitch] residue products, plane stride gplane
+  const int* srow;          // [m] row shifts
+  const int* scol;          // [n] column shifts
+  const uint32_t* table;    // [K] P limbs, then [N][K] weight limbs
+  int N, K;
+  int64_t gpitch, gplane;
+};
+constexpr int kOzMaxJobs = 16;
+
 cudaError_t oz_combine_launch(int comps, const void* jobs, int njobs, int m, int n, double* C,
                               int* status, cudaStream_t s);
+int oz_plan(int comps, int64_t m, int64_t n, int64_t l, const int* ela, const int* elb,
+            int* njobs, int* jobs, int* na, int* ranges_a, int* shift_a, int* nb, int* ranges_b,
+            int* shift_b);
 cudaError_t oz_shifts_launch(int comps, int nranges, const int* ranges, int odim, const int* EL,
                              int* shift, int* beta, cudaStream_t s);
 int int8_gemm_batched(int64_t m, int64_t n, int64_t k, int64_t batch, const int8_t* A,
                       const int8_t* Bt, int32_t* C, void* workspace, size_t ws_size,
                       cudaStream_t stream, std::string* err);
+
+// Keep freed stream-ordered allocations of the current device's default
+// pool mapped across synchronizations (the default threshold, 0, unmaps
+// them at every sync and the next call re-maps gigabytes of pages).
+cudaError_t retain_default_pool();
 
 cudaError_t fp64_burn_launch(int op, int blocks, int threads, int64_t iters, double* out,
                              cudaStream_t stream);

@@ -92,7 +92,8 @@ std::vector<std::vector<std::pair<int, int>>> partitions(int comps) {
 
 }  // namespace
 
-// returns 0 ok, 4 not representable; jobs: max 16 x 8 ints
+// returns 0 ok, 4 not representable; jobs: max 16 x 8 ints; shift_a /
+// shift_b may be null (the device derives the shifts itself)
 int oz_plan(int comps, int64_t m, int64_t n, int64_t l, const int* ela, const int* elb,
             int* njobs, int* jobs, int* na, int* ranges_a, int* shift_a, int* nb, int* ranges_b,
             int* shift_b) {
@@ -147,13 +148,15 @@ int oz_plan(int comps, int64_t m, int64_t n, int64_t l, const int* ela, const in
     const Range& A = ra_cache[get(ra_cache, ela, m, PA[x].first, PA[x].second)];
     ranges_a[2 * x] = A.c0;
     ranges_a[2 * x + 1] = A.c1;
-    for (int64_t o = 0; o < m; ++o) shift_a[x * m + o] = A.shift[o];
+    if (shift_a)
+      for (int64_t o = 0; o < m; ++o) shift_a[x * m + o] = A.shift[o];
   }
   for (size_t y = 0; y < PB.size(); ++y) {
     const Range& B = rb_cache[get(rb_cache, elb, n, PB[y].first, PB[y].second)];
     ranges_b[2 * y] = B.c0;
     ranges_b[2 * y + 1] = B.c1;
-    for (int64_t o = 0; o < n; ++o) shift_b[y * n + o] = B.shift[o];
+    if (shift_b)
+      for (int64_t o = 0; o < n; ++o) shift_b[y * n + o] = B.shift[o];
   }
   int q = 0;
   for (size_t x = 0; x < PA.size(); ++x)

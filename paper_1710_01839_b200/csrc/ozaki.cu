@@ -380,16 +380,7 @@ residues_cols_kernel(const double* __restrict__ X, int64_t ld, int rows, int col
 }  // namespace
 
 // Per-job CRT data (device): moduli count, limb count, P limbs, weights.
-struct CrtJob {
-  const int32_t* G;         // [N][.][gpitch] residue products, plane stride gplane
-  const int* srow;          // [m] row shifts
-  const int* scol;          // [n] column shifts
-  const uint32_t* table;    // [K] P limbs, then [N][K] weight limbs
-  int N, K;
-  int64_t gpitch, gplane;
-};
-
-constexpr int kMaxJobs = 16;
+constexpr int kMaxJobs = kOzMaxJobs;
 
 // up to kMaxJobs jobs by value (kernel parameter space, no device table)
 struct CrtJobs {

@@ -322,14 +322,7 @@ cudaError_t strassen_run(int comps, int64_t cutoff, int tile, int64_t m, int64_t
   // keep freed scratch in the stream-ordered pool across calls: with the
   // default release threshold (0) every synchronize returns it to the
   // driver and the next call re-maps gigabytes of pages
-  int dev = 0;
-  cudaError_t pe = cudaGetDevice(&dev);
-  cudaMemPool_t pool;
-  if (pe == cudaSuccess) pe = cudaDeviceGetDefaultMemPool(&pool, dev);
-  if (pe == cudaSuccess) {
-    uint64_t keep = UINT64_MAX;
-    pe = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-  }
+  cudaError_t pe = retain_default_pool();
   if (pe != cudaSuccess) return pe;
   int64_t budget = 0;
   if (const char* env = std::getenv("MPMM_STRASSEN_BUDGET_MB")) {

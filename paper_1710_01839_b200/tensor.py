@@ -86,17 +86,6 @@ def crt_table(N, K=None):
     return np.array(words, dtype=np.uint32), K
 
 
-_dev_cache = {}
-
-
-def _device_const(key, host_array, device):
-    k = (key, str(device))
-    if k not in _dev_cache:
-        import torch
-        _dev_cache[k] = torch.from_numpy(np.ascontiguousarray(host_array)).to(device)
-    return _dev_cache[k]
-
-
 class Plan:
     """A chosen component split: ranges of A and B with their bit widths
     (beta) and residue word counts, and the jobs (pairs of ranges) with
@@ -117,25 +106,6 @@ class Plan:
             self.beta_a[ia], self.beta_b[ib] = int(j[6]), int(j[7])
             self.need_a[ia] = max(self.need_a[ia], N)
             self.need_b[ib] = max(self.need_b[ib], N)
-
-    def fits(self, actual_a, actual_b):
-        """The plan is exact for operands whose per-range widths are these."""
-        return all(x <= y for x, y in zip(actual_a, self.beta_a)) and \
-            all(x <= y for x, y in zip(actual_b, self.beta_b))
-
-    def loose(self, actual_a, actual_b, slack=8):
-        """Much wider than needed (a fresh plan would use fewer moduli)."""
-        return any(x + slack < y for x, y in zip(actual_a, self.beta_a)) or \
-            any(x + slack < y for x, y in zip(actual_b, self.beta_b))
-
-
-_PLANS = {}   # (device, stream, comps, m, l, n) -> Plan of the last product
-
-
-def _widths(raw, ranges):
-    """Device betas (max(E - L) + 1 per range, 0 when empty) -> planner
-    widths (+1 bit per doubling of the range's component count)."""
-    return [max(int(b), 1) + (c1 - c0 - 1).bit_length() for b, (c0, c1) in zip(raw, ranges)]
 
 
 def _scan(A, B, stream):
@@ -176,156 +146,47 @@ def plan(A, B, stream=None):
     return _make_plan(buf, ea, eb, comps, m, l, B.shape[1])
 
 
-def _execute(pl, A, B, buf, aux, ea, stream):
-    """Shifts, residues, int8 GEMMs and the CRT combine for plan ``pl``;
-    everything is enqueued on ``stream`` (no host sync)."""
-    import torch
-    m, l, comps = A.shape
-    n = B.shape[1]
-    dev = A.device
-    pad = lambda x: -(-x // 16) * 16  # noqa: E731  (cuBLASLt IMMA alignment)
-    mp_, np_, lp = pad(m), pad(n), pad(l)
-    sh_a = torch.empty((len(pl.ranges_a), m), dtype=torch.int32, device=dev)
-    sh_b = torch.empty((len(pl.ranges_b), n), dtype=torch.int32, device=dev)
-    _cuda.oz_shifts_dev(comps, pl.ranges_a, m, buf.data_ptr(), sh_a.data_ptr(),
-                        aux[1:].data_ptr(), stream)
-    _cuda.oz_shifts_dev(comps, pl.ranges_b, n, buf[ea:].data_ptr(), sh_b.data_ptr(),
-                        aux[5:].data_ptr(), stream)
-    alloc = torch.zeros if (mp_, np_, lp) != (m, n, l) else torch.empty
-    RA, RB = [], []
-    for r, (c0, c1) in enumerate(pl.ranges_a):
-        R = alloc((pl.need_a[r], mp_, lp), dtype=torch.int8, device=dev)
-        _cuda.oz_residues_dev(0, comps, c0, c1, m, l, A.data_ptr(), A.shape[1], sh_a[r].data_ptr(),
-                              pl.need_a[r], pl.words_a[r], R.data_ptr(), lp, mp_ * lp, stream)
-        RA.append(R)
-    for r, (c0, c1) in enumerate(pl.ranges_b):
-        R = alloc((pl.need_b[r], np_, lp), dtype=torch.int8, device=dev)
-        _cuda.oz_residues_dev(1, comps, c0, c1, l, n, B.data_ptr(), B.shape[1], sh_b[r].data_ptr(),
-                              pl.need_b[r], pl.words_b[r], R.data_ptr(), lp, np_ * lp, stream)
-        RB.append(R)
-    ws = torch.empty(WORKSPACE_BYTES, dtype=torch.uint8, device=dev)
-    rec = np.zeros(len(pl.jobs), dtype=_REC)
-    Gs = []
-    for q, (ia, ib, N) in enumerate(pl.jobs):
-        G = torch.empty((N, mp_, np_), dtype=torch.int32, device=dev)
-        _cuda.int8_gemm_batched_dev(mp_, np_, lp, N, RA[ia].data_ptr(), RB[ib].data_ptr(),
-                                    G.data_ptr(), ws.data_ptr(), WORKSPACE_BYTES, stream)
-        table = _device_const(("crt", N, pl.K), crt_table(N, pl.K)[0], dev)
-        rec[q] = (G.data_ptr(), sh_a[ia].data_ptr(), sh_b[ib].data_ptr(), table.data_ptr(), N,
-                  pl.K, np_, mp_ * np_)
-        Gs.append(G)
-    C = torch.empty((m, n, comps), dtype=torch.float64, device=dev)
-    _cuda.oz_combine_dev(comps, rec.ctypes.data, len(pl.jobs), m, n, C.data_ptr(),
-                         aux.data_ptr(), stream)
-    # buffers return to the caching allocator in stream order
-    return C
-
-
-_REC = np.dtype([("G", "<u8"), ("sr", "<u8"), ("sc", "<u8"), ("tb", "<u8"), ("N", "<i4"),
-                 ("K", "<i4"), ("gp", "<i8"), ("gl", "<i8")])
-
-
-class _Replay:
-    """The whole device side of one product (scans, shifts, residues, int8
-    GEMMs, combine) captured as a CUDA graph for fixed operand addresses:
-    repeated products of the same operands pay one graph launch instead of
-    ~15 host-side launches.  The data are read afresh at every replay, and
-    the widths it reports are checked against the plan as on the eager path."""
-
-    def __init__(self, pl, A, B):
-        import torch
-        self.pl = pl
-        self.ptrs = (A.data_ptr(), B.data_ptr())
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
-            stream = torch.cuda.current_stream().cuda_stream
-            buf, aux, ea, _ = _scan(A, B, stream)
-            self.C = _execute(pl, A, B, buf, aux, ea, stream)
-        self.aux = aux
-
-    def run(self):
-        self.graph.replay()
-        return self.aux.cpu().numpy()
-
-
-_REPLAYS = {}        # key -> _Replay
-_LAST_PTRS = {}      # key -> operand addresses of the previous product
-GRAPH_MAX_BYTES = 1 << 30     # intermediates a cached graph may keep alive
-
-
-def _graph_bytes(pl, m, l, n):
-    pad = lambda x: -(-x // 16) * 16  # noqa: E731
-    g = sum(N for _, _, N in pl.jobs) * pad(m) * pad(n) * 4
-    r = (sum(pl.need_a) * pad(m) + sum(pl.need_b) * pad(n)) * pad(l)
-    return g + r
-
-
-def _check(h, pl):
-    if h[0] & 1:
-        raise RangeError("non-finite operand or product overflowed the working precision")
-    if h[0] & 2:
-        raise NotRepresentable("CRT combine window exceeded")
-    return (_widths(h[1:1 + len(pl.ranges_a)], pl.ranges_a),
-            _widths(h[5:5 + len(pl.ranges_b)], pl.ranges_b))
-
-
 def matmul_exact_tensors(A, B):
     """C = A*B for (m,l,comps) / (l,n,comps) float64 CUDA tensors, exact
     product rounded once to comps doubles; returns the (m,n,comps) tensor.
 
-    A product of the same shape on the same stream as the previous one
-    reuses its plan speculatively: the scans, the device-side shifts and
-    width check, the residues, GEMMs and combine are all enqueued at once
-    and the ONE host sync reads the status and the actual widths; if the
-    data needs a wider plan than the cached one the product is planned and
-    recomputed (never returned wrong).  When the same operands come back
-    (same addresses) the device side replays as one CUDA graph."""
+    One call into the native driver (csrc/exact.cpp, mpmm_gemm_exact_dev):
+    scans, [plan on the first product of a shape on this stream], shifts,
+    residues, int8 GEMMs and the CRT combine, with the plan reused
+    speculatively (device-side width check, replanned when it does not
+    fit), intermediates cached, and the whole device side replayed as one
+    CUDA graph when the same operand/result addresses come back."""
     import torch
     m, l, comps = A.shape
     n = B.shape[1]
+    if not (A.is_contiguous() and B.is_contiguous()):
+        A, B = A.contiguous(), B.contiguous()
     dev = A.device
     stream = torch.cuda.current_stream(dev).cuda_stream
-    key = (dev.index, stream, comps, m, l, n)
-    ptrs = (A.data_ptr(), B.data_ptr())
-    rp = _REPLAYS.get(key)
-    if rp is not None and rp.ptrs == ptrs:
-        try:
-            act = _check(rp.run(), rp.pl)
-            if rp.pl.fits(*act) and not rp.pl.loose(*act):
-                return rp.C.clone()
-        except (RangeError, NotRepresentable):
-            pass                      # redo eagerly: same error, or the exact reason
-        _REPLAYS.pop(key, None)
-        _PLANS.pop(key, None)
-    buf, aux, ea, eb = _scan(A, B, stream)
-    pl = _PLANS.get(key)
-    speculative = pl is not None
-    if pl is None:
-        pl = _make_plan(buf, ea, eb, comps, m, l, n)
-    C = _execute(pl, A, B, buf, aux, ea, stream)
-    h = aux.cpu().numpy()
-    try:
-        act_a, act_b = _check(h, pl)
-    except RangeError:
-        _PLANS.pop(key, None)
-        raise
-    if speculative and not pl.fits(act_a, act_b):
-        pl = _make_plan(buf, ea, eb, comps, m, l, n)
-        aux.zero_()
-        C = _execute(pl, A, B, buf, aux, ea, stream)
-        act_a, act_b = _check(aux.cpu().numpy(), pl)
-    if pl.loose(act_a, act_b):
-        _PLANS.pop(key, None)        # next product of this shape replans
-        _LAST_PTRS.pop(key, None)
-        return C
-    _PLANS[key] = pl
-    if _LAST_PTRS.get(key) == ptrs and _graph_bytes(pl, m, l, n) <= GRAPH_MAX_BYTES:
-        try:
-            _REPLAYS[key] = _Replay(pl, A, B)
-        except RuntimeError:
-            _REPLAYS.pop(key, None)   # capture not possible here: stay eager
-    _LAST_PTRS[key] = ptrs
-    return C
+    C = _out_buffer(m, n, comps, dev, stream)
+    rc = _cuda.gemm_exact_dev(comps, m, l, n, A.data_ptr(), l, B.data_ptr(), n, C.data_ptr(), n,
+                              stream)
+    if rc == 5:
+        raise RangeError(_cuda.last_error())
+    if rc == 4:
+        raise NotRepresentable(_cuda.last_error())
+    return C.clone()
+
+
+_OUT = {}   # (device, stream, shape) -> the driver's output buffer (stable address)
+
+
+def _out_buffer(m, n, comps, dev, stream):
+    """A stable result address per shape and stream, so repeated products
+    of the same operands can replay the driver's captured graph; callers
+    get a copy."""
+    import torch
+    key = (dev.index, stream, m, n, comps)
+    buf = _OUT.get(key)
+    if buf is None:
+        buf = torch.empty((m, n, comps), dtype=torch.float64, device=dev)
+        _OUT[key] = buf
+    return buf
 
 
 def matmul_exact(a, b):
