@@ -211,6 +211,12 @@ int mpmm_oz_residues_dev(int by_cols, int comps, int c0, int c1, int64_t rows, i
 int mpmm_gemm_exact_dev(int comps, int64_t m, int64_t l, int64_t n, const double *A,
                         int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc,
                         void *stream);
+/* tcgen05 residue GEMMs: R_t = (A_t * Bt_t^T) mod p_t for the first batch
+ * moduli, A_t m x k and Bt_t n x k int8 (k contiguous, planes m*k / n*k),
+ * R_t m x n uint8 row-major (plane m*n); the int32 accumulator stays in
+ * TMEM.  m % 128 == 0, n % 256 == 0, k % 128 == 0, k <= 131071. */
+int mpmm_residue_gemm_dev(int64_t m, int64_t n, int64_t k, int64_t batch, const int8_t *A,
+                          const int8_t *Bt, uint8_t *R, void *stream);
 /* Free every cached exact-mode plan, workspace and graph. */
 int mpmm_exact_release(void);
 /* Host-only planner of the exact tensor mode: from the scan arrays of A

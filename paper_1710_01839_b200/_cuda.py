@@ -69,6 +69,7 @@ _SIGNATURES = {
                      ctypes.POINTER(_INT), _VP, _VP, ctypes.POINTER(_INT), _VP, _VP],
     "mpmm_gemm_exact_dev": [_INT, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _VP],
     "mpmm_exact_release": [],
+    "mpmm_residue_gemm_dev": [_I64, _I64, _I64, _I64, _VP, _VP, _VP, _VP],
     "mpmm_int8_gemm_batched_dev": [_I64, _I64, _I64, _I64, _VP, _VP, _VP, _VP, _I64, _VP],
     "mpmm_oz_combine_dev": [_INT, _VP, _INT, _I64, _I64, _VP, _VP, _VP],
     "mpmm_oz_shifts_dev": [_INT, _INT, _VP, _I64, _VP, _VP, _VP, _VP],
@@ -396,6 +397,11 @@ def gemm_exact_dev(comps, m, l, n, A, lda, B, ldb, C, ldc, stream=None):
         return rc
     check(rc)
     return 0
+
+
+def residue_gemm_dev(m, n, k, batch, A, Bt, R, stream=None):
+    sync_device()
+    check(load().mpmm_residue_gemm_dev(m, n, k, batch, A, Bt, R, stream))
 
 
 def last_error():

@@ -614,6 +614,15 @@ int mpmm_gemm_exact_dev(int comps, int64_t m, int64_t l, int64_t n, const double
   }
 }
 
+int mpmm_residue_gemm_dev(int64_t m, int64_t n, int64_t k, int64_t batch, const int8_t* A,
+                          const int8_t* Bt, uint8_t* R, void* stream) {
+  if (!tc_residue_gemm_supported(m, n, k) || batch < 1 || batch > 54)
+    return fail(MPMM_ERR_ARG, "residue GEMM needs m % 128 == 0, n % 256 == 0, k % 128 == 0, "
+                              "k <= 131071, 1 <= batch <= 54");
+  cudaError_t e = tc_residue_gemm(m, n, k, (int)batch, A, Bt, R, (cudaStream_t)stream);
+  return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "residue gemm launch");
+}
+
 int mpmm_exact_release(void) {
   exact_release();
   return MPMM_OK;

@@ -3,9 +3,10 @@
 // C = A*B for DD/QD device matrices, the exact product rounded once, on
 // the int8 tensor cores (ozaki.cu documents the scheme).  Per call:
 //   scans of A and B -> [first product of a shape on a stream: host sync,
-//   oz_plan] -> device-side shifts and widths -> residues -> batched int8
-//   GEMMs (cuBLASLt) -> CRT combine -> ONE host read of the status and the
-//   actual widths.
+//   oz_plan] -> device-side shifts and widths -> residues -> tcgen05
+//   residue GEMMs (tc_i8.cu: int8 MMA, TMEM accumulator, reduced mod p_t
+//   in the epilogue; cuBLASLt int32 products as the fallback) -> CRT
+//   combine -> ONE host read of the status and the actual widths.
 // A plan is cached per (device, stream, comps, m, l, n) and reused
 // speculatively; if the actual widths exceed it the product is planned
 // and recomputed, so a result is never returned from a plan that does not
@@ -15,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -161,7 +163,33 @@ struct Plan {
   }
 };
 
-int64_t pad16(int64_t x) { return (x + 15) / 16 * 16; }
+int64_t pad_to(int64_t x, int64_t q) { return (x + q - 1) / q * q; }
+
+// Padded shapes of the residue planes: the tcgen05 residue GEMM needs
+// 128-row / 256-column / 128-byte tiles; cuBLASLt (fallback) multiples of 16.
+struct Pads {
+  bool tc;
+  int64_t mp, np, lp;
+};
+
+// Measured (B200, 39 moduli): the tcgen05 kernel beats cuBLASLt's int8
+// GEMM up to 2048^3 per plane (1024^3: 46 vs 60 us), cuBLASLt is ahead from
+// 4096^3 (1.80 vs 1.69 ms): switch by the per-plane work.
+constexpr double kTcMaxWork = 2048.0 * 2048.0 * 2048.0;
+
+Pads pads_for(int64_t m, int64_t l, int64_t n) {
+  const int64_t tn = tc_residue_gemm_tile_n();
+  Pads p{false, pad_to(m, 16), pad_to(n, 16), pad_to(l, 16)};
+  static const int force = [] {
+    const char* env = std::getenv("MPMM_EXACT_GEMM");   // "tc" / "lt" (measurement knob)
+    return env == nullptr ? 0 : (env[0] == 't' ? 1 : (env[0] == 'l' ? 2 : 0));
+  }();
+  const bool small = static_cast<double>(m) * n * l <= kTcMaxWork;
+  if (force != 2 && (small || force == 1) &&
+      tc_residue_gemm_supported(pad_to(m, 128), pad_to(n, tn), pad_to(l, 128)))
+    p = Pads{true, pad_to(m, 128), pad_to(n, tn), pad_to(l, 128)};
+  return p;
+}
 
 // Device buffers of one product: scan arrays + aux, shifts, residues,
 // residue products, cuBLASLt workspace.  One cudaMallocAsync block.
@@ -174,8 +202,8 @@ struct Workspace {
   int* sh_b = nullptr;         // [nb][n]
   int8_t* ra[4] = {};
   int8_t* rb[4] = {};
-  int32_t* g[kOzMaxJobs] = {};
-  void* lt = nullptr;
+  void* g[kOzMaxJobs] = {};    // per job: uint8 residues (tc) or int32 products
+  void* lt = nullptr;           // cuBLASLt workspace (fallback path only)
   bool padded_zeroed = false;
 };
 
@@ -197,13 +225,15 @@ std::mutex g_mu;
 std::map<Key, std::unique_ptr<Entry>> g_entries;
 
 size_t workspace_bytes(const Plan& pl, int comps, int64_t m, int64_t l, int64_t n) {
-  const int64_t mp = pad16(m), np = pad16(n), lp = pad16(l);
+  const Pads P = pads_for(m, l, n);
+  const int64_t mp = P.mp, np = P.np, lp = P.lp;
+  const int64_t gel = P.tc ? 1 : 4;     // bytes per residue-product element
   size_t b = static_cast<size_t>(2 * comps * (m + n) + 16) * 4 + 256;
   b += static_cast<size_t>((pl.na * m + pl.nb * n) * 4 + 512);
   for (int x = 0; x < pl.na; ++x) b += static_cast<size_t>(pl.need_a[x] * mp * lp) + 256;
   for (int y = 0; y < pl.nb; ++y) b += static_cast<size_t>(pl.need_b[y] * np * lp) + 256;
-  for (int j = 0; j < pl.njobs; ++j) b += static_cast<size_t>(pl.jobs[j][2] * mp * np) * 4 + 256;
-  return b + kLtWorkspace;
+  for (int j = 0; j < pl.njobs; ++j) b += static_cast<size_t>(pl.jobs[j][2] * mp * np) * gel + 256;
+  return b + (P.tc ? 0 : kLtWorkspace);
 }
 
 void free_workspace(Workspace& ws, cudaStream_t s) {
@@ -228,7 +258,8 @@ cudaError_t make_workspace(Workspace& ws, const Plan* pl, int comps, int64_t m, 
   ws.el = reinterpret_cast<int*>(take(elb));
   ws.aux = ws.el + 2 * comps * (m + n);
   if (!pl) return cudaSuccess;
-  const int64_t mp = pad16(m), np = pad16(n), lp = pad16(l);
+  const Pads P = pads_for(m, l, n);
+  const int64_t mp = P.mp, np = P.np, lp = P.lp;
   ws.sh_a = reinterpret_cast<int*>(take(static_cast<size_t>(pl->na * m) * 4));
   ws.sh_b = reinterpret_cast<int*>(take(static_cast<size_t>(pl->nb * n) * 4));
   for (int x = 0; x < pl->na; ++x)
@@ -236,8 +267,8 @@ cudaError_t make_workspace(Workspace& ws, const Plan* pl, int comps, int64_t m, 
   for (int y = 0; y < pl->nb; ++y)
     ws.rb[y] = reinterpret_cast<int8_t*>(take(static_cast<size_t>(pl->need_b[y] * np * lp)));
   for (int j = 0; j < pl->njobs; ++j)
-    ws.g[j] = reinterpret_cast<int32_t*>(take(static_cast<size_t>(pl->jobs[j][2] * mp * np) * 4));
-  ws.lt = take(kLtWorkspace);
+    ws.g[j] = take(static_cast<size_t>(pl->jobs[j][2] * mp * np) * (P.tc ? 1 : 4));
+  if (!P.tc) ws.lt = take(kLtWorkspace);
   return cudaSuccess;
 }
 
@@ -257,7 +288,8 @@ cudaError_t enqueue_product(const Plan& pl, int comps, int64_t m, int64_t l, int
                             const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                             int64_t ldc, Workspace& ws, int dev, cudaStream_t s,
                             std::string* err) {
-  const int64_t mp = pad16(m), np = pad16(n), lp = pad16(l);
+  const Pads P = pads_for(m, l, n);
+  const int64_t mp = P.mp, np = P.np, lp = P.lp;
   if (ldc != n) {
     *err = "the exact mode writes a dense C (ldc == n)";
     return cudaErrorInvalidValue;
@@ -278,15 +310,21 @@ cudaError_t enqueue_product(const Plan& pl, int comps, int64_t m, int64_t l, int
   CrtJob jobs[kOzMaxJobs];
   for (int j = 0; j < pl.njobs; ++j) {
     const int* q = pl.jobs[j];
-    if (int8_gemm_batched(mp, np, lp, q[2], ws.ra[q[0]], ws.rb[q[1]], ws.g[j], ws.lt,
-                          kLtWorkspace, s, err) != 0)
+    if (P.tc) {
+      if ((e = tc_residue_gemm(mp, np, lp, q[2], ws.ra[q[0]], ws.rb[q[1]],
+                               static_cast<uint8_t*>(ws.g[j]), s)) != cudaSuccess)
+        return e;
+    } else if (int8_gemm_batched(mp, np, lp, q[2], ws.ra[q[0]], ws.rb[q[1]],
+                                 static_cast<int32_t*>(ws.g[j]), ws.lt, kLtWorkspace, s,
+                                 err) != 0) {
       return cudaErrorUnknown;
+    }
     const uint32_t* tab = nullptr;
     if ((e = device_table(dev, q[2], pl.K, &tab)) != cudaSuccess) return e;
     jobs[j] = CrtJob{ws.g[j], ws.sh_a + q[0] * m, ws.sh_b + q[1] * n, tab, q[2], pl.K, np,
                      mp * np};
   }
-  return oz_combine_launch(comps, jobs, pl.njobs, (int)m, (int)n, C, ws.aux, s);
+  return oz_combine_launch(comps, jobs, pl.njobs, (int)m, (int)n, C, ws.aux, s, P.tc);
 }
 
 }  // namespace
@@ -399,7 +437,8 @@ int exact_gemm(int comps, int64_t m, int64_t l, int64_t n, const double* A, int6
     free_workspace(scratch, s);
     en.keep = en.ws.bytes <= kKeepBytes;
   }
-  const int64_t mp = pad16(m), np = pad16(n), lp = pad16(l);
+  const Pads PD = pads_for(m, l, n);
+  const int64_t mp = PD.mp, np = PD.np, lp = PD.lp;
   auto zero_pads = [&]() -> cudaError_t {
     if (en.ws.padded_zeroed || (mp == m && np == n && lp == l)) return cudaSuccess;
     for (int x = 0; x < en.plan.na; ++x) {

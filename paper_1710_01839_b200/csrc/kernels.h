@@ -101,7 +101,7 @@ cudaError_t oz_residues_launch(int by_cols, const double* X, int64_t ld, int row
                                int8_t* R, int64_t rpitch, int64_t rplane, cudaStream_t s);
 // One CRT job of the combine (56 bytes; tensor.py / exact.cpp build them).
 struct CrtJob {
-  const int32_t* G;         // [N][.][gpitch] residue products, plane stride gplane
+  const void* G;            // [N][.][gpitch] residue products (int32) or residues (uint8)
   const int* srow;          // [m] row shifts
   const int* scol;          // [n] column shifts
   const uint32_t* table;    // [K] P limbs, then [N][K] weight limbs
@@ -111,7 +111,7 @@ struct CrtJob {
 constexpr int kOzMaxJobs = 16;
 
 cudaError_t oz_combine_launch(int comps, const void* jobs, int njobs, int m, int n, double* C,
-                              int* status, cudaStream_t s);
+                              int* status, cudaStream_t s, bool res8 = false);
 int oz_plan(int comps, int64_t m, int64_t n, int64_t l, const int* ela, const int* elb,
             int* njobs, int* jobs, int* na, int* ranges_a, int* shift_a, int* nb, int* ranges_b,
             int* shift_b);
@@ -120,6 +120,12 @@ cudaError_t oz_shifts_launch(int comps, int nranges, const int* ranges, int odim
 int int8_gemm_batched(int64_t m, int64_t n, int64_t k, int64_t batch, const int8_t* A,
                       const int8_t* Bt, int32_t* C, void* workspace, size_t ws_size,
                       cudaStream_t stream, std::string* err);
+
+// tcgen05 residue GEMMs (tc_i8.cu): R_t = (A_t * Bt_t^T) mod p_t as uint8
+bool tc_residue_gemm_supported(int64_t m, int64_t n, int64_t k);
+int tc_residue_gemm_tile_n();
+cudaError_t tc_residue_gemm(int64_t m, int64_t n, int64_t k, int batch, const int8_t* A,
+                            const int8_t* Bt, uint8_t* R, cudaStream_t s);
 
 // Keep freed stream-ordered allocations of the current device's default
 // pool mapped across synchronizations (the default threshold, 0, unmaps

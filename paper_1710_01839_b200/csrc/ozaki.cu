@@ -22,6 +22,7 @@
 // (tensor.py) reports NotRepresentable when even single components do not
 // fit.
 #include <cstdint>
+#include <type_traits>
 
 #include "kernels.h"
 
@@ -508,10 +509,21 @@ __host__ __device__ constexpr int pwords(int K) { return (K + 3) / 4 * 4; }
 // are exact in binary64 -- and any others as 32x32->64-bit integer
 // multiply-adds.  The G planes are read 8 at
 // a time (eight loads in flight).
-template <int K>
-__device__ __forceinline__ void crt_accumulate(const int32_t* G, int64_t gplane, int N,
+// address of element e of a residue plane of either representation
+template <bool RES8>
+__device__ __forceinline__ const void* elem_ptr(const void* base, int64_t e) {
+  return RES8 ? static_cast<const void*>(static_cast<const uint8_t*>(base) + e)
+              : static_cast<const void*>(static_cast<const int32_t*>(base) + e);
+}
+
+// RES8: the planes already hold r_t = G_t mod p_t as bytes (the tcgen05
+// residue GEMM reduces in its epilogue); otherwise int32 G_t, reduced here.
+template <int K, bool RES8>
+__device__ __forceinline__ void crt_accumulate(const void* Gv, int64_t gplane, int N,
                                                const uint32_t* W, uint64_t (&acc)[K + 1]) {
   constexpr int CH = 8, KD = kd_limbs(K), KE = kd_even(K), RW = row_words(K);
+  using RT = typename std::conditional<RES8, uint8_t, int32_t>::type;
+  const RT* G = static_cast<const RT*>(Gv);
   double a[KD];
 #pragma unroll
   for (int q = 0; q < KD; ++q) a[q] = 0.0;
@@ -519,10 +531,10 @@ __device__ __forceinline__ void crt_accumulate(const int32_t* G, int64_t gplane,
   for (int q = 0; q <= K; ++q) acc[q] = 0;
   for (int t0 = 0; t0 < N; t0 += CH) {
     int g[CH];
-    const int32_t* gp = G + t0 * gplane;
+    const RT* gp = G + t0 * gplane;
 #pragma unroll
     for (int u = 0; u < CH; ++u) {
-      g[u] = t0 + u < N ? __ldcs(gp) : 0;
+      g[u] = t0 + u < N ? static_cast<int>(__ldcs(gp)) : 0;
       gp += gplane;
     }
 #pragma unroll
@@ -530,7 +542,8 @@ __device__ __forceinline__ void crt_accumulate(const int32_t* G, int64_t gplane,
       const int t = t0 + u;
       if (t >= N) break;
       const unsigned p = static_cast<unsigned>(kModsDev[t]);
-      const unsigned r = barrett(static_cast<unsigned>(g[u]) + kGBias[t], kModMu[t], p);
+      const unsigned r = RES8 ? static_cast<unsigned>(g[u])
+                              : barrett(static_cast<unsigned>(g[u]) + kGBias[t], kModMu[t], p);
       const double rd = static_cast<double>(r);
       const uint32_t* row = W + t * RW;
       const double2* wd = reinterpret_cast<const double2*>(row);
@@ -663,11 +676,11 @@ __device__ __forceinline__ void stage_table(const uint32_t* __restrict__ table, 
 }
 
 // CRT reconstruction of one job's output from a staged table.
-template <int K>
-__device__ __forceinline__ bool crt_reconstruct(const int32_t* Gij, int64_t gplane, int N,
+template <int K, bool RES8>
+__device__ __forceinline__ bool crt_reconstruct(const void* Gij, int64_t gplane, int N,
                                                 const uint32_t* sW, int64_t (&mag)[K]) {
   uint64_t acc[K + 1];
-  crt_accumulate<K>(Gij, gplane, N, sW + pwords(K), acc);
+  crt_accumulate<K, RES8>(Gij, gplane, N, sW + pwords(K), acc);
   return crt_finish<K>(acc, sW, mag);
 }
 
@@ -765,7 +778,7 @@ __device__ __forceinline__ bool round_dd_fast(const int64_t (&mag)[K], bool neg,
 }
 
 // single job: one output per thread, weights from shared memory
-template <int COMPS, int K>
+template <int COMPS, int K, bool RES8>
 __global__ void __launch_bounds__(128)
 combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __restrict__ status) {
   __shared__ __align__(16) uint32_t sW[StagedTable<K>::WORDS];
@@ -775,8 +788,8 @@ combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __re
   if (e >= static_cast<int64_t>(m) * n) return;
   const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
   int64_t mag[K];
-  const bool neg = crt_reconstruct<K>(jb.G + static_cast<int64_t>(i) * jb.gpitch + j, jb.gplane,
-                                      jb.N, sW, mag);
+  const bool neg = crt_reconstruct<K, RES8>(
+      elem_ptr<RES8>(jb.G, static_cast<int64_t>(i) * jb.gpitch + j), jb.gplane, jb.N, sW, mag);
   bool bad = false;
   const int ebase = -(jb.srow[i] + jb.scol[j]);
   if constexpr (COMPS == 2) {
@@ -803,7 +816,7 @@ combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __re
 constexpr int kMTB = 128;     // threads per block
 constexpr int kMWin = 28;     // window digits (896 bits)
 
-template <int COMPS, int K>
+template <int COMPS, int K, bool RES8>
 __global__ void __launch_bounds__(kMTB)
 combine_multi_kernel(const CrtJobs jobs, int njobs, int m, int n,
                      double* __restrict__ C, int* __restrict__ status) {
@@ -824,8 +837,9 @@ combine_multi_kernel(const CrtJobs jobs, int njobs, int m, int n,
   for (int J = 0; J < njobs; ++J) {
     const CrtJob& jb = jobs.j[J];
     int64_t mag[K];
-    const bool neg = crt_reconstruct<K>(jb.G + static_cast<int64_t>(i) * jb.gpitch + j, jb.gplane,
-                                        jb.N, tabs + J * tstride, mag);
+    const bool neg = crt_reconstruct<K, RES8>(
+        elem_ptr<RES8>(jb.G, static_cast<int64_t>(i) * jb.gpitch + j), jb.gplane, jb.N,
+        tabs + J * tstride, mag);
     const int shift = -(jb.srow[i] + jb.scol[j]) - ebase;
     const int q0 = shift >> 5, r = shift & 31;
     if (q0 + K + 1 > kMWin) atomicOr(status, 2);
@@ -974,13 +988,13 @@ cudaError_t oz_residues_launch(int by_cols, const double* X, int64_t ld, int row
   }
 }
 
-template <int COMPS>
+template <int COMPS, bool RES8>
 static cudaError_t combine_single(const CrtJob& jb, int m, int n, double* C, int* status,
                                   unsigned blocks, cudaStream_t s) {
   switch (jb.K) {
 #define MPMM_K(KK) \
   case KK:         \
-    combine_single_kernel<COMPS, KK><<<blocks, 128, 0, s>>>(jb, m, n, C, status); break;
+    combine_single_kernel<COMPS, KK, RES8><<<blocks, 128, 0, s>>>(jb, m, n, C, status); break;
     MPMM_K(1) MPMM_K(2) MPMM_K(3) MPMM_K(4) MPMM_K(5) MPMM_K(6) MPMM_K(7) MPMM_K(8) MPMM_K(9)
     MPMM_K(10) MPMM_K(11) MPMM_K(12)
 #undef MPMM_K
@@ -990,7 +1004,7 @@ static cudaError_t combine_single(const CrtJob& jb, int m, int n, double* C, int
   return cudaGetLastError();
 }
 
-template <int COMPS>
+template <int COMPS, bool RES8>
 static cudaError_t combine_multi(const CrtJobs& jobs, int njobs, int K, int m, int n, double* C,
                                  int* status, unsigned blocks, cudaStream_t s) {
   const size_t smem = static_cast<size_t>(kMWin) * kMTB * sizeof(int64_t) +
@@ -999,9 +1013,10 @@ static cudaError_t combine_multi(const CrtJobs& jobs, int njobs, int K, int m, i
   switch (K) {
 #define MPMM_K(KK)                                                                            \
   case KK:                                                                                    \
-    cudaFuncSetAttribute(combine_multi_kernel<COMPS, KK>,                                     \
+    cudaFuncSetAttribute(combine_multi_kernel<COMPS, KK, RES8>,                               \
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
-    combine_multi_kernel<COMPS, KK><<<blocks, kMTB, smem, s>>>(jobs, njobs, m, n, C, status); \
+    combine_multi_kernel<COMPS, KK, RES8><<<blocks, kMTB, smem, s>>>(jobs, njobs, m, n, C,    \
+                                                                     status);                 \
     break;
     MPMM_K(1) MPMM_K(2) MPMM_K(3) MPMM_K(4) MPMM_K(5) MPMM_K(6) MPMM_K(7) MPMM_K(8) MPMM_K(9)
     MPMM_K(10) MPMM_K(11) MPMM_K(12)
@@ -1012,9 +1027,10 @@ static cudaError_t combine_multi(const CrtJobs& jobs, int njobs, int K, int m, i
   return cudaGetLastError();
 }
 
-// jobs: HOST array of njobs CrtJob records (device pointers inside)
+// jobs: HOST array of njobs CrtJob records (device pointers inside); G of
+// each job: int32 residue products, or (res8) bytes already reduced mod p_t
 cudaError_t oz_combine_launch(int comps, const void* jobs, int njobs, int m, int n, double* C,
-                              int* status, cudaStream_t s) {
+                              int* status, cudaStream_t s, bool res8) {
   int64_t total = static_cast<int64_t>(m) * n;
   if (total <= 0) return cudaSuccess;
   if (jobs == nullptr || njobs < 1 || njobs > kMaxJobs) return cudaErrorInvalidValue;
@@ -1025,14 +1041,20 @@ cudaError_t oz_combine_launch(int comps, const void* jobs, int njobs, int m, int
     if (hj[q].K != K) return cudaErrorInvalidValue;   // host pads every table to one K
   if (njobs == 1) {
     unsigned blocks = static_cast<unsigned>((total + 127) / 128);
-    return comps == 2 ? combine_single<2>(*hj, m, n, C, status, blocks, s)
-                      : combine_single<4>(*hj, m, n, C, status, blocks, s);
+    if (res8)
+      return comps == 2 ? combine_single<2, true>(*hj, m, n, C, status, blocks, s)
+                        : combine_single<4, true>(*hj, m, n, C, status, blocks, s);
+    return comps == 2 ? combine_single<2, false>(*hj, m, n, C, status, blocks, s)
+                      : combine_single<4, false>(*hj, m, n, C, status, blocks, s);
   }
   CrtJobs all{};
   for (int q = 0; q < njobs; ++q) all.j[q] = hj[q];
   unsigned blocks = static_cast<unsigned>((total + kMTB - 1) / kMTB);
-  return comps == 2 ? combine_multi<2>(all, njobs, K, m, n, C, status, blocks, s)
-                    : combine_multi<4>(all, njobs, K, m, n, C, status, blocks, s);
+  if (res8)
+    return comps == 2 ? combine_multi<2, true>(all, njobs, K, m, n, C, status, blocks, s)
+                      : combine_multi<4, true>(all, njobs, K, m, n, C, status, blocks, s);
+  return comps == 2 ? combine_multi<2, false>(all, njobs, K, m, n, C, status, blocks, s)
+                    : combine_multi<4, false>(all, njobs, K, m, n, C, status, blocks, s);
 }
 
 // per-row shifts and the bit width of each component range, from the scan
