@@ -39,8 +39,8 @@ F_QD = 796   # flops per QD multiply-add (10 DFMA, 13 DMUL, 763 DADD)
 SPEC_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 
 
-# ~0.2 ms of GPU spin before each timed step (outside the events)
-HOST_SLACK_CYCLES = 400_000
+# ~1 ms of GPU spin before each timed step (outside the events)
+HOST_SLACK_CYCLES = 2_000_000
 
 def parse():
     p = argparse.ArgumentParser(description=__doc__.splitlines()[0])

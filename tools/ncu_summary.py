@@ -28,6 +28,10 @@ KEYS = {
     "smsp__inst_executed.sum": "warp_instructions",
     "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "alu_pipe_pct",
     "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed": "fmaheavy_pipe_pct",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tensor_pipe_pct_active",
+    "sm__ops_path_tensor_op_utcimma_src_int8_sparsity_off.sum.pct_of_peak_sustained_elapsed":
+        "int8_tensor_ops_pct_of_peak",
+    "sm__ops_path_tensor_op_utcimma_src_int8_sparsity_off.sum.per_second": "int8_tensor_ops_per_s",
 }
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ms": 1e-3, "us": 1e-6,
         "ns": 1e-9, "s": 1.0}
