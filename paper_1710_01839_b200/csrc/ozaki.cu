@@ -460,22 +460,6 @@ __device__ __forceinline__ bool limbs_sub_double(int64_t (&mag)[K], double d, in
   return true;
 }
 
-// sum_q v[q] 2^(32q), rounded (top limbs first; the powers are exact
-// compile-time constants, no ldexp)
-template <int K>
-__device__ __forceinline__ double limbs_double(const uint32_t (&v)[K + 1]) {
-  double d = 0.0, scale = 1.0;
-  double sc[K + 1];
-#pragma unroll
-  for (int q = 0; q <= K; ++q) {
-    sc[q] = scale;
-    scale *= 4294967296.0;
-  }
-#pragma unroll
-  for (int q = K; q >= 0; --q) d += static_cast<double>(v[q]) * sc[q];
-  return d;
-}
-
 // p_t * floor(2^31 / p_t): added to a residue product g (|g| < 2^31 -
 // 2^14 for k <= 131071) it makes g nonnegative and below 2^32 without
 // changing g mod p_t, so one Barrett step reduces it
@@ -568,100 +552,149 @@ __device__ __forceinline__ void crt_accumulate(const void* Gv, int64_t gplane, i
   for (int q = 0; q < KD; ++q) acc[q] = static_cast<uint64_t>(a[q]);
 }
 
+// Multi-limb add/subtract on the carry flag (separate asm volatile
+// statements keep their order; nothing between them writes CC).
+__device__ __forceinline__ uint32_t add_cc(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t addc_cc(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t sub_cc(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm volatile("sub.cc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t subc_cc(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm volatile("subc.cc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t subc(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm volatile("subc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+
+// d = a - b over N limbs; returns the borrow out (1 when a < b)
+template <int N>
+__device__ __forceinline__ uint32_t sub_limbs(uint32_t (&d)[N], const uint32_t (&a)[N],
+                                              const uint32_t* b) {
+  d[0] = sub_cc(a[0], b[0]);
+#pragma unroll
+  for (int q = 1; q < N; ++q) d[q] = subc_cc(a[q], b[q]);
+  return subc(0u, 0u) & 1u;
+}
+
+// Staged CRT table head (32-bit words): P (PW), P/2 (PW), 1/P as a double
+// (+2 pad); the weight rows follow.
+__host__ __device__ constexpr int table_head(int K) { return 2 * pwords(K) + 4; }
+
 // From the accumulated sums: the centred integer X = (sum mod P) as sign +
-// K magnitude limbs.  P: K limbs.
+// K magnitude limbs.  T: staged table head.  S < N 256 P < 2^14 P, so the
+// quotient from the top limbs times 1/P is off by at most one, fixed by
+// one conditional add or subtract of P.
 template <int K>
-__device__ __forceinline__ bool crt_finish(const uint64_t (&acc)[K + 1], const uint32_t* P,
+__device__ __forceinline__ bool crt_finish(const uint64_t (&acc)[K + 1], const uint32_t* T,
                                            int64_t (&mag)[K]) {
+  constexpr int PW = pwords(K);
+  const uint32_t* P = T;
+  const uint32_t* Ph = T + PW;
+  const double invP = *reinterpret_cast<const double*>(T + 2 * PW);
   uint32_t S[K + 1];
   uint64_t carry = 0;
 #pragma unroll
   for (int q = 0; q <= K; ++q) {
-    uint64_t v = acc[q] + carry;
+    const uint64_t v = acc[q] + carry;
     S[q] = static_cast<uint32_t>(v);
     carry = v >> 32;
   }
+  double sd = 0.0, sc = 1.0;
+#pragma unroll
+  for (int q = 0; q <= K; ++q) {
+    if (q >= K - 2) sd += static_cast<double>(S[q]) * sc;   // top three limbs
+    sc *= 4294967296.0;
+  }
+  const uint32_t qv = static_cast<uint32_t>(sd * invP);
+  uint32_t L[K + 1];                 // qv * P
+  uint64_t t = 0;
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    t = static_cast<uint64_t>(qv) * P[q] + (t >> 32);
+    L[q] = static_cast<uint32_t>(t);
+  }
+  L[K] = static_cast<uint32_t>(t >> 32);
+  uint32_t X[K + 1];
+  const uint32_t neg0 = sub_limbs<K + 1>(X, S, L);   // X = S - qv P, maybe negative
   uint32_t Pl[K + 1];
 #pragma unroll
   for (int q = 0; q < K; ++q) Pl[q] = P[q];
   Pl[K] = 0;
-  double qd = floor(limbs_double<K>(S) / limbs_double<K>(Pl));
-  const uint64_t qv = qd > 0.0 ? static_cast<uint64_t>(qd) : 0ull;
-  int64_t X[K + 1];
-  int64_t borrow = 0;
+  if (neg0) {                        // X += P
+    X[0] = add_cc(X[0], Pl[0]);
 #pragma unroll
-  for (int q = 0; q <= K; ++q) {
-    uint64_t pq = static_cast<uint64_t>(Pl[q]) * qv;
-    int64_t v = static_cast<int64_t>(S[q]) - static_cast<int64_t>(pq & 0xffffffffull) + borrow;
-    borrow = (v >> 32) - static_cast<int64_t>(pq >> 32);
-    X[q] = v & 0xffffffffll;
+    for (int q = 1; q <= K; ++q) X[q] = addc_cc(X[q], Pl[q]);
+  } else {                           // X >= P ? X - P : X
+    uint32_t Y[K + 1];
+    const uint32_t lt = sub_limbs<K + 1>(Y, X, Pl);
+#pragma unroll
+    for (int q = 0; q <= K; ++q) X[q] = lt ? X[q] : Y[q];
   }
-  {  // bring X into [0, P): one correction either way
-    bool add = borrow < 0;
-    bool ge = X[K] != 0;
-    if (!add && !ge) {
-      bool decided = false;
+  // centre: X > P/2 -> -(P - X)
+  uint32_t Xk[K], D[K];
 #pragma unroll
-      for (int q = K - 1; q >= 0; --q)
-        if (!decided && X[q] != static_cast<int64_t>(Pl[q])) {
-          ge = X[q] > static_cast<int64_t>(Pl[q]);
-          decided = true;
-        }
-      if (!decided) ge = true;
-    }
-    if (add || ge) {
-      const int64_t sgn = add ? 1 : -1;
-      int64_t c = 0;
+  for (int q = 0; q < K; ++q) Xk[q] = X[q];
+  uint32_t Phl[K];
 #pragma unroll
-      for (int q = 0; q <= K; ++q) {
-        int64_t v = X[q] + sgn * static_cast<int64_t>(Pl[q]) + c;
-        c = v >> 32;
-        X[q] = v & 0xffffffffll;
-      }
-    }
-  }
-  // centre: X > P/2  ->  -(P - X)
-  bool upper = false, decided = false;
-#pragma unroll
-  for (int q = K - 1; q >= 0; --q) {
-    const uint64_t twoq = ((static_cast<uint64_t>(X[q]) << 1) & 0xffffffffull) |
-                          (q > 0 ? static_cast<uint64_t>(X[q - 1]) >> 31 : 0ull);
-    if (!decided && twoq != Pl[q]) {
-      upper = twoq > Pl[q];
-      decided = true;
-    }
-  }
-  if ((static_cast<uint64_t>(X[K - 1]) >> 31) != 0 || X[K] != 0) upper = true;
+  for (int q = 0; q < K; ++q) Phl[q] = Ph[q];
+  const bool upper = sub_limbs<K>(D, Phl, Xk) != 0;   // Ph < X
   if (upper) {
-    int64_t c = 0;
+    uint32_t Pk[K];
 #pragma unroll
-    for (int q = 0; q < K; ++q) {
-      int64_t v = static_cast<int64_t>(Pl[q]) - X[q] + c;
-      c = v >> 32;
-      mag[q] = v & 0xffffffffll;
-    }
+    for (int q = 0; q < K; ++q) Pk[q] = P[q];
+    sub_limbs<K>(D, Pk, Xk);
+#pragma unroll
+    for (int q = 0; q < K; ++q) mag[q] = D[q];
   } else {
 #pragma unroll
-    for (int q = 0; q < K; ++q) mag[q] = X[q];
+    for (int q = 0; q < K; ++q) mag[q] = Xk[q];
   }
   return upper;
 }
 
-// Shared-memory CRT table of one job: P (K uint32 limbs, padded to a
-// 16-byte multiple) then the N weight rows (layout above).
+// Shared-memory CRT table of one job: the head (P, P/2, 1/P; table_head)
+// then the N weight rows (layout above).
 template <int K>
 struct StagedTable {
-  static constexpr int WORDS = pwords(K) + row_words(K) * kNumMods;   // uint32 words
+  static constexpr int WORDS = table_head(K) + row_words(K) * kNumMods;   // uint32 words
 };
 
 template <int K>
 __device__ __forceinline__ void stage_table(const uint32_t* __restrict__ table, int N,
                                             uint32_t* sW) {
   constexpr int PW = pwords(K), RW = row_words(K), KD = kd_limbs(K), KE = kd_even(K);
-  for (int q = threadIdx.x; q < PW; q += blockDim.x) sW[q] = q < K ? table[q] : 0u;
+  constexpr int HEAD = table_head(K);
+  for (int q = threadIdx.x; q < PW; q += blockDim.x) {
+    sW[q] = q < K ? table[q] : 0u;
+    // P/2 (P is even: 256 is always the first modulus)
+    const uint32_t lo = q < K ? table[q] : 0u, hi = q + 1 < K ? table[q + 1] : 0u;
+    sW[PW + q] = (lo >> 1) | (hi << 31);
+  }
+  if (threadIdx.x == 0) {
+    double pd = 0.0, sc = 1.0;
+    for (int q = 0; q < K; ++q) {
+      pd += static_cast<double>(table[q]) * sc;
+      sc *= 4294967296.0;
+    }
+    *reinterpret_cast<double*>(sW + 2 * PW) = 1.0 / pd;
+  }
   for (int q = threadIdx.x; q < N * RW; q += blockDim.x) {
     const int row = q / RW, col = q % RW;
-    uint32_t* dst = sW + PW + row * RW;
+    uint32_t* dst = sW + HEAD + row * RW;
     const uint32_t* src = table + (row + 1) * K;
     if (col < 2 * KE) {            // double limbs, written as their two halves
       const int d = col / 2;
@@ -680,7 +713,7 @@ template <int K, bool RES8>
 __device__ __forceinline__ bool crt_reconstruct(const void* Gij, int64_t gplane, int N,
                                                 const uint32_t* sW, int64_t (&mag)[K]) {
   uint64_t acc[K + 1];
-  crt_accumulate<K, RES8>(Gij, gplane, N, sW + pwords(K), acc);
+  crt_accumulate<K, RES8>(Gij, gplane, N, sW + table_head(K), acc);
   return crt_finish<K>(acc, sW, mag);
 }
 
@@ -1008,7 +1041,7 @@ template <int COMPS, bool RES8>
 static cudaError_t combine_multi(const CrtJobs& jobs, int njobs, int K, int m, int n, double* C,
                                  int* status, unsigned blocks, cudaStream_t s) {
   const size_t smem = static_cast<size_t>(kMWin) * kMTB * sizeof(int64_t) +
-                      static_cast<size_t>(njobs) * (pwords(K) + row_words(K) * kNumMods) *
+                      static_cast<size_t>(njobs) * (table_head(K) + row_words(K) * kNumMods) *
                           sizeof(uint32_t);
   switch (K) {
 #define MPMM_K(KK)                                                                            \
