@@ -502,10 +502,10 @@ __device__ __forceinline__ const void* elem_ptr(const void* base, int64_t e) {
 
 // RES8: the planes already hold r_t = G_t mod p_t as bytes (the tcgen05
 // residue GEMM reduces in its epilogue); otherwise int32 G_t, reduced here.
-template <int K, bool RES8>
+template <int K, bool RES8, int CH>
 __device__ __forceinline__ void crt_accumulate(const void* Gv, int64_t gplane, int N,
                                                const uint32_t* W, uint64_t (&acc)[K + 1]) {
-  constexpr int CH = 8, KD = kd_limbs(K), KE = kd_even(K), RW = row_words(K);
+  constexpr int KD = kd_limbs(K), KE = kd_even(K), RW = row_words(K);
   using RT = typename std::conditional<RES8, uint8_t, int32_t>::type;
   const RT* G = static_cast<const RT*>(Gv);
   double a[KD];
@@ -708,12 +708,15 @@ __device__ __forceinline__ void stage_table(const uint32_t* __restrict__ table, 
   }
 }
 
-// CRT reconstruction of one job's output from a staged table.
-template <int K, bool RES8>
+// CRT reconstruction of one job's output from a staged table; CH residue
+// planes are loaded at a time (measured: 8 best for the register-heavy
+// single-job kernel, 16 for the multi-job one, whose occupancy is bounded
+// by its shared-memory window).
+template <int K, bool RES8, int CH = 8>
 __device__ __forceinline__ bool crt_reconstruct(const void* Gij, int64_t gplane, int N,
                                                 const uint32_t* sW, int64_t (&mag)[K]) {
   uint64_t acc[K + 1];
-  crt_accumulate<K, RES8>(Gij, gplane, N, sW + table_head(K), acc);
+  crt_accumulate<K, RES8, CH>(Gij, gplane, N, sW + table_head(K), acc);
   return crt_finish<K>(acc, sW, mag);
 }
 
@@ -870,7 +873,7 @@ combine_multi_kernel(const CrtJobs jobs, int njobs, int m, int n,
   for (int J = 0; J < njobs; ++J) {
     const CrtJob& jb = jobs.j[J];
     int64_t mag[K];
-    const bool neg = crt_reconstruct<K, RES8>(
+    const bool neg = crt_reconstruct<K, RES8, 16>(
         elem_ptr<RES8>(jb.G, static_cast<int64_t>(i) * jb.gpitch + j), jb.gplane, jb.N,
         tabs + J * tstride, mag);
     const int shift = -(jb.srow[i] + jb.scol[j]) - ebase;
