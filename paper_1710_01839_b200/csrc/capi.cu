@@ -644,7 +644,7 @@ int mpmm_oz_combine_dev(int comps, const void* jobs, int njobs, int64_t m, int64
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
   if (njobs < 1 || njobs > 16 || !dims_ok(m, 0, n)) return fail(MPMM_ERR_ARG, "bad shape");
   cudaError_t e = oz_combine_launch(comps, jobs, njobs, (int)m, (int)n, C, status,
-                                    (cudaStream_t)stream);
+                                    (cudaStream_t)stream, false, 28);
   return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "combine launch");
 }
 

@@ -119,6 +119,7 @@ cudaError_t device_table(int dev, int N, int K, const uint32_t** out) {
 
 struct Plan {
   int njobs = 0, na = 0, nb = 0, K = 0;
+  int win = 28;                // multi-job combine window digits
   int jobs[kOzMaxJobs][8];     // a_range, b_range, N, K, words_a, words_b, beta_a, beta_b
   int ranges_a[8], ranges_b[8];
   int beta_a[4], beta_b[4], words_a[4], words_b[4], need_a[4], need_b[4];
@@ -324,7 +325,7 @@ cudaError_t enqueue_product(const Plan& pl, int comps, int64_t m, int64_t l, int
     jobs[j] = CrtJob{ws.g[j], ws.sh_a + q[0] * m, ws.sh_b + q[1] * n, tab, q[2], pl.K, np,
                      mp * np};
   }
-  return oz_combine_launch(comps, jobs, pl.njobs, (int)m, (int)n, C, ws.aux, s, P.tc);
+  return oz_combine_launch(comps, jobs, pl.njobs, (int)m, (int)n, C, ws.aux, s, P.tc, pl.win);
 }
 
 }  // namespace
@@ -410,13 +411,15 @@ int exact_gemm(int comps, int64_t m, int64_t l, int64_t n, const double* A, int6
       *err = "non-finite operand: the exact tensor mode needs finite inputs";
       return 5;
     }
-    int J[kOzMaxJobs * 8], nj = 0, na = 0, nb = 0, ra[8], rb[8];
+    int J[kOzMaxJobs * 8], nj = 0, na = 0, nb = 0, ra[8], rb[8], win = 28;
     if (oz_plan(comps, m, n, l, en.el_host, en.el_host + 2 * comps * m, &nj, J, &na, ra,
-                nullptr, &nb, rb, nullptr) != 0) {
+                nullptr, &nb, rb, nullptr, &win) != 0) {
       *err = "operand dynamic range too wide for the int8 CRT scheme";
       return 4;
     }
     en.plan.from(J, nj, na, ra, nb, rb);
+    // margin for speculative reuse on data with slightly wider shift spreads
+    en.plan.win = win + 2 > 28 ? 28 : win + 2;
     en.planned = true;
     return 0;
   };
@@ -480,6 +483,19 @@ int exact_gemm(int comps, int64_t m, int64_t l, int64_t n, const double* A, int6
       return cuda_err(e);
     std::memcpy(h, en.aux_host, sizeof h);
     en.keep = en.ws.bytes <= kKeepBytes;
+  }
+  if (!(h[0] & 1) && (h[0] & 2) && en.plan.win < 28) {
+    // the planned combine window was too narrow for these shifts: widest
+    // window, same plan, recompute
+    en.plan.win = 28;
+    if ((e = enqueue_scans(comps, m, l, n, A, lda, B, ldb, en.ws, s)) != cudaSuccess ||
+        (e = enqueue_product(en.plan, comps, m, l, n, A, lda, B, ldb, C, ldc, en.ws, dev, s,
+                             err)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(en.aux_host, en.ws.aux, 9 * sizeof(int), cudaMemcpyDeviceToHost,
+                             s)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(s)) != cudaSuccess)
+      return cuda_err(e);
+    std::memcpy(h, en.aux_host, sizeof h);
   }
   if (h[0] & 1) {
     en.planned = false;

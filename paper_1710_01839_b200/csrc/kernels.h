@@ -111,10 +111,10 @@ struct CrtJob {
 constexpr int kOzMaxJobs = 16;
 
 cudaError_t oz_combine_launch(int comps, const void* jobs, int njobs, int m, int n, double* C,
-                              int* status, cudaStream_t s, bool res8 = false);
+                              int* status, cudaStream_t s, bool res8 = false, int win = 28);
 int oz_plan(int comps, int64_t m, int64_t n, int64_t l, const int* ela, const int* elb,
             int* njobs, int* jobs, int* na, int* ranges_a, int* shift_a, int* nb, int* ranges_b,
-            int* shift_b);
+            int* shift_b, int* window_digits = nullptr);
 cudaError_t oz_shifts_launch(int comps, int nranges, const int* ranges, int odim, const int* EL,
                              int* shift, int* beta, cudaStream_t s);
 int int8_gemm_batched(int64_t m, int64_t n, int64_t k, int64_t batch, const int8_t* A,

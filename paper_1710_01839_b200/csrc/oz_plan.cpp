@@ -96,7 +96,7 @@ std::vector<std::vector<std::pair<int, int>>> partitions(int comps) {
 // shift_b may be null (the device derives the shifts itself)
 int oz_plan(int comps, int64_t m, int64_t n, int64_t l, const int* ela, const int* elb,
             int* njobs, int* jobs, int* na, int* ranges_a, int* shift_a, int* nb, int* ranges_b,
-            int* shift_b) {
+            int* shift_b, int* window_digits) {
   int log_l = 1;
   while ((int64_t{1} << log_l) < l) ++log_l;
   const auto parts = partitions(comps);
@@ -177,6 +177,27 @@ int oz_plan(int comps, int64_t m, int64_t n, int64_t l, const int* ela, const in
     }
   for (int j = 0; j < q; ++j) jobs[8 * j + 3] = K;   // one limb count for the whole combine
   *njobs = q;
+  if (window_digits) {
+    // multi-job combine window: job scales differ by at most the spread of
+    // the row shifts across A's ranges plus that across B's ranges; the
+    // largest job then needs K + 1 digits above its offset, +1 for carries
+    auto spread = [&](std::vector<Range>& cache, const int* EL, int64_t od,
+                      const std::vector<std::pair<int, int>>& parts) {
+      int sp = 0;
+      for (int64_t o = 0; o < od; ++o) {
+        int lo = 1 << 30, hi = -(1 << 30);
+        for (auto r : parts) {
+          const int sh = cache[get(cache, EL, od, r.first, r.second)].shift[o];
+          lo = sh < lo ? sh : lo;
+          hi = sh > hi ? sh : hi;
+        }
+        sp = hi - lo > sp ? hi - lo : sp;
+      }
+      return sp;
+    };
+    const int bits = spread(ra_cache, ela, m, PA) + spread(rb_cache, elb, n, PB);
+    *window_digits = bits / 32 + K + 2;
+  }
   return 0;
 }
 

@@ -850,15 +850,15 @@ combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __re
 // ---------------------------------------------------------------------------
 
 constexpr int kMTB = 128;     // threads per block
-constexpr int kMWin = 28;     // window digits (896 bits)
+constexpr int kMWin = 28;     // largest window (896 bits); the host passes what a plan needs
 
 template <int COMPS, int K, bool RES8>
 __global__ void __launch_bounds__(kMTB)
-combine_multi_kernel(const CrtJobs jobs, int njobs, int m, int n,
+combine_multi_kernel(const CrtJobs jobs, int njobs, int win, int m, int n,
                      double* __restrict__ C, int* __restrict__ status) {
   extern __shared__ unsigned char smraw[];
-  int64_t* win = reinterpret_cast<int64_t*>(smraw);                   // [kMWin][kMTB]
-  uint32_t* tabs = reinterpret_cast<uint32_t*>(win + kMWin * kMTB);   // [njobs][WORDS]
+  int64_t* wbuf = reinterpret_cast<int64_t*>(smraw);                  // [win][kMTB]
+  uint32_t* tabs = reinterpret_cast<uint32_t*>(wbuf + win * kMTB);    // [njobs][WORDS]
   const int tstride = StagedTable<K>::WORDS;
   for (int J = 0; J < njobs; ++J) stage_table<K>(jobs.j[J].table, jobs.j[J].N, tabs + J * tstride);
   __syncthreads();
@@ -866,8 +866,8 @@ combine_multi_kernel(const CrtJobs jobs, int njobs, int m, int n,
   int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + tid;
   if (e >= static_cast<int64_t>(m) * n) return;
   const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
-#define WIN(q) win[(q) * kMTB + tid]
-  for (int q = 0; q < kMWin; ++q) WIN(q) = 0;
+#define WIN(q) wbuf[(q) * kMTB + tid]
+  for (int q = 0; q < win; ++q) WIN(q) = 0;
   int ebase = 1 << 30;
   for (int J = 0; J < njobs; ++J) ebase = min(ebase, -(jobs.j[J].srow[i] + jobs.j[J].scol[j]));
   for (int J = 0; J < njobs; ++J) {
@@ -878,7 +878,7 @@ combine_multi_kernel(const CrtJobs jobs, int njobs, int m, int n,
         tabs + J * tstride, mag);
     const int shift = -(jb.srow[i] + jb.scol[j]) - ebase;
     const int q0 = shift >> 5, r = shift & 31;
-    if (q0 + K + 1 > kMWin) atomicOr(status, 2);
+    if (q0 + K + 1 > win) atomicOr(status, 2);
 #pragma unroll
     for (int p = 0; p < K; ++p) {
       uint64_t v = static_cast<uint64_t>(mag[p]) << r;
@@ -887,20 +887,20 @@ combine_multi_kernel(const CrtJobs jobs, int njobs, int m, int n,
         lo = -lo;
         hi = -hi;
       }
-      if (q0 + p < kMWin) WIN(q0 + p) += lo;
-      if (q0 + p + 1 < kMWin) WIN(q0 + p + 1) += hi;
+      if (q0 + p < win) WIN(q0 + p) += lo;
+      if (q0 + p + 1 < win) WIN(q0 + p + 1) += hi;
     }
   }
   auto normalize = [&]() -> bool {
     int64_t carry = 0;
-    for (int q = 0; q < kMWin; ++q) {
+    for (int q = 0; q < win; ++q) {
       int64_t v = WIN(q) + carry;
       carry = v >> 32;
       WIN(q) = v - (carry << 32);
     }
     if (carry >= 0) return false;
     int64_t c = 1;
-    for (int q = 0; q < kMWin; ++q) {
+    for (int q = 0; q < win; ++q) {
       int64_t v = (0xffffffffll - WIN(q)) + c;
       c = v >> 32;
       WIN(q) = v & 0xffffffffll;
@@ -911,7 +911,7 @@ combine_multi_kernel(const CrtJobs jobs, int njobs, int m, int n,
   double out[COMPS];
   for (int c = 0; c < COMPS; ++c) {
     // round-to-nearest of the magnitude
-    int top = kMWin - 1;
+    int top = win - 1;
     while (top >= 0 && WIN(top) == 0) --top;
     double d = 0.0;
     if (top >= 0) {
@@ -941,7 +941,7 @@ combine_multi_kernel(const CrtJobs jobs, int njobs, int m, int n,
       int q0 = ee >> 5, rr = ee & 31;
       unsigned __int128 ww = static_cast<unsigned __int128>(mm) << rr;
       for (int u = 0; u < 3; ++u)
-        if (q0 + u < kMWin)
+        if (q0 + u < win)
           WIN(q0 + u) -= static_cast<int64_t>(static_cast<uint32_t>(ww >> (32 * u)));
     }
     neg = neg ^ normalize();
@@ -1041,9 +1041,9 @@ static cudaError_t combine_single(const CrtJob& jb, int m, int n, double* C, int
 }
 
 template <int COMPS, bool RES8>
-static cudaError_t combine_multi(const CrtJobs& jobs, int njobs, int K, int m, int n, double* C,
-                                 int* status, unsigned blocks, cudaStream_t s) {
-  const size_t smem = static_cast<size_t>(kMWin) * kMTB * sizeof(int64_t) +
+static cudaError_t combine_multi(const CrtJobs& jobs, int njobs, int K, int win, int m, int n,
+                                 double* C, int* status, unsigned blocks, cudaStream_t s) {
+  const size_t smem = static_cast<size_t>(win) * kMTB * sizeof(int64_t) +
                       static_cast<size_t>(njobs) * (table_head(K) + row_words(K) * kNumMods) *
                           sizeof(uint32_t);
   switch (K) {
@@ -1051,8 +1051,8 @@ static cudaError_t combine_multi(const CrtJobs& jobs, int njobs, int K, int m, i
   case KK:                                                                                    \
     cudaFuncSetAttribute(combine_multi_kernel<COMPS, KK, RES8>,                               \
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
-    combine_multi_kernel<COMPS, KK, RES8><<<blocks, kMTB, smem, s>>>(jobs, njobs, m, n, C,    \
-                                                                     status);                 \
+    combine_multi_kernel<COMPS, KK, RES8><<<blocks, kMTB, smem, s>>>(jobs, njobs, win, m, n,  \
+                                                                     C, status);              \
     break;
     MPMM_K(1) MPMM_K(2) MPMM_K(3) MPMM_K(4) MPMM_K(5) MPMM_K(6) MPMM_K(7) MPMM_K(8) MPMM_K(9)
     MPMM_K(10) MPMM_K(11) MPMM_K(12)
@@ -1066,7 +1066,8 @@ static cudaError_t combine_multi(const CrtJobs& jobs, int njobs, int K, int m, i
 // jobs: HOST array of njobs CrtJob records (device pointers inside); G of
 // each job: int32 residue products, or (res8) bytes already reduced mod p_t
 cudaError_t oz_combine_launch(int comps, const void* jobs, int njobs, int m, int n, double* C,
-                              int* status, cudaStream_t s, bool res8) {
+                              int* status, cudaStream_t s, bool res8, int win) {
+  win = win < 4 ? 4 : (win > kMWin ? kMWin : win);
   int64_t total = static_cast<int64_t>(m) * n;
   if (total <= 0) return cudaSuccess;
   if (jobs == nullptr || njobs < 1 || njobs > kMaxJobs) return cudaErrorInvalidValue;
@@ -1087,10 +1088,10 @@ cudaError_t oz_combine_launch(int comps, const void* jobs, int njobs, int m, int
   for (int q = 0; q < njobs; ++q) all.j[q] = hj[q];
   unsigned blocks = static_cast<unsigned>((total + kMTB - 1) / kMTB);
   if (res8)
-    return comps == 2 ? combine_multi<2, true>(all, njobs, K, m, n, C, status, blocks, s)
-                      : combine_multi<4, true>(all, njobs, K, m, n, C, status, blocks, s);
-  return comps == 2 ? combine_multi<2, false>(all, njobs, K, m, n, C, status, blocks, s)
-                    : combine_multi<4, false>(all, njobs, K, m, n, C, status, blocks, s);
+    return comps == 2 ? combine_multi<2, true>(all, njobs, K, win, m, n, C, status, blocks, s)
+                      : combine_multi<4, true>(all, njobs, K, win, m, n, C, status, blocks, s);
+  return comps == 2 ? combine_multi<2, false>(all, njobs, K, win, m, n, C, status, blocks, s)
+                    : combine_multi<4, false>(all, njobs, K, win, m, n, C, status, blocks, s);
 }
 
 // per-row shifts and the bit width of each component range, from the scan

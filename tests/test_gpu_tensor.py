@@ -104,14 +104,19 @@ def test_cfg1_every_entry_and_speed(gpu, wide):
     assert worst <= worst_ref and worst <= 1e-3
 
 
-@pytest.mark.parametrize("tok,wide", [("dd", False), ("dd", True), ("qd", False)])
+@pytest.mark.parametrize("tok,wide", [("dd", False), ("dd", True), ("qd", False),
+                                      ("qd", True)])
 def test_every_entry_correctly_rounded(gpu, tok, wide):
     """All entries (not a sample) against exact rational arithmetic: the
     DD fast rounding path (128-bit window + sticky) and the limb paths must
     both give the nearest expansion."""
     prec = mp.PrecisionSpec.parse(tok)
     m, l, n = (16, 24, 12) if tok == "dd" else (6, 8, 5)
-    a, b = inputs.gemm_inputs(tok, m, l, n, seed=11, wide=wide)
+    a, b = inputs.gemm_inputs(tok, m, l, n, seed=11, wide=wide and tok == "dd")
+    if wide and tok == "qd":       # the spec's wide set is DD-only: scale QD entries by 2^k
+        rng = np.random.default_rng(12)
+        a = np.ldexp(a, rng.integers(-30, 31, a.shape[:2])[..., None])
+        b = np.ldexp(b, rng.integers(-30, 31, b.shape[:2])[..., None])
     # cancellation-heavy rows: the remainder after hi can be tiny
     a[0, :, :] = a[1, :, :]
     a[0, ::2, :] *= -1
