@@ -101,17 +101,27 @@ __global__ void scan_rows_kernel(const double* __restrict__ X, int64_t ld, int r
 #pragma unroll
   for (int c = 0; c < NC; ++c) e[c] = kEmptyE, lo[c] = kEmptyL;
   bool bad = false;
-  for (int k = lane; k < cols; k += 32) {
-    const double* p = X + ((int64_t)r * ld + k) * NC;
+  // four k per lane per step: independent loads in flight (one warp per row
+  // leaves few warps per SM, so latency, not bandwidth, bounds this loop)
+  constexpr int U = 8;
+  for (int k0 = lane; k0 < cols; k0 += 32 * U) {
+    double v[U][NC];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const double v = p[c];
-      bad |= not_finite(v);
-      if (!is_zero(v)) {
-        e[c] = max(e[c], top_exp(v));
-        lo[c] = min(lo[c], low_bit(v));
-      }
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + 32 * u;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) v[u][c] = k < cols ? X[((int64_t)r * ld + k) * NC + c] : 0.0;
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        bad |= not_finite(v[u][c]);
+        if (!is_zero(v[u][c])) {
+          e[c] = max(e[c], top_exp(v[u][c]));
+          lo[c] = min(lo[c], low_bit(v[u][c]));
+        }
+      }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)
@@ -152,18 +162,23 @@ __global__ void scan_cols_kernel(const double* __restrict__ X, int64_t ld, int r
   bool bad = false;
   if (j < cols) {
     const int k0 = blockIdx.y * 64;
-    for (int k = k0 + ty; k < rows && k < k0 + 64; k += 8) {
-      const double* p = X + ((int64_t)k * ld + j) * NC;
+    double v[8][NC];               // the 8 rows of this thread, loads in flight together
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int k = k0 + ty + 8 * u;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) v[u][c] = k < rows ? X[((int64_t)k * ld + j) * NC + c] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
-        const double v = p[c];
-        bad |= not_finite(v);
-        if (!is_zero(v)) {
-          e[c] = max(e[c], top_exp(v));
-          lo[c] = min(lo[c], low_bit(v));
+        bad |= not_finite(v[u][c]);
+        if (!is_zero(v[u][c])) {
+          e[c] = max(e[c], top_exp(v[u][c]));
+          lo[c] = min(lo[c], low_bit(v[u][c]));
         }
       }
-    }
   }
   if (__any_sync(0xffffffffu, bad) && tx == 0) atomicOr(status, 1);
 #pragma unroll
