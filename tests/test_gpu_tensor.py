@@ -146,3 +146,17 @@ def test_graph_replay_same_operands_and_in_place_change(gpu):
     c = tensor.matmul_exact_tensors(A, B).cpu().numpy()
     for i, j in ((0, 0), (11, 9), (4, 4)):
         assert list(c[i, j]) == _rn_expansion(_exact_entry(wa, wb, i, j), 2), (i, j)
+
+
+@pytest.mark.parametrize("tok,n", [("dd", 4096), ("qd", 2048), ("dd", 1000)])
+def test_large_and_unaligned_sampled_exact(gpu, tok, n):
+    """Beyond the tcgen05 size limit (cuBLASLt residue products, DD 4096)
+    and with padded tiles (1000 is no multiple of 128/256): sampled entries
+    against the exact superaccumulator verifier; a correctly rounded
+    result uses at most ~2^-104 / (4 l 2^-104) of the bound."""
+    prec = mp.PrecisionSpec.parse(tok)
+    A, B = inputs.gemm_inputs_device(tok, n, n, n, seed=1)
+    Am, Bm = DenseMatrix(n, n, prec, A), DenseMatrix(n, n, prec, B)
+    c = matmul_exact(Am, Bm)
+    worst, _, _ = exact_bound_ratio(Am, Bm, c, samples=2000)
+    assert worst <= 1e-3, worst
