@@ -384,6 +384,188 @@ residue_gemm_persistent(const __grid_constant__ CUtensorMap map_a,
   }
 }
 
+// Cluster-pair variant for large products: the two CTAs of a cluster work
+// on row tiles 2i and 2i+1 of the same column tile, so they share its B
+// tile -- each loads one half (128 rows) by TMA multicast into both CTAs'
+// smem, halving the B traffic from L2.  A slot is free again only when
+// both CTAs' MMAs have read it: every MMA warp commits to the empty
+// barrier of BOTH CTAs (arrival count 2).
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                               int c0, int c1, int c2, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "h"(mask)
+      : "memory");
+}
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+residue_gemm_pair(const __grid_constant__ CUtensorMap map_a,
+                  const __grid_constant__ CUtensorMap map_bh, int kp, int mp, int np, int batch,
+                  int64_t plane, uint8_t* __restrict__ R) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  TcSmemP<BN>& S = *reinterpret_cast<TcSmemP<BN>*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = static_cast<int>(cluster_rank());
+  const int kblocks = kp / BK;
+  const int tn = np / BN, tmp = mp / (2 * BM);          // row-tile pairs
+  const int pairs = tn * tmp * batch;
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.empty[s], 2);           // both CTAs' MMAs
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&S.tfull[a], 1);
+      mbar_init(&S.tempty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&S.tmem_base)),
+                 "n"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();                       // the peer's barriers exist before any multicast
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = S.tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {   // TMA producer: own A tile, one half of the shared B tile
+      int it = 0;
+      for (int pr = cluster; pr < pairs; pr += nclusters) {
+        const int t = pr / (tmp * tn), rem = pr % (tmp * tn);
+        const int m0 = ((rem / tn) * 2 + rank) * BM, n0 = (rem % tn) * BN;
+        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&S.empty[s], ((it / STAGES) & 1) ^ 1);
+          mbar_expect_tx(&S.full[s], (BM + BN) * BK);
+          tma_load_3d(S.a[s], &map_a, &S.full[s], kb * BK, m0, t);
+          tma_load_3d_mc(S.b[s] + rank * (BN / 2) * BK, &map_bh, &S.full[s], kb * BK,
+                         n0 + rank * (BN / 2), t, 0x3);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {   // MMA issuer
+      constexpr uint32_t idesc = i8_idesc<BN>();
+      int it = 0, local = 0;
+      for (int pr = cluster; pr < pairs; pr += nclusters, ++local) {
+        const int acc_stage = local & 1;
+        mbar_wait(&S.tempty[acc_stage], ((local >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + acc_stage * BN;
+        for (int kb = 0; kb < kblocks; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&S.full[s], (it / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = smem_u32(S.a[s]), sb = smem_u32(S.b[s]);
+#pragma unroll
+          for (int k = 0; k < BK / UK; ++k) {
+            const uint64_t da = sw128_desc(sa + k * UK), db = sw128_desc(sb + k * UK);
+            const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          }
+          // slot s is free for the producer of either CTA once both have read it
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster"
+              ".multicast::cluster.b64 [%0], %1;" ::"r"(smem_u32(&S.empty[s])),
+              "h"(static_cast<uint16_t>(0x3))
+              : "memory");
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                smem_u32(&S.tfull[acc_stage]))
+            : "memory");
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    int local = 0;
+    for (int pr = cluster; pr < pairs; pr += nclusters, ++local) {
+      const int t = pr / (tmp * tn), rem = pr % (tmp * tn);
+      const int m0 = ((rem / tn) * 2 + rank) * BM, n0 = (rem % tn) * BN;
+      const int acc_stage = local & 1;
+      mbar_wait(&S.tfull[acc_stage], (local >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const unsigned p = static_cast<unsigned>(kTcMods[t]);
+      const unsigned mu = static_cast<unsigned>((1ull << 32) / p);
+      const unsigned bias = p * (2147483648u / p);
+      const int row = m0 + q * 32 + lane;
+      uint8_t* dst = R + static_cast<int64_t>(t) * plane + static_cast<int64_t>(row) * np + n0;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        const uint32_t taddr =
+            tmem + acc_stage * BN + (static_cast<uint32_t>(q * 32) << 16) + c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+            "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+            "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+            "[%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+              "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+              "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        uint32_t w[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          uint32_t packed = 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const unsigned x = v[4 * e + u] + bias;
+            unsigned r = x - __umulhi(x, mu) * p;
+            r = r >= p ? r - p : r;
+            packed |= r << (8 * u);
+          }
+          w[e] = packed;
+        }
+        uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
+        d4[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        d4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.tempty[acc_stage]))
+                     : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();                       // no CTA leaves while the peer may still signal it
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "n"(2 * BN));
+  }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -439,11 +621,35 @@ cudaError_t tc_residue_gemm(int64_t m, int64_t n, int64_t k, int batch, const in
   CUtensorMap ma, mb;
   if (!make_map(&ma, A, k, m, batch, BM) || !make_map(&mb, Bt, k, n, batch, kTcBN))
     return cudaErrorInvalidValue;
-  static const bool persistent = [] {
-    const char* env = std::getenv("MPMM_TC_PERSISTENT");
-    return env == nullptr || env[0] != '0';
+  static const int variant = [] {   // 0 tile, 1 persistent, 2 cluster pair (measurement knob)
+    const char* env = std::getenv("MPMM_TC_KERNEL");
+    if (env == nullptr) return -1;
+    return env[0] == 't' ? 0 : (env[0] == 'p' && env[1] == 'e' ? 1 : 2);
   }();
-  if (!persistent) {
+  // pairs need an even number of 128-row tiles; they pay off on large planes
+  const bool pair_ok = (m / BM) % 2 == 0;
+  const int use = variant >= 0 ? (variant == 2 && !pair_ok ? 1 : variant)
+                               : (pair_ok && m * n * k >= (int64_t{1} << 33) ? 2 : 1);
+  if (use == 2) {
+    CUtensorMap mbh;
+    if (!make_map(&mbh, Bt, k, n, batch, kTcBN / 2)) return cudaErrorInvalidValue;
+    const size_t smem = sizeof(TcSmemP<kTcBN>) + 1024;
+    auto kern = residue_gemm_pair<kTcBN>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+      return e;
+    const int64_t pairs = (m / (2 * BM)) * (n / kTcBN) * batch;
+    int64_t clusters = sms / 2;
+    if (pairs < clusters) clusters = pairs;
+    kern<<<static_cast<unsigned>(2 * clusters), 192, smem, s>>>(
+        ma, mbh, static_cast<int>(k), static_cast<int>(m), static_cast<int>(n), batch, m * n, R);
+    return cudaGetLastError();
+  }
+  if (use == 0) {
     const size_t smem = sizeof(TcSmem<kTcBN>) + 1024;
     auto kern = residue_gemm_kernel<kTcBN>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

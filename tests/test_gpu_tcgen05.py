@@ -31,3 +31,19 @@ def test_residue_gemm_matches_cublaslt(gpu, m, n, k, batch):
 def test_residue_gemm_rejects_bad_shapes(gpu):
     with pytest.raises(ValueError):
         _cuda.residue_gemm_dev(100, 256, 128, 1, 0, 0, 0)
+
+
+@pytest.mark.parametrize("variant", ["tile", "pair"])
+def test_residue_gemm_kernel_variants(gpu, variant):
+    """The one-tile-per-CTA kernel and the cluster-pair (B multicast) kernel,
+    forced through MPMM_TC_KERNEL in a child process, against cuBLASLt."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MPMM_TC_KERNEL=variant)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        os.path.join(root, "tests", "test_gpu_tcgen05.py"),
+                        "-k", "matches_cublaslt"], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
