@@ -315,7 +315,25 @@ int host_block_cells(int comps, const double* a, const double* b, double* c, int
   int rc = block_cells_impl(comps, n_min, cell0 - ib0 * nbc, cell1 - ib0 * nbc, rows, l, n, dA.p,
                             l, dB.p, n, dC.p, n, hs->comp);
   if (rc != MPMM_OK) return rc;
-  CU(cudaMemcpyAsync(c + r0 * n * comps, dC.p, rows * n * el, cudaMemcpyDeviceToHost, hs->comp));
+  // copy back ONLY the cells of [cell0, cell1): other threads of the
+  // caller's pool own the rest of these block rows (multiply.py:99-112)
+  auto back = [&](int64_t q0, int64_t q1, int64_t c0, int64_t c1) -> int {
+    q1 = q1 < m ? q1 : m;
+    c1 = c1 < n ? c1 : n;
+    if (q1 <= q0 || c1 <= c0) return MPMM_OK;
+    CU(cudaMemcpy2DAsync(c + (q0 * n + c0) * comps, n * el, dC.p + ((q0 - r0) * n + c0) * comps,
+                         n * el, (c1 - c0) * el, q1 - q0, cudaMemcpyDeviceToHost, hs->comp));
+    return MPMM_OK;
+  };
+  const int64_t jb0 = cell0 % nbc, jb1 = (cell1 - 1) % nbc;
+  if (ib0 == ib1) {
+    if ((rc = back(ib0 * n_min, (ib0 + 1) * n_min, jb0 * n_min, (jb1 + 1) * n_min)) != MPMM_OK)
+      return rc;
+  } else {
+    if ((rc = back(ib0 * n_min, (ib0 + 1) * n_min, jb0 * n_min, n)) != MPMM_OK) return rc;
+    if (ib1 > ib0 + 1 && (rc = back((ib0 + 1) * n_min, ib1 * n_min, 0, n)) != MPMM_OK) return rc;
+    if ((rc = back(ib1 * n_min, (ib1 + 1) * n_min, 0, (jb1 + 1) * n_min)) != MPMM_OK) return rc;
+  }
   CU(cudaStreamSynchronize(hs->comp));
   return MPMM_OK;
 }

@@ -272,3 +272,27 @@ def test_panel_split_invariance(gpu):
         got = shard.broadcast_matmul(ta, tb, n_min=32, panel_rows=panel).cpu().numpy()
         assert np.array_equal(got, ref), panel
     assert np.array_equal(ref, oracle.matmul_simple(a, b))
+
+
+@pytest.mark.parametrize("tok", ["dd", "qd"])
+def test_protocol_reentrant_from_a_thread_pool(gpu, tok):
+    """The reference drives its kernel module from a thread pool on disjoint
+    ranges (multiply.py:99-112, _run_partitioned): four host threads calling
+    the C-ABI cell and row kernels concurrently give the serial result."""
+    from concurrent.futures import ThreadPoolExecutor
+    m, l, n = 70, 53, 66
+    a, b = inputs.gemm_inputs(tok, m, l, n, seed=41)
+    kern = backend.kernels()
+    want = oracle.matmul_simple(a, b)
+    n_min = 8
+    cells = (-(-m // n_min)) * (-(-n // n_min))
+    bounds = [(q * cells // 4, (q + 1) * cells // 4) for q in range(4)]
+    c = np.zeros_like(want)
+    with ThreadPoolExecutor(4) as pool:
+        list(pool.map(lambda r: getattr(kern, f"{tok}_block_cells")(a, b, c, n_min, *r), bounds))
+    assert np.array_equal(c, want)
+    rows = [(q * m // 4, (q + 1) * m // 4) for q in range(4)]
+    c2 = np.zeros_like(want)
+    with ThreadPoolExecutor(4) as pool:
+        list(pool.map(lambda r: getattr(kern, f"{tok}_simple_rows")(a, b, c2, *r), rows))
+    assert np.array_equal(c2, want)
