@@ -335,6 +335,21 @@ int exact_gemm(int comps, int64_t m, int64_t l, int64_t n, const double* A, int6
                const double* B, int64_t ldb, double* C, int64_t ldc, cudaStream_t s,
                std::string* err) {
   if (m == 0 || n == 0) return 0;
+  if (l == 0) {                    // empty inner dimension: C = 0
+    for (int64_t i = 0; i < m; ++i) {
+      const cudaError_t ce = cudaMemsetAsync(C + i * ldc * comps, 0, n * comps * sizeof(double), s);
+      if (ce != cudaSuccess) {
+        *err = cudaGetErrorString(ce);
+        return 2;
+      }
+    }
+    const cudaError_t ce = cudaStreamSynchronize(s);
+    if (ce != cudaSuccess) {
+      *err = cudaGetErrorString(ce);
+      return 2;
+    }
+    return 0;
+  }
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) {

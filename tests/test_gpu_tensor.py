@@ -160,3 +160,24 @@ def test_large_and_unaligned_sampled_exact(gpu, tok, n):
     c = matmul_exact(Am, Bm)
     worst, _, _ = exact_bound_ratio(Am, Bm, c, samples=2000)
     assert worst <= 1e-3, worst
+
+
+def test_nonfinite_and_empty(gpu):
+    import torch
+    from paper_1710_01839_b200 import tensor
+    from paper_1710_01839_b200.errors import RangeError
+    a, b = inputs.gemm_inputs("dd", 9, 7, 5, seed=3)
+    a[2, 3, 0] = np.inf
+    with pytest.raises(RangeError):
+        tensor.matmul_exact_tensors(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    b[1, 1, 1] = np.nan
+    a[2, 3, 0] = 1.0
+    with pytest.raises(RangeError):
+        tensor.matmul_exact_tensors(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    z = tensor.matmul_exact_tensors(torch.zeros((4, 0, 2), dtype=torch.float64, device="cuda"),
+                                    torch.zeros((0, 3, 2), dtype=torch.float64, device="cuda"))
+    assert z.shape == (4, 3, 2) and not z.any()
+    # after the errors the same shapes work again
+    a, b = inputs.gemm_inputs("dd", 9, 7, 5, seed=4)
+    c = tensor.matmul_exact_tensors(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    assert list(c.cpu().numpy()[0, 0]) == _rn_expansion(_exact_entry(a, b, 0, 0), 2)
