@@ -296,3 +296,38 @@ def test_protocol_reentrant_from_a_thread_pool(gpu, tok):
     with ThreadPoolExecutor(4) as pool:
         list(pool.map(lambda r: getattr(kern, f"{tok}_simple_rows")(a, b, c2, *r), rows))
     assert np.array_equal(c2, want)
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (1, 300, 1), (300, 1, 2), (2, 3, 300)])
+@pytest.mark.parametrize("prec", [DD, QD])
+def test_degenerate_shapes(gpu, shape, prec):
+    """Thin and single-element products on every entry point, bit for bit."""
+    m, l, n = shape
+    a, b = inputs.gemm_inputs("dd" if prec is DD else "qd", m, l, n, seed=6)
+    want = oracle.matmul_simple(a, b)
+    A, B = M(a, prec), M(b, prec)
+    for c in (mp.matmul_simple(A, B), mp.matmul_block(A, B, 4),
+              mp.matmul_block(A.to_device(), B.to_device(), 64).to_host()):
+        assert np.array_equal(c.data, want)
+    if m == l == n:
+        assert np.array_equal(mp.matmul_strassen(A, B, 2, 2).data, want)
+
+
+@pytest.mark.parametrize("shape", [(0, 5, 3), (4, 0, 3), (4, 5, 0)])
+def test_empty_shapes(gpu, shape):
+    """The drop-in API rejects empty matrices like the reference
+    (matrix.py: ShapeError); the C ABI accepts them: C untouched when
+    m or n is 0, zeros when l is 0."""
+    import torch
+    m, l, n = shape
+    with pytest.raises(mp.ShapeError):
+        M(np.zeros((m, l, 2)), DD) if m * l == 0 else M(np.zeros((l, n, 2)), DD)
+    A = torch.zeros((m, l, 2), dtype=torch.float64, device="cuda")
+    B = torch.zeros((l, n, 2), dtype=torch.float64, device="cuda")
+    C = torch.full((m, n, 2), 7.0, dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    for algo in (_cuda.ALGO_SIMPLE, _cuda.ALGO_BLOCK):
+        _cuda.gemm_dev(2, algo, 16, m, l, n, A.data_ptr(), max(l, 1), B.data_ptr(), max(n, 1),
+                       C.data_ptr(), max(n, 1), False, None, s)
+        torch.cuda.synchronize()
+        assert (C == 0).all() if l == 0 else (C == 7).all()
