@@ -105,9 +105,9 @@ def load():
     if _load_error is not None:
         raise DeviceError(_load_error)
     if not os.path.exists(LIB_PATH):
-        _load_error = (f"CUDA extension not built: {LIB_PATH} is missing "
-                       "(run `python -c 'import __graft_entry__ as g; g.build()'`)")
-        raise DeviceError(_load_error)
+        # not cached: build() may produce the library later in this process
+        raise DeviceError(f"CUDA extension not built: {LIB_PATH} is missing "
+                          "(run `python -c 'import __graft_entry__ as g; g.build()'`)")
     try:
         lib = ctypes.CDLL(LIB_PATH)
     except OSError as ex:
