@@ -39,8 +39,11 @@ F_QD = 796   # flops per QD multiply-add (10 DFMA, 13 DMUL, 763 DADD)
 SPEC_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
 
 
-# ~1 ms of GPU spin before each timed step (outside the events)
-HOST_SLACK_CYCLES = 2_000_000
+# ~5 ms of GPU spin before each timed step (outside the events): the host
+# enqueue of a step (plus the clock sampler's nvidia-smi forks competing
+# for the host) must finish before the device reaches the start event, or
+# host time leaks into the device-timed step (seen with 1 ms: +0.7 ms/step)
+HOST_SLACK_CYCLES = 10_000_000
 
 def parse():
     p = argparse.ArgumentParser(description=__doc__.splitlines()[0])

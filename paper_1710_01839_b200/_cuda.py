@@ -22,7 +22,8 @@ from .errors import DeviceError, ShapeError
 NAME = "cuda"
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmpmm_cuda.so")
+# MPMM_LIB_PATH: load a variant build instead (tools/ experiments only)
+LIB_PATH = os.environ.get("MPMM_LIB_PATH") or os.path.join(_HERE, "libmpmm_cuda.so")
 
 _lib = None
 _load_error = None

@@ -28,6 +28,41 @@ __device__ __forceinline__ double two_sum(double a, double b, double& err) {
   return s;
 }
 
+// TwoSum through magnitude order: s = fl(a + b) and the same exact error
+// as two_sum, in 3 DADD instead of 6.  With t the operand of larger
+// magnitude and u the other, t - s is exact (Sterbenz) and (t - s) + u is
+// the exact a + b - s (Fast2Sum, Dekker 1971), the unique value two_sum
+// also returns -- so every later rounding sees the same operand.  The
+// sign of a zero error matches too: two_sum's error is never -0.0, and
+// (t - s) + u is -0.0 only if t - s = -0.0, i.e. t = -0.0 with s = +0.0,
+// which |u| <= |t| rules out.
+//
+// The order test costs no FP64 pipe time: the high words of a and b
+// (sign, 11 exponent bits, 20 mantissa bits), read as float32 bit patterns
+// under |.|, compare like the magnitudes of the doubles whenever their
+// exponent fields are below 0x7f8 (|x| < 2^1017; the reference's own
+// TwoProd guard is 2^996, eft.py:21) -- one FSETP on the FP32 side plus
+// four SELs on the ALU pipe.  Equal high words mean equal exponents, for
+// which either order is exact (float32 subnormal patterns, i.e. doubles
+// below 2^-1015, compare exactly too: no -ftz).
+__device__ __forceinline__ double two_sum_ord(double a, double b, double& err) {
+  double s = a + b;
+  const float fa = __int_as_float(__double2hiint(a));
+  const float fb = __int_as_float(__double2hiint(b));
+  const bool ge = fabsf(fa) >= fabsf(fb);
+  const double t = ge ? a : b;
+  const double u = ge ? b : a;
+  err = (t - s) + u;
+  return s;
+}
+
+// Either TwoSum, chosen at compile time (both bit-identical; see above).
+template <bool ORD>
+__device__ __forceinline__ double two_sum_t(double a, double b, double& err) {
+  if constexpr (ORD) return two_sum_ord(a, b, err);
+  else return two_sum(a, b, err);
+}
+
 // eft.py:33-36 _quick_two_sum_raw
 __device__ __forceinline__ double quick_two_sum(double a, double b, double& err) {
   double s = a + b;
@@ -46,12 +81,13 @@ __device__ __forceinline__ double two_prod(double a, double b, double& err) {
 // double-double
 // ---------------------------------------------------------------------------
 
-// ddqd.py:63-70 dd_add == _kernels.pyx:189-204 (20 DADD)
+// ddqd.py:63-70 dd_add == _kernels.pyx:189-204 (20 DADD; 14 when ORD)
+template <bool ORD = false>
 __device__ __forceinline__ void dd_add(double xh, double xl, double yh, double yl,
                                        double& hi, double& lo) {
   double s2, t2, e;
-  double s1 = two_sum(xh, yh, s2);
-  double t1 = two_sum(xl, yl, t2);
+  double s1 = two_sum_t<ORD>(xh, yh, s2);
+  double t1 = two_sum_t<ORD>(xl, yl, t2);
   s2 = s2 + t1;
   s1 = quick_two_sum(s1, s2, e);
   s2 = e + t2;
@@ -59,7 +95,8 @@ __device__ __forceinline__ void dd_add(double xh, double xl, double yh, double y
 }
 
 // ddqd.py:77-91 dd_mul, as inlined at _kernels.pyx:140-171
-// (4 DMUL + 3 DFMA + 23 DADD).
+// (4 DMUL + 3 DFMA + 23 DADD; 17 DADD when ORD).
+template <bool ORD = false>
 __device__ __forceinline__ void dd_mul(double ah, double al, double bh, double bl,
                                        double& ph, double& pl) {
   double e, e1, e2, r1, r2, w;
@@ -67,8 +104,8 @@ __device__ __forceinline__ void dd_mul(double ah, double al, double bh, double b
   double p1 = two_prod(ah, bl, e1);
   double p2 = two_prod(al, bh, e2);
   double tail = (e1 + e2) + al * bl;
-  double s = two_sum(p1, p2, r1);
-  s = two_sum(e, s, r2);
+  double s = two_sum_t<ORD>(p1, p2, r1);
+  s = two_sum_t<ORD>(e, s, r2);
   double losum = (r1 + r2) + tail;
   double h = quick_two_sum(p, s, w);
   w = w + losum;
@@ -76,12 +113,15 @@ __device__ __forceinline__ void dd_mul(double ah, double al, double bh, double b
 }
 
 // One DD multiply-add, the k-loop body of _kernels.pyx:135-184:
-// c <- dd_add(c, dd_mul(a, b)).  50 FP64 instructions, 53 flops.
+// c <- dd_add(c, dd_mul(a, b)).  50 FP64 instructions, 53 flops; with
+// ORD the four TwoSums run as two_sum_ord: 38 FP64 instructions (4 DMUL +
+// 3 DFMA + 31 DADD) + 4 FSETP + 16 SEL, same bits.
+template <bool ORD = false>
 __device__ __forceinline__ void dd_madd(double& ch, double& cl, double ah, double al,
                                         double bh, double bl) {
   double ph, pl;
-  dd_mul(ah, al, bh, bl, ph, pl);
-  dd_add(ch, cl, ph, pl, ch, cl);
+  dd_mul<ORD>(ah, al, bh, bl, ph, pl);
+  dd_add<ORD>(ch, cl, ph, pl, ch, cl);
 }
 
 // Faithful ("fast") DD multiply-add -- NOT the reference's sequence, an
@@ -171,7 +211,12 @@ __device__ __forceinline__ void renorm5(double x0, double x1, double x2, double 
 // therefore sees exactly the operands of the sequential loop
 // (ddqd.py:181-186) -- same bits -- while each round holds up to four
 // independent TwoSums, so in-order issue is not stalled by the pass chains.
-template <int N>
+//
+// ORDMASK bit p runs pass p's TwoSums as two_sum_ord (same bits, half the
+// DADDs, the order test on the FP32/ALU pipes): a knob to balance the FP64
+// pipe against the ALU pipe, which the QD multiply-add loads with its zero
+// tests and selects.
+template <int N, int ORDMASK = 0>
 __device__ __forceinline__ void compress4_dense(double (&v)[N], double out[4]) {
   double s[4];
 #pragma unroll
@@ -181,7 +226,10 @@ __device__ __forceinline__ void compress4_dense(double (&v)[N], double out[4]) {
       const int i = d - 2 * p;
       if (i >= 1 && i <= N - 1) {
         if (i == 1) s[p] = v[0];
-        s[p] = two_sum(s[p], v[i], v[i - 1]);
+        if ((ORDMASK >> p) & 1)
+          s[p] = two_sum_ord(s[p], v[i], v[i - 1]);
+        else
+          s[p] = two_sum(s[p], v[i], v[i - 1]);
         if (i == N - 1) v[N - 1] = s[p];
       }
     }
@@ -244,6 +292,9 @@ __device__ __forceinline__ void compress4_slow(const double (&v)[N], double out[
 }
 
 // _kernels.pyx:311-341 _qd_mul_add: cc += x*y, bit-identical.
+// M23 / M8: ORDMASKs of the product's 23-term and the accumulate's 8-term
+// compressions (see compress4_dense).
+template <int M23 = 0, int M8 = 0>
 __device__ __forceinline__ void qd_mul_add(double cc[4], const double x[4], const double y[4]) {
   double t[23];
   t[0] = two_prod(x[0], y[0], t[1]);
@@ -264,7 +315,7 @@ __device__ __forceinline__ void qd_mul_add(double cc[4], const double x[4], cons
   for (int i = 0; i < 23; ++i) dense &= nonzero(t[i]);
   double prod[4];
   if (dense) {
-    compress4_dense<23>(t, prod);
+    compress4_dense<23, M23>(t, prod);
   } else {
     compress4_slow<23>(t, prod);
   }
@@ -273,7 +324,7 @@ __device__ __forceinline__ void qd_mul_add(double cc[4], const double x[4], cons
   bool pd = nonzero(prod[0]) & nonzero(prod[1]) & nonzero(prod[2]) & nonzero(prod[3]);
   bool cd = nonzero(cc[0]) & nonzero(cc[1]) & nonzero(cc[2]) & nonzero(cc[3]);
   if (cd & pd) {
-    compress4_dense<8>(add, cc);
+    compress4_dense<8, M8>(add, cc);
   } else if (cz & pd) {
     // filtered term list is exactly prod[0..3] (k = 0 of every product)
     double p4[4] = {prod[0], prod[1], prod[2], prod[3]};
