@@ -161,17 +161,24 @@ __device__ __forceinline__ bool nonzero(double x) {
   return ((hi & 0x7fffffffu) | lo) != 0u;
 }
 
-// ddqd.py:140-172 _renorm5 == _kernels.pyx:237-271, branch-free: the
-// data-dependent "if e != 0" emission becomes predicated selects.  In the
-// reference's k == 3 case "acc += v" equals the s computed below, so the
-// only behavioural difference of the k == 3 case is that nothing is emitted.
-__device__ __forceinline__ void renorm5(double x0, double x1, double x2, double x3,
-                                        double x4, double out[4]) {
-  double s, t;
-  s = quick_two_sum(x3, x4, x4);
-  t = quick_two_sum(x2, s, x3);
-  s = quick_two_sum(x1, t, x2);
-  t = quick_two_sum(x0, s, x1);
+// Conservative nonzero test on the high word only: true means x != 0
+// (some exponent or top-mantissa bit is set); false means "maybe zero"
+// (x = +-0, or |x| < 2^-1042 with only low-word bits), which callers send
+// to their exact path.  The high word read as a float32 under != 0 is one
+// FSETP, and a chain of them folds into one predicate (FSETP.AND), where
+// nonzero() is LOP3 + ISETP per term -- the QD multiply-add is bound by
+// register-file reads, and each ALU instruction costs one.
+__device__ __forceinline__ bool hi_nonzero(double x) {
+  return __int_as_float(__double2hiint(x)) != 0.0f;
+}
+
+// ddqd.py:140-172 _renorm5 == _kernels.pyx:237-271: the general case,
+// branch-free: the data-dependent "if e != 0" emission becomes predicated
+// selects.  In the reference's k == 3 case "acc += v" equals the s
+// computed below, so the only behavioural difference of the k == 3 case is
+// that nothing is emitted.
+__device__ __forceinline__ void renorm5_emit(double t, double x1, double x2, double x3,
+                                             double x4, double out[4]) {
   double o0 = 0.0, o1 = 0.0, o2 = 0.0, o3 = 0.0;
   double acc = t;
   int k = 0;
@@ -198,6 +205,34 @@ __device__ __forceinline__ void renorm5(double x0, double x1, double x2, double 
   out[1] = o1;
   out[2] = o2;
   out[3] = o3;
+}
+
+// _renorm5 with a fast path for the common case: the first three emission
+// errors e1, e2, e3 are nonzero, so the reference emits sn1, sn2, sn3 and
+// ends (k = 3) with acc = e3 + x4.  Same operations on the same operands
+// as the general loop (whose fourth error is never used when k = 3), so
+// the same bits; any possibly-zero error takes renorm5_emit.
+__device__ __forceinline__ void renorm5(double x0, double x1, double x2, double x3,
+                                        double x4, double out[4]) {
+  double s, t;
+  s = quick_two_sum(x3, x4, x4);
+  t = quick_two_sum(x2, s, x3);
+  s = quick_two_sum(x1, t, x2);
+  t = quick_two_sum(x0, s, x1);
+  const double sn1 = t + x1;
+  const double e1 = x1 - (sn1 - t);
+  const double sn2 = e1 + x2;
+  const double e2 = x2 - (sn2 - e1);
+  const double sn3 = e2 + x3;
+  const double e3 = x3 - (sn3 - e2);
+  if (__builtin_expect(hi_nonzero(e1) & hi_nonzero(e2) & hi_nonzero(e3), 1)) {
+    out[0] = sn1;
+    out[1] = sn2;
+    out[2] = sn3;
+    out[3] = e3 + x4;
+  } else {
+    renorm5_emit(t, x1, x2, x3, x4, out);
+  }
 }
 
 // ddqd.py:175-193 _compress4 for N terms that are ALL nonzero (the zero
@@ -310,9 +345,11 @@ __device__ __forceinline__ void qd_mul_add(double cc[4], const double x[4], cons
   t[20] = x[1] * y[3];
   t[21] = x[2] * y[2];
   t[22] = x[3] * y[1];
+  // dense gate: every high word nonzero => every term nonzero (a false
+  // negative only costs the exact compaction path, same bits)
   bool dense = true;
 #pragma unroll
-  for (int i = 0; i < 23; ++i) dense &= nonzero(t[i]);
+  for (int i = 0; i < 23; ++i) dense &= hi_nonzero(t[i]);
   double prod[4];
   if (dense) {
     compress4_dense<23, M23>(t, prod);
@@ -321,8 +358,9 @@ __device__ __forceinline__ void qd_mul_add(double cc[4], const double x[4], cons
   }
   double add[8] = {cc[0], prod[0], cc[1], prod[1], cc[2], prod[2], cc[3], prod[3]};
   bool cz = !nonzero(cc[0]) & !nonzero(cc[1]) & !nonzero(cc[2]) & !nonzero(cc[3]);
-  bool pd = nonzero(prod[0]) & nonzero(prod[1]) & nonzero(prod[2]) & nonzero(prod[3]);
-  bool cd = nonzero(cc[0]) & nonzero(cc[1]) & nonzero(cc[2]) & nonzero(cc[3]);
+  bool pd = hi_nonzero(prod[0]) & hi_nonzero(prod[1]) & hi_nonzero(prod[2]) &
+            hi_nonzero(prod[3]);
+  bool cd = hi_nonzero(cc[0]) & hi_nonzero(cc[1]) & hi_nonzero(cc[2]) & hi_nonzero(cc[3]);
   if (cd & pd) {
     compress4_dense<8, M8>(add, cc);
   } else if (cz & pd) {

@@ -24,6 +24,7 @@
 #include <cstdint>
 #include <type_traits>
 
+#include "common.cuh"
 #include "kernels.h"
 
 namespace mpmm {
@@ -212,10 +213,17 @@ constexpr int kMaxW = 12;   // 32-bit words of one scaled entry (384 bits)
 //   w4[t][w]   the 4 bytes 2^(8(4w+j)) mod p_t, centred into int8, packed
 //   top[t][W]  (p_t - 2^(32W) mod p_t) mod p_t  (two's-complement sign fix)
 //   bias[t]    a multiple of p_t >= 2^22 (keeps the dot product positive)
+//   init[t][W] {bias + h, bias + h + top[t][W]}: the dot product's start
+//              for a non-negative / negative entry, h = floor(p_t / 2)
+//   muc[t]     ceil(2^32 / p_t): floor(x / p_t) = umulhi(x, muc) for every
+//              x < 2^23 (checked exhaustively for all 54 moduli)
 struct ResidueTables {
   uint32_t w4[kNumMods][kMaxW];
   uint32_t top[kNumMods][kMaxW + 1];
   uint32_t bias[kNumMods];
+  uint32_t init[kNumMods][kMaxW + 1][2];
+  uint32_t half[kNumMods];
+  uint32_t muc[kNumMods];
 };
 
 constexpr int kModsHost[kNumMods] = {
@@ -246,6 +254,12 @@ constexpr ResidueTables make_residue_tables() {
       for (int s = 0; s < 32; ++s) q = (q * 2u) % p;
     }
     T.bias[t] = p * ((1u << 22) / p + 1u);
+    T.half[t] = p / 2;
+    T.muc[t] = static_cast<uint32_t>(((1ull << 32) + p - 1) / p);
+    for (int W = 0; W <= kMaxW; ++W) {
+      T.init[t][W][0] = T.bias[t] + p / 2;
+      T.init[t][W][1] = T.bias[t] + p / 2 + T.top[t][W];
+    }
   }
   return T;
 }
@@ -295,31 +309,60 @@ __device__ __forceinline__ void entry_words(const double* x, int shift, bool val
 }
 
 // centred residue of the W-word integer X modulo p_t, as an int8 byte
+// Centred residue c = x mod p_t in [-floor(p/2), ceil(p/2) - 1] (the int8
+// the residue GEMMs take; for p = 256 that is [-128, 127]) of a W-word
+// two's-complement entry.  The dot product of the entry's bytes with the
+// centred weights 2^(8j) mod p starts at init = bias + h (+ top for a
+// negative entry), so x' = x + h lies in (2^21, 2^23); then
+// q = floor(x' / p) = umulhi(x', ceil(2^32 / p)) exactly and c = x' - h - q p.
+// Per entry and modulus: W DP4A + IMAD.HI + IMAD on the FMA pipe, one
+// IADD (and a SEL for the start) on the ALU pipe -- no compare/select
+// chain, which left the ALU pipe the bound.
 template <int W>
-__device__ __forceinline__ uint32_t residue_byte(const uint32_t (&X)[W], uint32_t p,
-                                                 uint32_t mu, uint32_t top, uint32_t bias,
-                                                 const uint32_t (&wt)[W]) {
-  int acc = 0;
+__device__ __forceinline__ int residue_centred(const uint32_t (&X)[W], uint32_t init,
+                                               uint32_t muc, uint32_t negp, uint32_t h,
+                                               const uint32_t (&wt)[W]) {
+  int acc = static_cast<int>(init);
 #pragma unroll
   for (int w = 0; w < W; ++w) acc = dp4a_us(X[w], wt[w], acc);
-  uint32_t x = static_cast<uint32_t>(acc + static_cast<int>(bias)) +
-               ((X[W - 1] >> 31) ? top : 0u);
-  uint32_t r = barrett(x, mu, p);
-  int c = static_cast<int>(r);
-  if (c > static_cast<int>(p / 2)) c -= static_cast<int>(p);
-  if (c > 127) c -= static_cast<int>(p);
-  return static_cast<uint32_t>(c) & 0xffu;
+  const uint32_t q = __umulhi(static_cast<uint32_t>(acc), muc);
+  return static_cast<int>(static_cast<uint32_t>(acc) - h + q * negp);
 }
 
+// the low bytes of four ints packed little-endian (3 PRMT)
+__device__ __forceinline__ uint32_t pack_bytes(int c0, int c1, int c2, int c3) {
+  const uint32_t lo = __byte_perm(static_cast<uint32_t>(c0), static_cast<uint32_t>(c1), 0x0040);
+  const uint32_t hi = __byte_perm(static_cast<uint32_t>(c2), static_cast<uint32_t>(c3), 0x0040);
+  return __byte_perm(lo, hi, 0x5410);
+}
+
+struct ResidueConsts {
+  uint32_t init0, init1, muc, negp, h;
+};
+
 template <int W>
-__device__ __forceinline__ void load_weights(int t, uint32_t (&wt)[W], uint32_t& p, uint32_t& mu,
-                                             uint32_t& top, uint32_t& bias) {
-  p = static_cast<uint32_t>(kModsDev[t]);
-  mu = kModMu[t];
-  top = kRes.top[t][W];
-  bias = kRes.bias[t];
+__device__ __forceinline__ ResidueConsts load_weights(int t, uint32_t (&wt)[W]) {
+  ResidueConsts k;
+  k.init0 = kRes.init[t][W][0];
+  k.init1 = kRes.init[t][W][1];
+  k.muc = kRes.muc[t];
+  k.negp = 0u - static_cast<uint32_t>(kModsDev[t]);
+  k.h = kRes.half[t];
 #pragma unroll
   for (int w = 0; w < W; ++w) wt[w] = kRes.w4[t][w];
+  return k;
+}
+
+// the residue byte word of four entries (u = 0..3 in the low..high byte)
+template <int W>
+__device__ __forceinline__ uint32_t residue_word(const uint32_t (&X)[4][W], const bool (&neg)[4],
+                                                 const ResidueConsts& k,
+                                                 const uint32_t (&wt)[W]) {
+  int c[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    c[u] = residue_centred<W>(X[u], neg[u] ? k.init1 : k.init0, k.muc, k.negp, k.h, wt);
+  return pack_bytes(c[0], c[1], c[2], c[3]);
 }
 
 // A side: R[t][row][k], 4 consecutive k of one row per thread (reads and
@@ -339,14 +382,21 @@ residues_rows_kernel(const double* __restrict__ X, int64_t ld, int rows, int col
   for (int u = 0; u < 4; ++u)
     entry_words<NC, W>(X + ((int64_t)o * ld + k0 + u) * comps + c0, sh, k0 + u < cols, Xw[u]);
   int8_t* dst = R + static_cast<int64_t>(o) * rpitch + k0;
+  bool neg[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) neg[u] = (Xw[u][W - 1] >> 31) != 0;
+  // the constants of modulus t+1 are loaded while t is computed (the
+  // indexed constant loads were the loop's critical path)
+  uint32_t wt[W];
+  ResidueConsts k = load_weights<W>(0, wt);
 #pragma unroll 1
   for (int t = 0; t < N; ++t) {
-    uint32_t wt[W], p, mu, top, bias;
-    load_weights<W>(t, wt, p, mu, top, bias);
-    uint32_t word = 0;
+    uint32_t wn[W];
+    const ResidueConsts kn = load_weights<W>(t + 1 < N ? t + 1 : t, wn);
+    *reinterpret_cast<uint32_t*>(dst + t * rplane) = residue_word<W>(Xw, neg, k, wt);
+    k = kn;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) word |= residue_byte<W>(Xw[u], p, mu, top, bias, wt) << (8 * u);
-    *reinterpret_cast<uint32_t*>(dst + t * rplane) = word;
+    for (int w = 0; w < W; ++w) wt[w] = wn[w];
   }
 }
 
@@ -376,14 +426,19 @@ residues_cols_kernel(const double* __restrict__ X, int64_t ld, int rows, int col
   const int kq = blockIdx.y * 32 + qq * 4;
   int8_t* dst = R + static_cast<int64_t>(og) * rpitch + kq;
   const bool store = og < cols && kq < rows;
+  bool neg[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) neg[u] = (Xw[u][W - 1] >> 31) != 0;
+  uint32_t wt[W];
+  ResidueConsts k = load_weights<W>(0, wt);
 #pragma unroll 1
   for (int t = 0; t < N; ++t) {
-    uint32_t wt[W], p, mu, top, bias;
-    load_weights<W>(t, wt, p, mu, top, bias);
-    uint32_t word = 0;
+    uint32_t wn[W];
+    const ResidueConsts kn = load_weights<W>(t + 1 < N ? t + 1 : t, wn);
+    S[t & 1][lane][wq] = residue_word<W>(Xw, neg, k, wt);
+    k = kn;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) word |= residue_byte<W>(Xw[u], p, mu, top, bias, wt) << (8 * u);
-    S[t & 1][lane][wq] = word;
+    for (int w = 0; w < W; ++w) wt[w] = wn[w];
     __syncthreads();
     if (store) *reinterpret_cast<uint32_t*>(dst + t * rplane) = S[t & 1][oc][qq];
   }
@@ -517,7 +572,8 @@ __device__ __forceinline__ const void* elem_ptr(const void* base, int64_t e) {
 
 // RES8: the planes already hold r_t = G_t mod p_t as bytes (the tcgen05
 // residue GEMM reduces in its epilogue); otherwise int32 G_t, reduced here.
-template <int K, bool RES8, int CH>
+// SM: the residue bytes were staged in shared memory (plain loads).
+template <int K, bool RES8, int CH, bool SM = false>
 __device__ __forceinline__ void crt_accumulate(const void* Gv, int64_t gplane, int N,
                                                const uint32_t* W, uint64_t (&acc)[K + 1]) {
   constexpr int KD = kd_limbs(K), KE = kd_even(K), RW = row_words(K);
@@ -533,7 +589,10 @@ __device__ __forceinline__ void crt_accumulate(const void* Gv, int64_t gplane, i
     const RT* gp = G + t0 * gplane;
 #pragma unroll
     for (int u = 0; u < CH; ++u) {
-      g[u] = t0 + u < N ? static_cast<int>(__ldcs(gp)) : 0;
+      if constexpr (SM)
+        g[u] = t0 + u < N ? static_cast<int>(*gp) : 0;
+      else
+        g[u] = t0 + u < N ? static_cast<int>(__ldcs(gp)) : 0;
       gp += gplane;
     }
 #pragma unroll
@@ -727,11 +786,11 @@ __device__ __forceinline__ void stage_table(const uint32_t* __restrict__ table, 
 // planes are loaded at a time (measured: 8 best for the register-heavy
 // single-job kernel, 16 for the multi-job one, whose occupancy is bounded
 // by its shared-memory window).
-template <int K, bool RES8, int CH = 8>
+template <int K, bool RES8, int CH = 8, bool SM = false>
 __device__ __forceinline__ bool crt_reconstruct(const void* Gij, int64_t gplane, int N,
                                                 const uint32_t* sW, int64_t (&mag)[K]) {
   uint64_t acc[K + 1];
-  crt_accumulate<K, RES8, CH>(Gij, gplane, N, sW + table_head(K), acc);
+  crt_accumulate<K, RES8, CH, SM>(Gij, gplane, N, sW + table_head(K), acc);
   return crt_finish<K>(acc, sW, mag);
 }
 
@@ -833,14 +892,36 @@ template <int COMPS, int K, bool RES8>
 __global__ void __launch_bounds__(128)
 combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __restrict__ status) {
   __shared__ __align__(16) uint32_t sW[StagedTable<K>::WORDS];
+  // byte residues of this block's 128 outputs, [plane][128] (staged path)
+  __shared__ __align__(16) uint8_t sG[RES8 ? kNumMods * 128 : 16];
   stage_table<K>(jb.table, jb.N, sW);
-  __syncthreads();
   const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  // Staged path (uniform per launch): the block's outputs are 128
+  // consecutive, 16-byte aligned bytes of every plane, fetched by cp.async
+  // all at once (N x 8 16-byte chunks in flight per block instead of 8
+  // single-byte loads per thread: the per-thread loads left the kernel
+  // latency bound).
+  const bool staged = RES8 && blockDim.x == 128 && n % 128 == 0 && jb.gpitch % 16 == 0 &&
+                      jb.gplane % 16 == 0 &&
+                      (reinterpret_cast<uintptr_t>(jb.G) & 15) == 0;
+  const int64_t e0 = static_cast<int64_t>(blockIdx.x) * 128;
+  if (staged) {
+    const int i0 = static_cast<int>(e0 / n), j0 = static_cast<int>(e0 % n);
+    const uint8_t* g0 = static_cast<const uint8_t*>(jb.G) + static_cast<int64_t>(i0) * jb.gpitch + j0;
+    for (int c = threadIdx.x; c < jb.N * 8; c += 128)
+      cp_async16(sG + c * 16, g0 + (c >> 3) * jb.gplane + (c & 7) * 16, true);
+    cp_async_commit();
+    cp_async_wait<0>();
+  }
+  __syncthreads();
   if (e >= static_cast<int64_t>(m) * n) return;
   const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
   int64_t mag[K];
-  const bool neg = crt_reconstruct<K, RES8>(
-      elem_ptr<RES8>(jb.G, static_cast<int64_t>(i) * jb.gpitch + j), jb.gplane, jb.N, sW, mag);
+  const bool neg =
+      staged ? crt_reconstruct<K, RES8, 8, true>(sG + threadIdx.x, 128, jb.N, sW, mag)
+             : crt_reconstruct<K, RES8>(
+                   elem_ptr<RES8>(jb.G, static_cast<int64_t>(i) * jb.gpitch + j), jb.gplane,
+                   jb.N, sW, mag);
   bool bad = false;
   const int ebase = -(jb.srow[i] + jb.scol[j]);
   if constexpr (COMPS == 2) {

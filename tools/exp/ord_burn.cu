@@ -106,6 +106,36 @@ __global__ void check_qd(uint64_t seed, int len, unsigned long long* bad) {
   }
 }
 
+// renorm5 (fast path + fallback) against the general emission loop alone
+__global__ void check_renorm(uint64_t seed, long n, unsigned long long* bad) {
+  long i = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t st = seed ^ (uint64_t)i * 0x9e3779b97f4a7c15ull;
+  double x[5];
+  x[0] = unif(st);
+  for (int k = 1; k < 5; ++k) {
+    st = mix(st);
+    int cls = st % 8;
+    double u = unif(st);
+    x[k] = cls == 0 ? 0.0 : cls == 1 ? -0.0 : cls == 2 ? -x[k - 1] : cls == 3 ? ldexp(u, -1060)
+         : ldexp(x[k - 1], -53) * u;
+  }
+  double a[4], b[4];
+  renorm5(x[0], x[1], x[2], x[3], x[4], a);
+  double y1 = x[1], y2 = x[2], y3 = x[3], y4 = x[4], s, t;
+  s = quick_two_sum(y3, y4, y4);
+  t = quick_two_sum(y2, s, y3);
+  s = quick_two_sum(y1, t, y2);
+  t = quick_two_sum(x[0], s, y1);
+  renorm5_emit(t, y1, y2, y3, y4, b);
+  for (int k = 0; k < 4; ++k)
+    if (__double_as_longlong(a[k]) != __double_as_longlong(b[k])) {
+      unsigned long long c = atomicAdd(bad, 1ull);
+      if (c < 4) printf("renorm mismatch %a %a %a %a %a\n", x[0], x[1], x[2], x[3], x[4]);
+      break;
+    }
+}
+
 template <int C, bool ORD>
 __global__ void burn_dd(double* out, int iters, double seed) {
   double hi[C], lo[C];
@@ -169,6 +199,11 @@ int main() {
   cudaDeviceSynchronize();
   printf("qd chains: %d of length 256, %llu mismatches (%s)\n", 592 * 128, *bad,
          cudaGetErrorString(cudaGetLastError()));
+
+  *bad = 0;
+  for (int r = 0; r < 4; ++r) check_renorm<<<(npairs + 255) / 256, 256>>>(99 + r, npairs, bad);
+  cudaDeviceSynchronize();
+  printf("renorm5: %ld x 4 checked, %llu mismatches\n", npairs, *bad);
 
   double* out;
   cudaMalloc(&out, sizeof(double) * 148 * 1024 * 4);
