@@ -602,7 +602,10 @@ __device__ __forceinline__ void crt_accumulate(const void* Gv, int64_t gplane, i
       const unsigned p = static_cast<unsigned>(kModsDev[t]);
       const unsigned r = RES8 ? static_cast<unsigned>(g[u])
                               : barrett(static_cast<unsigned>(g[u]) + kGBias[t], kModMu[t], p);
-      const double rd = static_cast<double>(r);
+      // r < 2^32 as a double without the XU conversion (I2F.F64 was the
+      // kernel's top stall): (2^52 + r) from its bit pattern, minus 2^52,
+      // one exact DADD on the FP64 pipe
+      const double rd = __hiloint2double(0x43300000, static_cast<int>(r)) - 4503599627370496.0;
       const uint32_t* row = W + t * RW;
       const double2* wd = reinterpret_cast<const double2*>(row);
 #pragma unroll
@@ -952,15 +955,35 @@ template <int COMPS, int K, bool RES8>
 __global__ void __launch_bounds__(kMTB)
 combine_multi_kernel(const CrtJobs jobs, int njobs, int win, int m, int n,
                      double* __restrict__ C, int* __restrict__ status) {
-  extern __shared__ unsigned char smraw[];
+  extern __shared__ __align__(16) unsigned char smraw[];
   int64_t* wbuf = reinterpret_cast<int64_t*>(smraw);                  // [win][kMTB]
   uint32_t* tabs = reinterpret_cast<uint32_t*>(wbuf + win * kMTB);    // [njobs][WORDS]
   const int tstride = StagedTable<K>::WORDS;
   for (int J = 0; J < njobs; ++J) stage_table<K>(jobs.j[J].table, jobs.j[J].N, tabs + J * tstride);
+  // Staged path (uniform per launch, as in combine_single_kernel): each
+  // job's residue bytes for the block's 128 outputs arrive by cp.async into
+  // one of two buffers while the previous job is reconstructed.
+  uint8_t* sG = reinterpret_cast<uint8_t*>(tabs + njobs * tstride);   // [2][kNumMods][kMTB]
+  bool staged = RES8 && n % kMTB == 0;
+  for (int J = 0; J < njobs; ++J)
+    staged = staged && jobs.j[J].gpitch % 16 == 0 && jobs.j[J].gplane % 16 == 0 &&
+             (reinterpret_cast<uintptr_t>(jobs.j[J].G) & 15) == 0;
+  const int64_t e0 = static_cast<int64_t>(blockIdx.x) * kMTB;
+  auto prefetch = [&](int J) {
+    const CrtJob& jb = jobs.j[J];
+    const int i0 = static_cast<int>(e0 / n), j0 = static_cast<int>(e0 % n);
+    const uint8_t* g0 =
+        static_cast<const uint8_t*>(jb.G) + static_cast<int64_t>(i0) * jb.gpitch + j0;
+    uint8_t* dst = sG + (J & 1) * kNumMods * kMTB;
+    for (int c = threadIdx.x; c < jb.N * (kMTB / 16); c += kMTB)
+      cp_async16(dst + c * 16, g0 + (c / (kMTB / 16)) * jb.gplane + (c % (kMTB / 16)) * 16, true);
+    cp_async_commit();
+  };
+  if (staged) prefetch(0);
   __syncthreads();
   const int tid = threadIdx.x;
   int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + tid;
-  if (e >= static_cast<int64_t>(m) * n) return;
+  if (e >= static_cast<int64_t>(m) * n) return;   // never taken when staged (n % kMTB == 0)
   const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
 #define WIN(q) wbuf[(q) * kMTB + tid]
   for (int q = 0; q < win; ++q) WIN(q) = 0;
@@ -969,9 +992,23 @@ combine_multi_kernel(const CrtJobs jobs, int njobs, int win, int m, int n,
   for (int J = 0; J < njobs; ++J) {
     const CrtJob& jb = jobs.j[J];
     int64_t mag[K];
-    const bool neg = crt_reconstruct<K, RES8, 16>(
-        elem_ptr<RES8>(jb.G, static_cast<int64_t>(i) * jb.gpitch + j), jb.gplane, jb.N,
-        tabs + J * tstride, mag);
+    bool neg;
+    if (staged) {
+      if (J + 1 < njobs) {
+        prefetch(J + 1);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      neg = crt_reconstruct<K, RES8, 16, true>(sG + (J & 1) * kNumMods * kMTB + tid, kMTB,
+                                               jb.N, tabs + J * tstride, mag);
+      __syncthreads();   // buffer J & 1 is refilled by the prefetch of job J + 2
+    } else {
+      neg = crt_reconstruct<K, RES8, 16>(
+          elem_ptr<RES8>(jb.G, static_cast<int64_t>(i) * jb.gpitch + j), jb.gplane, jb.N,
+          tabs + J * tstride, mag);
+    }
     const int shift = -(jb.srow[i] + jb.scol[j]) - ebase;
     const int q0 = shift >> 5, r = shift & 31;
     if (q0 + K + 1 > win) atomicOr(status, 2);
@@ -1141,7 +1178,8 @@ static cudaError_t combine_multi(const CrtJobs& jobs, int njobs, int K, int win,
                                  double* C, int* status, unsigned blocks, cudaStream_t s) {
   const size_t smem = static_cast<size_t>(win) * kMTB * sizeof(int64_t) +
                       static_cast<size_t>(njobs) * (table_head(K) + row_words(K) * kNumMods) *
-                          sizeof(uint32_t);
+                          sizeof(uint32_t) +
+                      (RES8 ? 2 * kNumMods * kMTB : 0);
   switch (K) {
 #define MPMM_K(KK)                                                                            \
   case KK:                                                                                    \
