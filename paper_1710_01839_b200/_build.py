@@ -13,7 +13,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmpmm_cuda.so")
 SOURCES = ["gemm_dd.cu", "gemm_qd.cu", "ewise.cu", "verify.cu", "rng.cu", "ozaki.cu", "tc_i8.cu", "int8gemm.cpp",
            "strassen.cpp", "runtime.cpp", "oz_plan.cpp", "exact.cpp", "capi.cu", "host_norms.cpp"]
-HEADERS = ["ddqd.cuh", "common.cuh", "kernels.h", "gemm.cuh"]
+HEADERS = ["ddqd.cuh", "common.cuh", "kernels.h", "gemm.cuh", "trace.h"]
 
 # -fmad=false: no implicit contraction (the reference is built with
 # -ffp-contract=off, pkg/setup.py:9-11); explicit __fma_rn stays a DFMA.

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/mpmm_cuda.h"
+#include "trace.h"
 #include "kernels.h"
 
 using namespace mpmm;
@@ -461,6 +462,7 @@ int mpmm_qd_ewise_sub(const double* x, const double* y, double* out, int64_t row
 
 int mpmm_gemm_host(int comps, int algo, int64_t n_min, int64_t m, int64_t l, int64_t n,
                    const double* a, const double* b, double* c, int accumulate, int* nonfinite) {
+  TraceRange trace_("mpmm_gemm_host");
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
   if (!dims_ok(m, l, n)) return fail(MPMM_ERR_ARG, "bad shape");
   if (algo != MPMM_ALGO_SIMPLE && algo != MPMM_ALGO_BLOCK && algo != MPMM_ALGO_BLOCK_FAST)
@@ -474,6 +476,7 @@ int mpmm_gemm_host(int comps, int algo, int64_t n_min, int64_t m, int64_t l, int
 int mpmm_gemm_dev(int comps, int algo, int64_t n_min, int64_t m, int64_t l, int64_t n,
                   const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                   int64_t ldc, int accumulate, int* nonfinite, void* stream) {
+  TraceRange trace_("mpmm_gemm_dev");
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
   if (!dims_ok(m, l, n)) return fail(MPMM_ERR_ARG, "bad shape");
   if (lda < l || ldb < n || ldc < n) return fail(MPMM_ERR_ARG, "leading dimension too small");
@@ -493,6 +496,7 @@ int mpmm_gemm_dev(int comps, int algo, int64_t n_min, int64_t m, int64_t l, int6
 int mpmm_gemm_batched_dev(int comps, int algo, int64_t n_min, int64_t batch, int64_t m,
                           int64_t l, int64_t n, const void* problems, int accumulate,
                           int* nonfinite, void* stream) {
+  TraceRange trace_("mpmm_gemm_batched_dev");
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
   if (!dims_ok(m, l, n) || batch < 0 || batch > (1 << 24)) return fail(MPMM_ERR_ARG, "bad shape");
   if (algo != MPMM_ALGO_SIMPLE && algo != MPMM_ALGO_BLOCK && algo != MPMM_ALGO_BLOCK_FAST)
@@ -515,6 +519,7 @@ int mpmm_gemm_batched_dev(int comps, int algo, int64_t n_min, int64_t batch, int
 int mpmm_block_cells_dev(int comps, int64_t n_min, int64_t cell0, int64_t cell1, int64_t m,
                          int64_t l, int64_t n, const double* A, int64_t lda, const double* B,
                          int64_t ldb, double* C, int64_t ldc, void* stream) {
+  TraceRange trace_("mpmm_block_cells_dev");
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
   if (!dims_ok(m, l, n)) return fail(MPMM_ERR_ARG, "bad shape");
   return block_cells_impl(comps, n_min, cell0, cell1, m, l, n, A, lda, B, ldb, C, ldc,
@@ -525,6 +530,7 @@ int mpmm_ewise_dev(int comps, int nops, int64_t rows, int64_t cols, const double
                    int64_t ldx, const double* Y, int64_t ldy, int sy, const double* Z,
                    int64_t ldz, int sz, const double* W, int64_t ldw, int sw, double* O,
                    int64_t ldo, void* stream) {
+  TraceRange trace_("mpmm_ewise_dev");
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
   if (nops < 1 || nops > 3) return fail(MPMM_ERR_ARG, "nops must be 1..3");
   if (!dims_ok(rows, 0, cols)) return fail(MPMM_ERR_ARG, "bad shape");
@@ -536,6 +542,7 @@ int mpmm_ewise_dev(int comps, int nops, int64_t rows, int64_t cols, const double
 
 int mpmm_ewise_batched_dev(int comps, int64_t batch, int64_t rows, int64_t cols,
                            const void* problems, void* stream) {
+  TraceRange trace_("mpmm_ewise_batched_dev");
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
   if (!dims_ok(rows, 0, cols) || batch < 0 || batch > 65535) return fail(MPMM_ERR_ARG, "bad shape");
   if (batch == 0) return MPMM_OK;
@@ -558,6 +565,7 @@ int mpmm_exact_check_dev(int comps, int64_t m, int64_t l, int64_t n, const doubl
                          int64_t lda, const double* B, int64_t ldb, const double* C, int64_t ldc,
                          const int64_t* idx_i, const int64_t* idx_j, int64_t count, int u_exp,
                          double* ratio, void* stream) {
+  TraceRange trace_("mpmm_exact_check_dev");
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
   if (!dims_ok(m, l, n) || count < 0) return fail(MPMM_ERR_ARG, "bad shape");
   cudaError_t err = exact_check_launch(comps, (int)l, A, lda, B, ldb, C, ldc, idx_i, idx_j, count,
@@ -618,6 +626,7 @@ int mpmm_oz_plan(int comps, int64_t m, int64_t n, int64_t l, const int* ela, con
 int mpmm_gemm_exact_dev(int comps, int64_t m, int64_t l, int64_t n, const double* A,
                         int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc,
                         void* stream) {
+  TraceRange trace_("mpmm_gemm_exact_dev");
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
   if (!dims_ok(m, l, n)) return fail(MPMM_ERR_ARG, "bad shape");
   if (lda < l || ldb < n || ldc < n) return fail(MPMM_ERR_ARG, "leading dimension too small");
@@ -634,6 +643,7 @@ int mpmm_gemm_exact_dev(int comps, int64_t m, int64_t l, int64_t n, const double
 
 int mpmm_residue_gemm_dev(int64_t m, int64_t n, int64_t k, int64_t batch, const int8_t* A,
                           const int8_t* Bt, uint8_t* R, void* stream) {
+  TraceRange trace_("mpmm_residue_gemm_dev");
   if (!tc_residue_gemm_supported(m, n, k) || batch < 1 || batch > 54)
     return fail(MPMM_ERR_ARG, "residue GEMM needs m % 128 == 0, n % 256 == 0, k % 128 == 0, "
                               "k <= 131071, 1 <= batch <= 54");
@@ -659,6 +669,7 @@ int mpmm_int8_gemm_batched_dev(int64_t m, int64_t n, int64_t k, int64_t batch, c
 
 int mpmm_oz_combine_dev(int comps, const void* jobs, int njobs, int64_t m, int64_t n, double* C,
                         int* status, void* stream) {
+  TraceRange trace_("mpmm_oz_combine_dev");
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
   if (njobs < 1 || njobs > 16 || !dims_ok(m, 0, n)) return fail(MPMM_ERR_ARG, "bad shape");
   cudaError_t e = oz_combine_launch(comps, jobs, njobs, (int)m, (int)n, C, status,
@@ -682,6 +693,7 @@ int mpmm_oz_shifts_dev(int comps, int nranges, const int* ranges, int64_t odim, 
 int mpmm_strassen_dev(int comps, int64_t cutoff, int64_t leaf_n_min, int64_t m, int64_t l,
                       int64_t n, const double* A, int64_t lda, const double* B, int64_t ldb,
                       double* C, int64_t ldc, int* nonfinite, int64_t* stats, void* stream) {
+  TraceRange trace_("mpmm_strassen_dev");
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
   if (!dims_ok(m, l, n)) return fail(MPMM_ERR_ARG, "bad shape");
   if (lda < l || ldb < n || ldc < n) return fail(MPMM_ERR_ARG, "leading dimension too small");
@@ -713,6 +725,7 @@ int mpmm_runtime_gpus(int* ngpus, int* devices, int cap) {
 int mpmm_gemm_multi(int comps, int algo, int64_t n_min, int64_t cutoff, int64_t m, int64_t l,
                     int64_t n, const double* a, const double* b, double* c, int64_t panels,
                     int* nonfinite, double* device_ms) {
+  TraceRange trace_("mpmm_gemm_multi");
   if (comps != 2 && comps != 4) return fail(MPMM_ERR_ARG, "comps must be 2 or 4");
   if (!dims_ok(m, l, n)) return fail(MPMM_ERR_ARG, "bad shape");
   if (algo < MPMM_ALGO_SIMPLE || algo > MPMM_ALGO_STRASSEN) return fail(MPMM_ERR_ARG, "bad algo");

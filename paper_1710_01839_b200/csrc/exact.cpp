@@ -25,6 +25,7 @@
 #include <tuple>
 #include <vector>
 
+#include "trace.h"
 #include "kernels.h"
 
 namespace mpmm {
@@ -289,6 +290,7 @@ cudaError_t enqueue_product(const Plan& pl, int comps, int64_t m, int64_t l, int
                             const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                             int64_t ldc, Workspace& ws, int dev, cudaStream_t s,
                             std::string* err) {
+  TraceRange trace_("exact: enqueue product (shifts, residues, residue GEMMs, combine)");
   const Pads P = pads_for(m, l, n);
   const int64_t mp = P.mp, np = P.np, lp = P.lp;
   if (ldc != n) {

@@ -28,6 +28,7 @@
 #include <string>
 #include <vector>
 
+#include "trace.h"
 #include "kernels.h"
 
 namespace mpmm {
@@ -283,6 +284,7 @@ int rt_gemm_host(int comps, int algo, int tile, int64_t cutoff, int64_t m, int64
                                 cudaMemcpyHostToDevice, d.comm));
       }
       if (G > 1) {
+        TraceRange trace_("runtime: ncclBroadcast of a B k-panel");
         RT_NC(g_nccl.groupStart());
         for (int g = 0; g < G; ++g) {
           RT_CU(cudaSetDevice(g_gpus[g].id));

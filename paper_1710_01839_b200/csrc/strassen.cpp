@@ -24,6 +24,7 @@
 #include <cstring>
 #include <vector>
 
+#include "trace.h"
 #include "kernels.h"
 
 namespace mpmm {
@@ -149,6 +150,7 @@ class Driver {
   // operand sums, and the children (returned).  multiply.py:300-332.
   cudaError_t expand(std::vector<Node>& nodes, int64_t m, int64_t l, int64_t n,
                      std::vector<Node>* children) {
+    TraceRange trace_("strassen: operand sums (one level)");
     const int64_t me = m + (m & 1), le = l + (l & 1), ne = n + (n & 1);
     const int64_t hm = me / 2, hl = le / 2, hn = ne / 2;
     std::vector<EwiseProblem> sa, sb;
