@@ -35,6 +35,7 @@ class Algorithm(enum.Enum):
     SIMPLE = "simple"
     BLOCK = "block"
     STRASSEN = "strassen"
+    EXACT = "exact"     # extension: the int8 tensor-core exact mode (tensor.py)
 
 
 DEFAULT_STRASSEN_CUTOFF = 64
@@ -44,7 +45,10 @@ DEFAULT_BLOCK_SIZE = 64
 @dataclass(frozen=True)
 class AlgorithmChoice:
     """One tuner outcome; tokens ``simple``, ``block:N``, ``strassen:C/N``
-    (reference multiply.py:35-71)."""
+    (reference multiply.py:35-71), and ``exact`` for the opt-in exact
+    tensor-core mode (``TuningConfig.exact``).  ``exact`` may carry the
+    mirror block size to fall back to (``exact/N``) when an operand's
+    dynamic range is too wide for the int8 CRT scheme."""
     kind: Algorithm
     n_min: Optional[int] = None
     cutoff: Optional[int] = None
@@ -64,6 +68,8 @@ class AlgorithmChoice:
             return "simple"
         if self.kind is Algorithm.BLOCK:
             return f"block:{self.n_min}"
+        if self.kind is Algorithm.EXACT:
+            return "exact" if self.n_min is None else f"exact/{self.n_min}"
         return f"strassen:{self.cutoff}/{self.n_min}"
 
     @staticmethod
@@ -75,6 +81,10 @@ class AlgorithmChoice:
         if tok.startswith("strassen:"):
             cut, _, leaf = tok[len("strassen:"):].partition("/")
             return AlgorithmChoice(Algorithm.STRASSEN, n_min=int(leaf), cutoff=int(cut))
+        if tok == "exact":
+            return AlgorithmChoice(Algorithm.EXACT)
+        if tok.startswith("exact/"):
+            return AlgorithmChoice(Algorithm.EXACT, n_min=int(tok[len("exact/"):]))
         raise ValueError(f"bad algorithm token {tok!r}")
 
     def __str__(self):
@@ -402,4 +412,11 @@ def run_choice(a, b, choice, threads=1):
         return matmul_simple(a, b, threads)
     if choice.kind is Algorithm.BLOCK:
         return matmul_block(a, b, choice.n_min, threads)
+    if choice.kind is Algorithm.EXACT:
+        from .tensor import NotRepresentable, matmul_exact
+        try:
+            return matmul_exact(a, b)
+        except NotRepresentable:
+            # operands outside the int8 CRT range: the mirror blocked kernel
+            return matmul_block(a, b, choice.n_min or DEFAULT_BLOCK_SIZE, threads)
     return matmul_strassen(a, b, choice.cutoff, choice.n_min, threads)

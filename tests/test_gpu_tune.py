@@ -93,3 +93,29 @@ def test_strassen_cutoff_sweep_cfg3_rectangular(gpu):
     S, T = DenseMatrix(96, 96, DD, s), DenseMatrix(96, 96, DD, t)
     assert mp.matmul_strassen(S, T, 16, 8, rectangular=True) == mp.matmul_strassen(S, T, 16, 8)
     assert np.array_equal(mp.matmul_strassen(S, T, 16, 8).data, oracle.strassen(s, t, 16, 8))
+
+
+def test_tune_one_with_exact_candidate_and_run_choice(gpu, tmp_path):
+    """The opt-in exact tensor-core candidate: timed, ranked last on ties,
+    written as a v3 table; run_choice on its token returns the exact mode's
+    product (the exact product rounded once, within the north_star bound)."""
+    from paper_1710_01839_b200.tensor import matmul_exact
+    cfg = mp.TuningConfig(precisions=[DD], dims=[512], block_candidates=[32, 64],
+                          thread_counts=[1], strassen_cutoff=128, exact=True,
+                          out_path=str(tmp_path / "t3.tbl"))
+    r = mp.tune_one(DD, 512, 1, cfg)
+    assert r.exact_time_s is not None and r.exact_time_s > 0
+    times = {mp.Algorithm.BLOCK: r.block_time_s, mp.Algorithm.STRASSEN: r.strassen_time_s,
+             mp.Algorithm.SIMPLE: r.simple_time_s, mp.Algorithm.EXACT: r.exact_time_s}
+    assert times[r.winner.kind] == min(times.values())
+    table = mp.tune_sweep(cfg)
+    assert open(cfg.out_path).read().startswith("mpmmtune v3")
+    assert mp.load_table(cfg.out_path) == table
+    a, b = inputs.gemm_inputs("dd", 96, 80, 72, seed=3)
+    A = DenseMatrix(96, 80, DD, a).to_device()
+    B = DenseMatrix(80, 72, DD, b).to_device()
+    c = mp.run_choice(A, B, mp.AlgorithmChoice.parse("exact/32")).host_array()
+    assert np.array_equal(c, matmul_exact(A, B).host_array())
+    from oracle import exact
+    ratio, _ = exact.bound_ratio(a, b, c, range(0, 96, 7), range(0, 72, 5), 104)
+    assert ratio <= 1.0

@@ -22,7 +22,7 @@ QD = mp.PrecisionSpec.qd()
 
 
 def test_algorithm_choice_tokens():
-    for tok in ("simple", "block:64", "strassen:64/32"):
+    for tok in ("simple", "block:64", "strassen:64/32", "exact", "exact/32"):
         assert mp.AlgorithmChoice.parse(tok).token == tok
     with pytest.raises(ValueError):
         mp.AlgorithmChoice.parse("winograd")
@@ -214,6 +214,35 @@ def test_v2_table_with_gpus(tmp_path):
     assert mp.load_table(str(p)) == t
     assert mp.lookup_best(t, DD, 1024, 1, gpus=8) == (t.rows[0].winner, "exact")
     assert mp.lookup_best(t, DD, 4096, 1, gpus=8)[1] == "nearest"
+
+
+def test_v3_table_with_exact_candidate(tmp_path):
+    ex = mk_row(DD, 2048, 1, False)
+    ex.exact_time_s = 0.125
+    ex.winner = mp.AlgorithmChoice(mp.Algorithm.EXACT, n_min=ex.best_n_min)
+    t = mp.TuningTable(rows=[mk_row(DD, 1024, 1, True), ex], thresholds={},
+                       total_tuning_time_s=2.0, prediction_total_s=0.5)
+    p = tmp_path / "v3.tbl"
+    mp.save_table(t, str(p))
+    text = p.read_text()
+    assert text.startswith("mpmmtune v3") and " exact/8" in text
+    assert mp.load_table(str(p)) == t
+    assert mp.lookup_best(t, DD, 2048, 1) == (ex.winner, "exact")
+    assert mp.lookup_best(t, DD, 4096, 1) == (ex.winner, "nearest")
+    # no exact column / winner: the reference's v1 format, unchanged
+    t1 = mp.TuningTable(rows=[mk_row(DD, 1024, 1, True)], thresholds={})
+    mp.save_table(t1, str(p))
+    assert p.read_text().startswith("mpmmtune v1")
+
+
+def test_pick_winner_with_exact_candidate():
+    from paper_1710_01839_b200.tune import _pick_winner
+    w = _pick_winner(2.0, 3.0, None, 32, 64, exact_time=1.0)
+    assert w.kind is mp.Algorithm.EXACT and w.n_min == 32
+    # ties go to the reference's algorithms first
+    assert _pick_winner(1.0, 1.0, 1.0, 32, 64, exact_time=1.0).kind is mp.Algorithm.BLOCK
+    assert _pick_winner(2.0, 1.0, None, 32, 64, exact_time=1.0).kind is mp.Algorithm.STRASSEN
+    assert _pick_winner(2.0, None, None, 32, 64).kind is mp.Algorithm.BLOCK
 
 
 def test_table_errors(tmp_path):
