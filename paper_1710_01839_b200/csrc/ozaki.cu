@@ -21,7 +21,10 @@
 // result is still the exact product, rounded once.  The planner
 // (tensor.py) reports NotRepresentable when even single components do not
 // fit.
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "common.cuh"
@@ -897,9 +900,10 @@ combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __re
   __shared__ __align__(16) uint32_t sW[StagedTable<K>::WORDS];
   // byte residues of this block's 128 outputs, [plane][128] (staged path)
   __shared__ __align__(16) uint8_t sG[RES8 ? kNumMods * 128 : 16];
+  // persistent blocks (grid-stride over 128-output tiles): the table is
+  // staged once per block
   stage_table<K>(jb.table, jb.N, sW);
-  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  // Staged path (uniform per launch): the block's outputs are 128
+  // Staged path (uniform per launch): the tile's outputs are 128
   // consecutive, 16-byte aligned bytes of every plane, fetched by cp.async
   // all at once (N x 8 16-byte chunks in flight per block instead of 8
   // single-byte loads per thread: the per-thread loads left the kernel
@@ -907,39 +911,281 @@ combine_single_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __re
   const bool staged = RES8 && blockDim.x == 128 && n % 128 == 0 && jb.gpitch % 16 == 0 &&
                       jb.gplane % 16 == 0 &&
                       (reinterpret_cast<uintptr_t>(jb.G) & 15) == 0;
-  const int64_t e0 = static_cast<int64_t>(blockIdx.x) * 128;
-  if (staged) {
-    const int i0 = static_cast<int>(e0 / n), j0 = static_cast<int>(e0 % n);
-    const uint8_t* g0 = static_cast<const uint8_t*>(jb.G) + static_cast<int64_t>(i0) * jb.gpitch + j0;
-    for (int c = threadIdx.x; c < jb.N * 8; c += 128)
-      cp_async16(sG + c * 16, g0 + (c >> 3) * jb.gplane + (c & 7) * 16, true);
-    cp_async_commit();
-    cp_async_wait<0>();
+  const int64_t total = static_cast<int64_t>(m) * n;
+  for (int64_t e0 = static_cast<int64_t>(blockIdx.x) * blockDim.x; e0 < total;
+       e0 += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (staged) {
+      const int i0 = static_cast<int>(e0 / n), j0 = static_cast<int>(e0 % n);
+      const uint8_t* g0 =
+          static_cast<const uint8_t*>(jb.G) + static_cast<int64_t>(i0) * jb.gpitch + j0;
+      for (int c = threadIdx.x; c < jb.N * 8; c += 128)
+        cp_async16(sG + c * 16, g0 + (c >> 3) * jb.gplane + (c & 7) * 16, true);
+      cp_async_commit();
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int64_t e = e0 + threadIdx.x;
+    if (e < total) {
+      const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
+      int64_t mag[K];
+      const bool neg =
+          staged ? crt_reconstruct<K, RES8, 8, true>(sG + threadIdx.x, 128, jb.N, sW, mag)
+                 : crt_reconstruct<K, RES8>(
+                       elem_ptr<RES8>(jb.G, static_cast<int64_t>(i) * jb.gpitch + j),
+                       jb.gplane, jb.N, sW, mag);
+      bool bad = false;
+      const int ebase = -(jb.srow[i] + jb.scol[j]);
+      if constexpr (COMPS == 2) {
+        double hi, lo;
+        if (round_dd_fast<K>(mag, neg, ebase, hi, lo)) {
+          C[e * 2] = hi;
+          C[e * 2 + 1] = lo;
+          bad = !isfinite(hi) || !isfinite(lo);
+        } else {
+          round_out<COMPS, K>(mag, neg, ebase, C + e * COMPS, bad);
+        }
+      } else {
+        round_out<COMPS, K>(mag, neg, ebase, C + e * COMPS, bad);
+      }
+      if (bad) atomicOr(status, 1);
+    }
+    __syncthreads();   // sG is refilled for the next tile
   }
-  __syncthreads();
-  if (e >= static_cast<int64_t>(m) * n) return;
-  const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
-  int64_t mag[K];
-  const bool neg =
-      staged ? crt_reconstruct<K, RES8, 8, true>(sG + threadIdx.x, 128, jb.N, sW, mag)
-             : crt_reconstruct<K, RES8>(
-                   elem_ptr<RES8>(jb.G, static_cast<int64_t>(i) * jb.gpitch + j), jb.gplane,
-                   jb.N, sW, mag);
-  bool bad = false;
-  const int ebase = -(jb.srow[i] + jb.scol[j]);
-  if constexpr (COMPS == 2) {
-    double hi, lo;
-    if (round_dd_fast<K>(mag, neg, ebase, hi, lo)) {
-      C[e * 2] = hi;
-      C[e * 2 + 1] = lo;
-      bad = !isfinite(hi) || !isfinite(lo);
+}
+
+// ---------------------------------------------------------------------------
+// CRT sums on the tensor cores
+//
+// The bulk of a CUDA-core combine is S_q = sum_t r_t W_t[q]: N x K
+// multiply-adds per output (39 x 9 for DD 1024^3).  Splitting each weight
+// limb into its four bytes turns that into an integer matrix product --
+// residues (outputs x moduli, u8) times weight bytes (moduli x 4K byte
+// columns, u8) -- with int32 sums < 54 * 255^2 < 2^22, exact; then
+// S_q = sum_b s_{4q+b} 2^(8b) < 2^48 per limb.  One block of 128 threads
+// reconstructs 128 outputs: the residues are staged as rows of sA (moduli
+// contiguous, zero above N), each warp runs IMMA.16832.U8.U8 (mma.sync
+// m16n8k32) over its 32 outputs x 8*NT columns x 64 moduli, the sums go
+// through sC to the thread that owns the output, and crt_finish / rounding
+// follow as in the CUDA-core kernels (same integer, same bits).
+// ---------------------------------------------------------------------------
+
+template <int K>
+struct MmaLayout {
+  static constexpr int NT = (4 * K + 7) / 8;   // n-tiles of 8 byte columns
+  static constexpr int COLS = 8 * NT;
+  static constexpr int AST = 20;               // sA / sWB row stride in words (16 used): the
+                                               // fragment loads hit 32 distinct banks
+  static constexpr int CST = COLS + 4;         // sC row stride: CST/4 odd, LDS.128 conflict-free
+  static constexpr int WB_OFF = 0;
+  static constexpr int A_OFF = WB_OFF + COLS * AST * 4;
+  static constexpr int C_OFF = A_OFF + 128 * AST * 4;
+  static constexpr int S_OFF = C_OFF + 128 * CST * 4;          // [kNumMods][128] staged bytes
+  static constexpr int H_OFF = S_OFF + kNumMods * 128;         // P, P/2, 1/P
+  static constexpr int BYTES = H_OFF + table_head(K) * 4;
+};
+
+__device__ __forceinline__ void mma_u8_16832(int (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                             uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// Weight bytes sWB[c][t] (c = 4q + b: byte b of W_t[q]; t contiguous,
+// zero for t >= N or q >= K) and the head (P, P/2, 1/P) of one job.
+template <int K>
+__device__ __forceinline__ void stage_mma_tables(const uint32_t* __restrict__ table, int N,
+                                                 unsigned char* sm) {
+  using L = MmaLayout<K>;
+  uint32_t* sWB = reinterpret_cast<uint32_t*>(sm + L::WB_OFF);
+  for (int idx = threadIdx.x; idx < L::COLS * 16; idx += blockDim.x) {
+    const int c = idx >> 4, w = idx & 15;
+    const int q = c >> 2, b = c & 3;
+    uint32_t v = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = 4 * w + u;
+      const uint32_t byte = (q < K && t < N) ? (table[(t + 1) * K + q] >> (8 * b)) & 0xffu : 0u;
+      v |= byte << (8 * u);
+    }
+    sWB[c * L::AST + w] = v;
+  }
+  constexpr int PW = pwords(K);
+  uint32_t* sH = reinterpret_cast<uint32_t*>(sm + L::H_OFF);
+  for (int q = threadIdx.x; q < PW; q += blockDim.x) {
+    sH[q] = q < K ? table[q] : 0u;
+    const uint32_t lo = q < K ? table[q] : 0u, hi = q + 1 < K ? table[q + 1] : 0u;
+    sH[PW + q] = (lo >> 1) | (hi << 31);     // P/2 (P is even)
+  }
+  if (threadIdx.x == 0) {
+    double pd = 0.0, sc = 1.0;
+    for (int q = 0; q < K; ++q) {
+      pd += static_cast<double>(table[q]) * sc;
+      sc *= 4294967296.0;
+    }
+    *reinterpret_cast<double*>(sH + 2 * PW) = 1.0 / pd;
+  }
+}
+
+// The staged path's condition (uniform per launch): the block's 128 outputs
+// are 128 consecutive, 16-byte aligned bytes of every residue plane.
+__device__ __forceinline__ bool mma_staged(const CrtJob& jb, int n) {
+  return n % 128 == 0 && jb.gpitch % 16 == 0 && jb.gplane % 16 == 0 &&
+         (reinterpret_cast<uintptr_t>(jb.G) & 15) == 0;
+}
+
+// cp.async the block's residue bytes [t][128] into the staging area (RES8).
+__device__ __forceinline__ void mma_prefetch(const CrtJob& jb, int64_t e0, int n,
+                                             unsigned char* stage) {
+  const int i0 = static_cast<int>(e0 / n), j0 = static_cast<int>(e0 % n);
+  const uint8_t* g0 = static_cast<const uint8_t*>(jb.G) + static_cast<int64_t>(i0) * jb.gpitch + j0;
+  for (int c = threadIdx.x; c < jb.N * 8; c += blockDim.x)
+    cp_async16(stage + c * 16, g0 + (c >> 3) * jb.gplane + (c & 7) * 16, true);
+  cp_async_commit();
+}
+
+// Reconstruction of the calling thread's output (o = threadIdx.x of 128;
+// element (i, j), valid when in range) for one job whose tables are staged
+// in `sm`: (neg, mag) exactly as crt_reconstruct returns them.  STAGED:
+// the residue bytes are already in the staging area (mma_prefetch, waited).
+// Every thread of the block must call it (warp-synchronous MMAs).
+template <int K, bool RES8>
+__device__ __forceinline__ bool crt_reconstruct_mma(const CrtJob& jb, bool staged, bool valid,
+                                                    int i, int j, unsigned char* sm,
+                                                    int64_t (&mag)[K]) {
+  using L = MmaLayout<K>;
+  const int o = threadIdx.x, lane = o & 31, warp = o >> 5;
+  uint32_t* sA = reinterpret_cast<uint32_t*>(sm + L::A_OFF);
+  // 1. this output's residues r_t (t < 64) as 16 words of sA row o
+  {
+    uint32_t w[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) w[q] = 0u;
+    const int N = jb.N;
+    if (staged) {
+      const unsigned char* stage = sm + L::S_OFF;
+#pragma unroll
+      for (int t = 0; t < kNumMods; ++t)
+        if (t < N) w[t >> 2] |= static_cast<uint32_t>(stage[t * 128 + o]) << (8 * (t & 3));
+    } else if (valid) {
+      const int64_t off = static_cast<int64_t>(i) * jb.gpitch + j;
+#pragma unroll
+      for (int t = 0; t < kNumMods; ++t) {
+        if (t < N) {
+          uint32_t r;
+          if constexpr (RES8) {
+            r = __ldcs(static_cast<const uint8_t*>(jb.G) + t * jb.gplane + off);
+          } else {
+            const int g = __ldcs(static_cast<const int32_t*>(jb.G) + t * jb.gplane + off);
+            r = barrett(static_cast<unsigned>(g) + kGBias[t], kModMu[t],
+                        static_cast<unsigned>(kModsDev[t]));
+          }
+          w[t >> 2] |= r << (8 * (t & 3));
+        }
+      }
+    }
+    uint4* row = reinterpret_cast<uint4*>(sA + o * L::AST);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) row[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+  }
+  __syncwarp();
+  // 2. S = R W on the tensor cores, this warp's 32 outputs
+  const uint32_t* sWB = reinterpret_cast<const uint32_t*>(sm + L::WB_OFF);
+  int acc[2][L::NT][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < L::NT; ++nt)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[mt][nt][v] = 0;
+  const int g = lane >> 2, tg = lane & 3;
+#pragma unroll
+  for (int ks = 0; ks < 2; ++ks) {
+    uint32_t b[L::NT][2];
+#pragma unroll
+    for (int nt = 0; nt < L::NT; ++nt) {
+      const uint32_t* col = sWB + (nt * 8 + g) * L::AST + ks * 8 + tg;
+      b[nt][0] = col[0];
+      b[nt][1] = col[4];
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      const uint32_t* r0 = sA + (warp * 32 + mt * 16 + g) * L::AST + ks * 8 + tg;
+      const uint32_t a[4] = {r0[0], r0[8 * L::AST], r0[4], r0[8 * L::AST + 4]};
+#pragma unroll
+      for (int nt = 0; nt < L::NT; ++nt) mma_u8_16832(acc[mt][nt], a, b[nt][0], b[nt][1]);
+    }
+  }
+  // 3. the sums to the owning thread
+  int* sC = reinterpret_cast<int*>(sm + L::C_OFF);
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < L::NT; ++nt) {
+      int* c0 = sC + (warp * 32 + mt * 16 + g) * L::CST + nt * 8 + 2 * tg;
+      *reinterpret_cast<int2*>(c0) = make_int2(acc[mt][nt][0], acc[mt][nt][1]);
+      *reinterpret_cast<int2*>(c0 + 8 * L::CST) = make_int2(acc[mt][nt][2], acc[mt][nt][3]);
+    }
+  __syncwarp();
+  uint64_t S[K + 1];
+  {
+    const int4* my = reinterpret_cast<const int4*>(sC + o * L::CST);
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      const int4 v = my[q];
+      S[q] = static_cast<uint64_t>(static_cast<uint32_t>(v.x)) +
+             (static_cast<uint64_t>(static_cast<uint32_t>(v.y)) << 8) +
+             (static_cast<uint64_t>(static_cast<uint32_t>(v.z)) << 16) +
+             (static_cast<uint64_t>(static_cast<uint32_t>(v.w)) << 24);
+    }
+    S[K] = 0;
+  }
+  __syncwarp();   // sA / sC rows are rewritten by the next job
+  return crt_finish<K>(S, reinterpret_cast<const uint32_t*>(sm + L::H_OFF), mag);
+}
+
+template <int COMPS, int K, bool RES8>
+__global__ void __launch_bounds__(128)
+combine_mma_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char smm[];
+  using L = MmaLayout<K>;
+  // persistent blocks: the tables are staged once per block, not per tile
+  stage_mma_tables<K>(jb.table, jb.N, smm);
+  const bool staged = RES8 && mma_staged(jb, n);
+  const int64_t total = static_cast<int64_t>(m) * n;
+  const int64_t tiles = (total + 127) / 128;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t e0 = tile * 128;
+    if (staged) {
+      mma_prefetch(jb, e0, n, smm + L::S_OFF);
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const int64_t e = e0 + threadIdx.x;
+    const bool valid = e < total;
+    const int i = valid ? static_cast<int>(e / n) : 0, j = valid ? static_cast<int>(e % n) : 0;
+    int64_t mag[K];
+    const bool neg = crt_reconstruct_mma<K, RES8>(jb, staged, valid, i, j, smm, mag);
+    __syncthreads();   // the staging area is refilled for the next tile
+    if (!valid) continue;
+    bool bad = false;
+    const int ebase = -(jb.srow[i] + jb.scol[j]);
+    if constexpr (COMPS == 2) {
+      double hi, lo;
+      if (round_dd_fast<K>(mag, neg, ebase, hi, lo)) {
+        C[e * 2] = hi;
+        C[e * 2 + 1] = lo;
+        bad = !isfinite(hi) || !isfinite(lo);
+      } else {
+        round_out<COMPS, K>(mag, neg, ebase, C + e * COMPS, bad);
+      }
     } else {
       round_out<COMPS, K>(mag, neg, ebase, C + e * COMPS, bad);
     }
-  } else {
-    round_out<COMPS, K>(mag, neg, ebase, C + e * COMPS, bad);
+    if (bad) atomicOr(status, 1);
   }
-  if (bad) atomicOr(status, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -968,124 +1214,131 @@ combine_multi_kernel(const CrtJobs jobs, int njobs, int win, int m, int n,
   for (int J = 0; J < njobs; ++J)
     staged = staged && jobs.j[J].gpitch % 16 == 0 && jobs.j[J].gplane % 16 == 0 &&
              (reinterpret_cast<uintptr_t>(jobs.j[J].G) & 15) == 0;
-  const int64_t e0 = static_cast<int64_t>(blockIdx.x) * kMTB;
-  auto prefetch = [&](int J) {
-    const CrtJob& jb = jobs.j[J];
-    const int i0 = static_cast<int>(e0 / n), j0 = static_cast<int>(e0 % n);
-    const uint8_t* g0 =
-        static_cast<const uint8_t*>(jb.G) + static_cast<int64_t>(i0) * jb.gpitch + j0;
-    uint8_t* dst = sG + (J & 1) * kNumMods * kMTB;
-    for (int c = threadIdx.x; c < jb.N * (kMTB / 16); c += kMTB)
-      cp_async16(dst + c * 16, g0 + (c / (kMTB / 16)) * jb.gplane + (c % (kMTB / 16)) * 16, true);
-    cp_async_commit();
-  };
-  if (staged) prefetch(0);
-  __syncthreads();
-  const int tid = threadIdx.x;
-  int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + tid;
-  if (e >= static_cast<int64_t>(m) * n) return;   // never taken when staged (n % kMTB == 0)
-  const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
-#define WIN(q) wbuf[(q) * kMTB + tid]
-  for (int q = 0; q < win; ++q) WIN(q) = 0;
-  int ebase = 1 << 30;
-  for (int J = 0; J < njobs; ++J) ebase = min(ebase, -(jobs.j[J].srow[i] + jobs.j[J].scol[j]));
-  for (int J = 0; J < njobs; ++J) {
-    const CrtJob& jb = jobs.j[J];
-    int64_t mag[K];
-    bool neg;
-    if (staged) {
-      if (J + 1 < njobs) {
-        prefetch(J + 1);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
+  __syncthreads();   // tables staged
+  // persistent blocks (grid-stride over 128-output tiles): the tables above
+  // are staged once per block
+  const int64_t total = static_cast<int64_t>(m) * n;
+  for (int64_t e0 = static_cast<int64_t>(blockIdx.x) * kMTB; e0 < total;
+       e0 += static_cast<int64_t>(gridDim.x) * kMTB) {
+    auto prefetch = [&](int J) {
+      const CrtJob& jb = jobs.j[J];
+      const int i0 = static_cast<int>(e0 / n), j0 = static_cast<int>(e0 % n);
+      const uint8_t* g0 =
+          static_cast<const uint8_t*>(jb.G) + static_cast<int64_t>(i0) * jb.gpitch + j0;
+      uint8_t* dst = sG + (J & 1) * kNumMods * kMTB;
+      for (int c = threadIdx.x; c < jb.N * (kMTB / 16); c += kMTB)
+        cp_async16(dst + c * 16, g0 + (c / (kMTB / 16)) * jb.gplane + (c % (kMTB / 16)) * 16, true);
+      cp_async_commit();
+    };
+    if (staged) prefetch(0);
+    [&]() {
+      const int tid = threadIdx.x;
+      const int64_t e = e0 + tid;
+      if (e >= total) return;   // never taken when staged (n % kMTB == 0)
+      const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
+    #define WIN(q) wbuf[(q) * kMTB + tid]
+      for (int q = 0; q < win; ++q) WIN(q) = 0;
+      int ebase = 1 << 30;
+      for (int J = 0; J < njobs; ++J) ebase = min(ebase, -(jobs.j[J].srow[i] + jobs.j[J].scol[j]));
+      for (int J = 0; J < njobs; ++J) {
+        const CrtJob& jb = jobs.j[J];
+        int64_t mag[K];
+        bool neg;
+        if (staged) {
+          if (J + 1 < njobs) {
+            prefetch(J + 1);
+            cp_async_wait<1>();
+          } else {
+            cp_async_wait<0>();
+          }
+          __syncthreads();
+          neg = crt_reconstruct<K, RES8, 16, true>(sG + (J & 1) * kNumMods * kMTB + tid, kMTB,
+                                                   jb.N, tabs + J * tstride, mag);
+          __syncthreads();   // buffer J & 1 is refilled by the prefetch of job J + 2
+        } else {
+          neg = crt_reconstruct<K, RES8, 16>(
+              elem_ptr<RES8>(jb.G, static_cast<int64_t>(i) * jb.gpitch + j), jb.gplane, jb.N,
+              tabs + J * tstride, mag);
+        }
+        const int shift = -(jb.srow[i] + jb.scol[j]) - ebase;
+        const int q0 = shift >> 5, r = shift & 31;
+        if (q0 + K + 1 > win) atomicOr(status, 2);
+    #pragma unroll
+        for (int p = 0; p < K; ++p) {
+          uint64_t v = static_cast<uint64_t>(mag[p]) << r;
+          int64_t lo = static_cast<int64_t>(v & 0xffffffffull), hi = static_cast<int64_t>(v >> 32);
+          if (neg) {
+            lo = -lo;
+            hi = -hi;
+          }
+          if (q0 + p < win) WIN(q0 + p) += lo;
+          if (q0 + p + 1 < win) WIN(q0 + p + 1) += hi;
+        }
       }
-      __syncthreads();
-      neg = crt_reconstruct<K, RES8, 16, true>(sG + (J & 1) * kNumMods * kMTB + tid, kMTB,
-                                               jb.N, tabs + J * tstride, mag);
-      __syncthreads();   // buffer J & 1 is refilled by the prefetch of job J + 2
-    } else {
-      neg = crt_reconstruct<K, RES8, 16>(
-          elem_ptr<RES8>(jb.G, static_cast<int64_t>(i) * jb.gpitch + j), jb.gplane, jb.N,
-          tabs + J * tstride, mag);
-    }
-    const int shift = -(jb.srow[i] + jb.scol[j]) - ebase;
-    const int q0 = shift >> 5, r = shift & 31;
-    if (q0 + K + 1 > win) atomicOr(status, 2);
-#pragma unroll
-    for (int p = 0; p < K; ++p) {
-      uint64_t v = static_cast<uint64_t>(mag[p]) << r;
-      int64_t lo = static_cast<int64_t>(v & 0xffffffffull), hi = static_cast<int64_t>(v >> 32);
-      if (neg) {
-        lo = -lo;
-        hi = -hi;
+      auto normalize = [&]() -> bool {
+        int64_t carry = 0;
+        for (int q = 0; q < win; ++q) {
+          int64_t v = WIN(q) + carry;
+          carry = v >> 32;
+          WIN(q) = v - (carry << 32);
+        }
+        if (carry >= 0) return false;
+        int64_t c = 1;
+        for (int q = 0; q < win; ++q) {
+          int64_t v = (0xffffffffll - WIN(q)) + c;
+          c = v >> 32;
+          WIN(q) = v & 0xffffffffll;
+        }
+        return true;
+      };
+      bool neg = normalize();
+      double out[COMPS];
+      for (int c = 0; c < COMPS; ++c) {
+        // round-to-nearest of the magnitude
+        int top = win - 1;
+        while (top >= 0 && WIN(top) == 0) --top;
+        double d = 0.0;
+        if (top >= 0) {
+          uint64_t hi = static_cast<uint64_t>(WIN(top));
+          uint64_t mid = top >= 1 ? static_cast<uint64_t>(WIN(top - 1)) : 0;
+          uint64_t lo = top >= 2 ? static_cast<uint64_t>(WIN(top - 2)) : 0;
+          bool sticky = false;
+          for (int q = top - 3; q >= 0; --q) sticky |= (WIN(q) != 0);
+          int lz = __clzll(static_cast<long long>(hi)) - 32;
+          unsigned __int128 w = (static_cast<unsigned __int128>(hi) << 64) |
+                                (static_cast<unsigned __int128>(mid) << 32) | lo;
+          w <<= lz;
+          uint64_t top64 = static_cast<uint64_t>(w >> 32);
+          if ((static_cast<uint64_t>(w) & 0xffffffffull) != 0 || sticky) top64 |= 1ull;
+          d = ldexp(__ull2double_rn(top64), 32 * (top - 2) - lz + 32 + ebase);
+        }
+        out[c] = neg ? -d : d;
+        if (d != 0.0) {   // subtract d (a multiple of 2^ebase) from the magnitude
+          unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(d));
+          int be = static_cast<int>((b >> 52) & 0x7ff);
+          unsigned long long mm = b & ((1ull << 52) - 1);
+          if (be > 0) mm |= (1ull << 52);
+          int ee = (be > 0 ? be - 1075 : -1074) - ebase;
+          int tz = __ffsll(static_cast<long long>(mm)) - 1;
+          mm >>= tz;
+          ee += tz;
+          int q0 = ee >> 5, rr = ee & 31;
+          unsigned __int128 ww = static_cast<unsigned __int128>(mm) << rr;
+          for (int u = 0; u < 3; ++u)
+            if (q0 + u < win)
+              WIN(q0 + u) -= static_cast<int64_t>(static_cast<uint32_t>(ww >> (32 * u)));
+        }
+        neg = neg ^ normalize();
       }
-      if (q0 + p < win) WIN(q0 + p) += lo;
-      if (q0 + p + 1 < win) WIN(q0 + p + 1) += hi;
-    }
+    #undef WIN
+      bool bad = false;
+      for (int c = 0; c < COMPS; ++c) {
+        C[e * COMPS + c] = out[c];
+        bad |= !isfinite(out[c]);
+      }
+      if (bad) atomicOr(status, 1);
+    }();
   }
-  auto normalize = [&]() -> bool {
-    int64_t carry = 0;
-    for (int q = 0; q < win; ++q) {
-      int64_t v = WIN(q) + carry;
-      carry = v >> 32;
-      WIN(q) = v - (carry << 32);
-    }
-    if (carry >= 0) return false;
-    int64_t c = 1;
-    for (int q = 0; q < win; ++q) {
-      int64_t v = (0xffffffffll - WIN(q)) + c;
-      c = v >> 32;
-      WIN(q) = v & 0xffffffffll;
-    }
-    return true;
-  };
-  bool neg = normalize();
-  double out[COMPS];
-  for (int c = 0; c < COMPS; ++c) {
-    // round-to-nearest of the magnitude
-    int top = win - 1;
-    while (top >= 0 && WIN(top) == 0) --top;
-    double d = 0.0;
-    if (top >= 0) {
-      uint64_t hi = static_cast<uint64_t>(WIN(top));
-      uint64_t mid = top >= 1 ? static_cast<uint64_t>(WIN(top - 1)) : 0;
-      uint64_t lo = top >= 2 ? static_cast<uint64_t>(WIN(top - 2)) : 0;
-      bool sticky = false;
-      for (int q = top - 3; q >= 0; --q) sticky |= (WIN(q) != 0);
-      int lz = __clzll(static_cast<long long>(hi)) - 32;
-      unsigned __int128 w = (static_cast<unsigned __int128>(hi) << 64) |
-                            (static_cast<unsigned __int128>(mid) << 32) | lo;
-      w <<= lz;
-      uint64_t top64 = static_cast<uint64_t>(w >> 32);
-      if ((static_cast<uint64_t>(w) & 0xffffffffull) != 0 || sticky) top64 |= 1ull;
-      d = ldexp(__ull2double_rn(top64), 32 * (top - 2) - lz + 32 + ebase);
-    }
-    out[c] = neg ? -d : d;
-    if (d != 0.0) {   // subtract d (a multiple of 2^ebase) from the magnitude
-      unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(d));
-      int be = static_cast<int>((b >> 52) & 0x7ff);
-      unsigned long long mm = b & ((1ull << 52) - 1);
-      if (be > 0) mm |= (1ull << 52);
-      int ee = (be > 0 ? be - 1075 : -1074) - ebase;
-      int tz = __ffsll(static_cast<long long>(mm)) - 1;
-      mm >>= tz;
-      ee += tz;
-      int q0 = ee >> 5, rr = ee & 31;
-      unsigned __int128 ww = static_cast<unsigned __int128>(mm) << rr;
-      for (int u = 0; u < 3; ++u)
-        if (q0 + u < win)
-          WIN(q0 + u) -= static_cast<int64_t>(static_cast<uint32_t>(ww >> (32 * u)));
-    }
-    neg = neg ^ normalize();
-  }
-#undef WIN
-  bool bad = false;
-  for (int c = 0; c < COMPS; ++c) {
-    C[e * COMPS + c] = out[c];
-    bad |= !isfinite(out[c]);
-  }
-  if (bad) atomicOr(status, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -1157,13 +1410,63 @@ cudaError_t oz_residues_launch(int by_cols, const double* X, int64_t ld, int row
   }
 }
 
+// MPMM_COMBINE=cuda selects the CUDA-core CRT sums (A/B tests); default:
+// the tensor-core sums (combine_mma_kernel).
+static bool combine_on_cuda_cores() {
+  static const bool v = [] {
+    const char* e = std::getenv("MPMM_COMBINE");
+    return e != nullptr && std::strcmp(e, "cuda") == 0;
+  }();
+  return v;
+}
+
+template <int COMPS, bool RES8>
+static cudaError_t combine_mma(const CrtJob& jb, int m, int n, double* C, int* status,
+                               unsigned blocks, cudaStream_t s) {
+  switch (jb.K) {
+#define MPMM_K(KK)                                                                        \
+  case KK: {                                                                              \
+    auto kern = combine_mma_kernel<COMPS, KK, RES8>;                                      \
+    const int smem = MmaLayout<KK>::BYTES;                                                \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);        \
+    int dev = 0, sms = 148, occ = 1;                                                      \
+    cudaGetDevice(&dev);                                                                  \
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);                    \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, smem);                 \
+    const unsigned grid = std::min<unsigned>(blocks, (unsigned)(sms * (occ > 0 ? occ : 1))); \
+    kern<<<grid, 128, smem, s>>>(jb, m, n, C, status);                                    \
+    break;                                                                                \
+  }
+    MPMM_K(1) MPMM_K(2) MPMM_K(3) MPMM_K(4) MPMM_K(5) MPMM_K(6) MPMM_K(7) MPMM_K(8) MPMM_K(9)
+    MPMM_K(10) MPMM_K(11) MPMM_K(12)
+#undef MPMM_K
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 template <int COMPS, bool RES8>
 static cudaError_t combine_single(const CrtJob& jb, int m, int n, double* C, int* status,
                                   unsigned blocks, cudaStream_t s) {
+  // the tensor-core sums for byte residues; int32 products (cuBLASLt planes)
+  // keep the CUDA-core kernel, which interleaves their Barrett reductions
+  // with the sums (measured faster)
+  if (RES8 && !combine_on_cuda_cores())
+    return combine_mma<COMPS, RES8>(jb, m, n, C, status, blocks, s);
   switch (jb.K) {
 #define MPMM_K(KK) \
   case KK:         \
-    combine_single_kernel<COMPS, KK, RES8><<<blocks, 128, 0, s>>>(jb, m, n, C, status); break;
+    {                                                                                    \
+      auto kern = combine_single_kernel<COMPS, KK, RES8>;                                \
+      int dev = 0, sms = 148, occ = 1;                                                   \
+      cudaGetDevice(&dev);                                                               \
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);                 \
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, 0);                 \
+      kern<<<std::min<unsigned>(blocks, (unsigned)(sms * (occ > 0 ? occ : 1))), 128, 0, s>>>( \
+          jb, m, n, C, status);                                                          \
+    }                                                                                    \
+    break;
     MPMM_K(1) MPMM_K(2) MPMM_K(3) MPMM_K(4) MPMM_K(5) MPMM_K(6) MPMM_K(7) MPMM_K(8) MPMM_K(9)
     MPMM_K(10) MPMM_K(11) MPMM_K(12)
 #undef MPMM_K
@@ -1183,10 +1486,16 @@ static cudaError_t combine_multi(const CrtJobs& jobs, int njobs, int K, int win,
   switch (K) {
 #define MPMM_K(KK)                                                                            \
   case KK:                                                                                    \
-    cudaFuncSetAttribute(combine_multi_kernel<COMPS, KK, RES8>,                               \
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
-    combine_multi_kernel<COMPS, KK, RES8><<<blocks, kMTB, smem, s>>>(jobs, njobs, win, m, n,  \
-                                                                     C, status);              \
+  {                                                                                           \
+    auto kern = combine_multi_kernel<COMPS, KK, RES8>;                                        \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
+    int dev = 0, sms = 148, occ = 1;                                                          \
+    cudaGetDevice(&dev);                                                                      \
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);                        \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kMTB, smem);                    \
+    kern<<<std::min<unsigned>(blocks, (unsigned)(sms * (occ > 0 ? occ : 1))), kMTB, smem, s>>>( \
+        jobs, njobs, win, m, n, C, status);                                                   \
+  }                                                                                           \
     break;
     MPMM_K(1) MPMM_K(2) MPMM_K(3) MPMM_K(4) MPMM_K(5) MPMM_K(6) MPMM_K(7) MPMM_K(8) MPMM_K(9)
     MPMM_K(10) MPMM_K(11) MPMM_K(12)
