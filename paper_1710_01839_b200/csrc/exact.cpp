@@ -175,10 +175,13 @@ struct Pads {
 };
 
 // Measured (B200, 39 moduli): the tcgen05 kernel beats cuBLASLt's int8
-// GEMM up to 2048^3 per plane (1024^3: 46 vs 60 us), cuBLASLt is ahead from
-// 4096^3 (1.80 vs 1.69 ms): switch by the per-plane work.
-constexpr double kTcMaxWork = 2048.0 * 2048.0 * 2048.0;
-
+// GEMM up to 2048^3 per plane (1024^3: 46 vs 60 us) and trails it from
+// 4096^3 (1.80 vs 1.69 ms) -- but it writes the residues as bytes, which
+// the tensor-core CRT combine consumes, where cuBLASLt writes int32 planes
+// (4x the HBM traffic, and the CUDA-core combine).  End to end the tcgen05
+// path wins at every size measured (DD 4096^3 3.94 vs 4.50 ms, 8192^3 26.2
+// vs 29.3 ms; QD 4096^3 17.0 vs 17.7 ms), so cuBLASLt is the fallback for
+// shapes the tcgen05 kernel does not take.
 Pads pads_for(int64_t m, int64_t l, int64_t n) {
   const int64_t tn = tc_residue_gemm_tile_n();
   Pads p{false, pad_to(m, 16), pad_to(n, 16), pad_to(l, 16)};
@@ -186,8 +189,7 @@ Pads pads_for(int64_t m, int64_t l, int64_t n) {
     const char* env = std::getenv("MPMM_EXACT_GEMM");   // "tc" / "lt" (measurement knob)
     return env == nullptr ? 0 : (env[0] == 't' ? 1 : (env[0] == 'l' ? 2 : 0));
   }();
-  const bool small = static_cast<double>(m) * n * l <= kTcMaxWork;
-  if (force != 2 && (small || force == 1) &&
+  if (force != 2 &&
       tc_residue_gemm_supported(pad_to(m, 128), pad_to(n, tn), pad_to(l, 128)))
     p = Pads{true, pad_to(m, 128), pad_to(n, tn), pad_to(l, 128)};
   return p;

@@ -150,7 +150,7 @@ def test_graph_replay_same_operands_and_in_place_change(gpu):
 
 @pytest.mark.parametrize("tok,n", [("dd", 4096), ("qd", 2048), ("dd", 1000)])
 def test_large_and_unaligned_sampled_exact(gpu, tok, n):
-    """Beyond the tcgen05 size limit (cuBLASLt residue products, DD 4096)
+    """Large sizes (DD 4096: cluster-pair tcgen05 residue GEMMs)
     and with padded tiles (1000 is no multiple of 128/256): sampled entries
     against the exact superaccumulator verifier; a correctly rounded
     result uses at most ~2^-104 / (4 l 2^-104) of the bound."""
@@ -181,3 +181,36 @@ def test_nonfinite_and_empty(gpu):
     a, b = inputs.gemm_inputs("dd", 9, 7, 5, seed=4)
     c = tensor.matmul_exact_tensors(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
     assert list(c.cpu().numpy()[0, 0]) == _rn_expansion(_exact_entry(a, b, 0, 0), 2)
+
+
+_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_1710_01839_b200 import inputs, tensor
+tok, n, out = sys.argv[2], int(sys.argv[3]), sys.argv[4]
+A, B = inputs.gemm_inputs_device(tok, n, n, n, seed=5)
+np.save(out, tensor.matmul_exact_tensors(A, B).cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("env", [{"MPMM_EXACT_GEMM": "lt"}, {"MPMM_COMBINE": "cuda"},
+                                 {"MPMM_EXACT_GEMM": "lt", "MPMM_COMBINE": "cuda"}])
+@pytest.mark.parametrize("tok,n", [("dd", 512), ("qd", 256)])
+def test_fallback_paths_bit_identical(gpu, tmp_path, env, tok, n):
+    """The default path (tcgen05 residue GEMMs, byte residues, tensor-core
+    CRT sums) and the fallbacks (cuBLASLt int32 residue products; CUDA-core
+    CRT sums), forced in child processes: all return the exact product
+    rounded once, so the same bits."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for k, e in enumerate(({}, env)):
+        path = str(tmp_path / f"c{k}.npy")
+        r = subprocess.run([sys.executable, "-c", _CHILD, root, tok, str(n), path], cwd=root,
+                           env=dict(os.environ, **e), capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])
