@@ -997,9 +997,8 @@ __device__ __forceinline__ void mma_u8_16832(int (&d)[4], const uint32_t (&a)[4]
 // zero for t >= N or q >= K) and the head (P, P/2, 1/P) of one job.
 template <int K>
 __device__ __forceinline__ void stage_mma_tables(const uint32_t* __restrict__ table, int N,
-                                                 unsigned char* sm) {
+                                                 uint32_t* sWB, uint32_t* sH) {
   using L = MmaLayout<K>;
-  uint32_t* sWB = reinterpret_cast<uint32_t*>(sm + L::WB_OFF);
   for (int idx = threadIdx.x; idx < L::COLS * 16; idx += blockDim.x) {
     const int c = idx >> 4, w = idx & 15;
     const int q = c >> 2, b = c & 3;
@@ -1013,7 +1012,6 @@ __device__ __forceinline__ void stage_mma_tables(const uint32_t* __restrict__ ta
     sWB[c * L::AST + w] = v;
   }
   constexpr int PW = pwords(K);
-  uint32_t* sH = reinterpret_cast<uint32_t*>(sm + L::H_OFF);
   for (int q = threadIdx.x; q < PW; q += blockDim.x) {
     sH[q] = q < K ? table[q] : 0u;
     const uint32_t lo = q < K ? table[q] : 0u, hi = q + 1 < K ? table[q + 1] : 0u;
@@ -1051,13 +1049,30 @@ __device__ __forceinline__ void mma_prefetch(const CrtJob& jb, int64_t e0, int n
 // in `sm`: (neg, mag) exactly as crt_reconstruct returns them.  STAGED:
 // the residue bytes are already in the staging area (mma_prefetch, waited).
 // Every thread of the block must call it (warp-synchronous MMAs).
+struct MmaBufs {
+  const uint32_t* wb;      // the job's weight bytes [COLS][AST]
+  const uint32_t* head;    // the job's P, P/2, 1/P
+  uint32_t* a;             // [128][AST] residue rows
+  int* c;                  // [128][CST] sums
+  const unsigned char* stage;   // [kNumMods][128] staged residue bytes (staged path)
+};
+
+template <int K>
+__device__ __forceinline__ MmaBufs mma_bufs(unsigned char* sm) {
+  using L = MmaLayout<K>;
+  return MmaBufs{reinterpret_cast<const uint32_t*>(sm + L::WB_OFF),
+                 reinterpret_cast<const uint32_t*>(sm + L::H_OFF),
+                 reinterpret_cast<uint32_t*>(sm + L::A_OFF), reinterpret_cast<int*>(sm + L::C_OFF),
+                 sm + L::S_OFF};
+}
+
 template <int K, bool RES8>
 __device__ __forceinline__ bool crt_reconstruct_mma(const CrtJob& jb, bool staged, bool valid,
-                                                    int i, int j, unsigned char* sm,
+                                                    int i, int j, const MmaBufs& bf,
                                                     int64_t (&mag)[K]) {
   using L = MmaLayout<K>;
   const int o = threadIdx.x, lane = o & 31, warp = o >> 5;
-  uint32_t* sA = reinterpret_cast<uint32_t*>(sm + L::A_OFF);
+  uint32_t* sA = bf.a;
   // 1. this output's residues r_t (t < 64) as 16 words of sA row o
   {
     uint32_t w[16];
@@ -1065,7 +1080,7 @@ __device__ __forceinline__ bool crt_reconstruct_mma(const CrtJob& jb, bool stage
     for (int q = 0; q < 16; ++q) w[q] = 0u;
     const int N = jb.N;
     if (staged) {
-      const unsigned char* stage = sm + L::S_OFF;
+      const unsigned char* stage = bf.stage;
 #pragma unroll
       for (int t = 0; t < kNumMods; ++t)
         if (t < N) w[t >> 2] |= static_cast<uint32_t>(stage[t * 128 + o]) << (8 * (t & 3));
@@ -1092,7 +1107,7 @@ __device__ __forceinline__ bool crt_reconstruct_mma(const CrtJob& jb, bool stage
   }
   __syncwarp();
   // 2. S = R W on the tensor cores, this warp's 32 outputs
-  const uint32_t* sWB = reinterpret_cast<const uint32_t*>(sm + L::WB_OFF);
+  const uint32_t* sWB = bf.wb;
   int acc[2][L::NT][4];
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
@@ -1119,7 +1134,7 @@ __device__ __forceinline__ bool crt_reconstruct_mma(const CrtJob& jb, bool stage
     }
   }
   // 3. the sums to the owning thread
-  int* sC = reinterpret_cast<int*>(sm + L::C_OFF);
+  int* sC = bf.c;
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -1143,7 +1158,7 @@ __device__ __forceinline__ bool crt_reconstruct_mma(const CrtJob& jb, bool stage
     S[K] = 0;
   }
   __syncwarp();   // sA / sC rows are rewritten by the next job
-  return crt_finish<K>(S, reinterpret_cast<const uint32_t*>(sm + L::H_OFF), mag);
+  return crt_finish<K>(S, bf.head, mag);
 }
 
 template <int COMPS, int K, bool RES8>
@@ -1152,7 +1167,9 @@ combine_mma_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __restr
   extern __shared__ __align__(16) unsigned char smm[];
   using L = MmaLayout<K>;
   // persistent blocks: the tables are staged once per block, not per tile
-  stage_mma_tables<K>(jb.table, jb.N, smm);
+  stage_mma_tables<K>(jb.table, jb.N, reinterpret_cast<uint32_t*>(smm + L::WB_OFF),
+                      reinterpret_cast<uint32_t*>(smm + L::H_OFF));
+  const MmaBufs bf = mma_bufs<K>(smm);
   const bool staged = RES8 && mma_staged(jb, n);
   const int64_t total = static_cast<int64_t>(m) * n;
   const int64_t tiles = (total + 127) / 128;
@@ -1167,7 +1184,7 @@ combine_mma_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __restr
     const bool valid = e < total;
     const int i = valid ? static_cast<int>(e / n) : 0, j = valid ? static_cast<int>(e % n) : 0;
     int64_t mag[K];
-    const bool neg = crt_reconstruct_mma<K, RES8>(jb, staged, valid, i, j, smm, mag);
+    const bool neg = crt_reconstruct_mma<K, RES8>(jb, staged, valid, i, j, bf, mag);
     __syncthreads();   // the staging area is refilled for the next tile
     if (!valid) continue;
     bool bad = false;
@@ -1196,6 +1213,101 @@ combine_mma_kernel(CrtJob jb, int m, int n, double* __restrict__ C, int* __restr
 
 constexpr int kMTB = 128;     // threads per block
 constexpr int kMWin = 28;     // largest window (896 bits); the host passes what a plan needs
+
+// One job's reconstructed value (sign + K magnitude limbs, scaled by
+// 2^-(s_i + t_j)) added into the thread's exact window, digits of 32 bits
+// relative to 2^ebase; *status |= 2 when it does not fit.
+template <int K>
+__device__ __forceinline__ void window_add(int64_t* wbuf, int tid, int win, const CrtJob& jb,
+                                           int i, int j, int ebase, bool neg,
+                                           const int64_t (&mag)[K], int* status) {
+#define WIN(q) wbuf[(q) * kMTB + tid]
+  const int shift = -(jb.srow[i] + jb.scol[j]) - ebase;
+  const int q0 = shift >> 5, r = shift & 31;
+  if (q0 + K + 1 > win) atomicOr(status, 2);
+#pragma unroll
+  for (int p = 0; p < K; ++p) {
+    uint64_t v = static_cast<uint64_t>(mag[p]) << r;
+    int64_t lo = static_cast<int64_t>(v & 0xffffffffull), hi = static_cast<int64_t>(v >> 32);
+    if (neg) {
+      lo = -lo;
+      hi = -hi;
+    }
+    if (q0 + p < win) WIN(q0 + p) += lo;
+    if (q0 + p + 1 < win) WIN(q0 + p + 1) += hi;
+  }
+#undef WIN
+}
+
+// Normalise the window, round it to COMPS non-overlapping doubles (each the
+// round-to-nearest of the remaining magnitude), write them to C[e].
+template <int COMPS>
+__device__ __forceinline__ void window_round(int64_t* wbuf, int tid, int win, int ebase,
+                                             double* __restrict__ C, int64_t e, int* status) {
+#define WIN(q) wbuf[(q) * kMTB + tid]
+auto normalize = [&]() -> bool {
+  int64_t carry = 0;
+  for (int q = 0; q < win; ++q) {
+    int64_t v = WIN(q) + carry;
+    carry = v >> 32;
+    WIN(q) = v - (carry << 32);
+  }
+  if (carry >= 0) return false;
+  int64_t c = 1;
+  for (int q = 0; q < win; ++q) {
+    int64_t v = (0xffffffffll - WIN(q)) + c;
+    c = v >> 32;
+    WIN(q) = v & 0xffffffffll;
+  }
+  return true;
+};
+bool neg = normalize();
+double out[COMPS];
+for (int c = 0; c < COMPS; ++c) {
+  // round-to-nearest of the magnitude
+  int top = win - 1;
+  while (top >= 0 && WIN(top) == 0) --top;
+  double d = 0.0;
+  if (top >= 0) {
+    uint64_t hi = static_cast<uint64_t>(WIN(top));
+    uint64_t mid = top >= 1 ? static_cast<uint64_t>(WIN(top - 1)) : 0;
+    uint64_t lo = top >= 2 ? static_cast<uint64_t>(WIN(top - 2)) : 0;
+    bool sticky = false;
+    for (int q = top - 3; q >= 0; --q) sticky |= (WIN(q) != 0);
+    int lz = __clzll(static_cast<long long>(hi)) - 32;
+    unsigned __int128 w = (static_cast<unsigned __int128>(hi) << 64) |
+                          (static_cast<unsigned __int128>(mid) << 32) | lo;
+    w <<= lz;
+    uint64_t top64 = static_cast<uint64_t>(w >> 32);
+    if ((static_cast<uint64_t>(w) & 0xffffffffull) != 0 || sticky) top64 |= 1ull;
+    d = ldexp(__ull2double_rn(top64), 32 * (top - 2) - lz + 32 + ebase);
+  }
+  out[c] = neg ? -d : d;
+  if (d != 0.0) {   // subtract d (a multiple of 2^ebase) from the magnitude
+    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(d));
+    int be = static_cast<int>((b >> 52) & 0x7ff);
+    unsigned long long mm = b & ((1ull << 52) - 1);
+    if (be > 0) mm |= (1ull << 52);
+    int ee = (be > 0 ? be - 1075 : -1074) - ebase;
+    int tz = __ffsll(static_cast<long long>(mm)) - 1;
+    mm >>= tz;
+    ee += tz;
+    int q0 = ee >> 5, rr = ee & 31;
+    unsigned __int128 ww = static_cast<unsigned __int128>(mm) << rr;
+    for (int u = 0; u < 3; ++u)
+      if (q0 + u < win)
+        WIN(q0 + u) -= static_cast<int64_t>(static_cast<uint32_t>(ww >> (32 * u)));
+  }
+  neg = neg ^ normalize();
+}
+#undef WIN
+bool bad = false;
+for (int c = 0; c < COMPS; ++c) {
+  C[e * COMPS + c] = out[c];
+  bad |= !isfinite(out[c]);
+}
+if (bad) atomicOr(status, 1);
+}
 
 template <int COMPS, int K, bool RES8>
 __global__ void __launch_bounds__(kMTB)
@@ -1260,86 +1372,14 @@ combine_multi_kernel(const CrtJobs jobs, int njobs, int win, int m, int n,
               elem_ptr<RES8>(jb.G, static_cast<int64_t>(i) * jb.gpitch + j), jb.gplane, jb.N,
               tabs + J * tstride, mag);
         }
-        const int shift = -(jb.srow[i] + jb.scol[j]) - ebase;
-        const int q0 = shift >> 5, r = shift & 31;
-        if (q0 + K + 1 > win) atomicOr(status, 2);
-    #pragma unroll
-        for (int p = 0; p < K; ++p) {
-          uint64_t v = static_cast<uint64_t>(mag[p]) << r;
-          int64_t lo = static_cast<int64_t>(v & 0xffffffffull), hi = static_cast<int64_t>(v >> 32);
-          if (neg) {
-            lo = -lo;
-            hi = -hi;
-          }
-          if (q0 + p < win) WIN(q0 + p) += lo;
-          if (q0 + p + 1 < win) WIN(q0 + p + 1) += hi;
-        }
-      }
-      auto normalize = [&]() -> bool {
-        int64_t carry = 0;
-        for (int q = 0; q < win; ++q) {
-          int64_t v = WIN(q) + carry;
-          carry = v >> 32;
-          WIN(q) = v - (carry << 32);
-        }
-        if (carry >= 0) return false;
-        int64_t c = 1;
-        for (int q = 0; q < win; ++q) {
-          int64_t v = (0xffffffffll - WIN(q)) + c;
-          c = v >> 32;
-          WIN(q) = v & 0xffffffffll;
-        }
-        return true;
-      };
-      bool neg = normalize();
-      double out[COMPS];
-      for (int c = 0; c < COMPS; ++c) {
-        // round-to-nearest of the magnitude
-        int top = win - 1;
-        while (top >= 0 && WIN(top) == 0) --top;
-        double d = 0.0;
-        if (top >= 0) {
-          uint64_t hi = static_cast<uint64_t>(WIN(top));
-          uint64_t mid = top >= 1 ? static_cast<uint64_t>(WIN(top - 1)) : 0;
-          uint64_t lo = top >= 2 ? static_cast<uint64_t>(WIN(top - 2)) : 0;
-          bool sticky = false;
-          for (int q = top - 3; q >= 0; --q) sticky |= (WIN(q) != 0);
-          int lz = __clzll(static_cast<long long>(hi)) - 32;
-          unsigned __int128 w = (static_cast<unsigned __int128>(hi) << 64) |
-                                (static_cast<unsigned __int128>(mid) << 32) | lo;
-          w <<= lz;
-          uint64_t top64 = static_cast<uint64_t>(w >> 32);
-          if ((static_cast<uint64_t>(w) & 0xffffffffull) != 0 || sticky) top64 |= 1ull;
-          d = ldexp(__ull2double_rn(top64), 32 * (top - 2) - lz + 32 + ebase);
-        }
-        out[c] = neg ? -d : d;
-        if (d != 0.0) {   // subtract d (a multiple of 2^ebase) from the magnitude
-          unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(d));
-          int be = static_cast<int>((b >> 52) & 0x7ff);
-          unsigned long long mm = b & ((1ull << 52) - 1);
-          if (be > 0) mm |= (1ull << 52);
-          int ee = (be > 0 ? be - 1075 : -1074) - ebase;
-          int tz = __ffsll(static_cast<long long>(mm)) - 1;
-          mm >>= tz;
-          ee += tz;
-          int q0 = ee >> 5, rr = ee & 31;
-          unsigned __int128 ww = static_cast<unsigned __int128>(mm) << rr;
-          for (int u = 0; u < 3; ++u)
-            if (q0 + u < win)
-              WIN(q0 + u) -= static_cast<int64_t>(static_cast<uint32_t>(ww >> (32 * u)));
-        }
-        neg = neg ^ normalize();
+        window_add<K>(wbuf, tid, win, jb, i, j, ebase, neg, mag, status);
       }
     #undef WIN
-      bool bad = false;
-      for (int c = 0; c < COMPS; ++c) {
-        C[e * COMPS + c] = out[c];
-        bad |= !isfinite(out[c]);
-      }
-      if (bad) atomicOr(status, 1);
+      window_round<COMPS>(wbuf, tid, win, ebase, C, e, status);
     }();
   }
 }
+
 
 // ---------------------------------------------------------------------------
 // launchers
