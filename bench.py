@@ -383,8 +383,13 @@ def run_ours(args, rank, world, local_rank):
     Ah = DenseMatrix(n, n, prec, host_a)
     Bh = DenseMatrix(n, n, prec, host_b)
     if world == 1:
-        for _ in range(max(3, args.warmup)):   # warm: pools, streams, pinned cache
-            mp.matmul_block(Ah, Bh, args.nmin)
+        # warm: pools, streams, and the pinned-host cache in the loop's own
+        # pattern -- `ch` keeps the previous result alive while the next is
+        # allocated, so the steady state holds two page-locked results (the
+        # second cudaHostAlloc, ~7 ms, would otherwise land in the timed loop)
+        ch = None
+        for _ in range(max(3, args.warmup)):
+            ch = mp.matmul_block(Ah, Bh, args.nmin)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
@@ -392,8 +397,8 @@ def run_ours(args, rank, world, local_rank):
         e2e_s = time.perf_counter() - t0
     else:
         for _ in range(max(3, args.warmup)):
-            shard.sharded_matmul_host(host_a, host_b if rank == 0 else None, n, n, prec,
-                                      n_min=args.nmin)
+            ch = shard.sharded_matmul_host(host_a, host_b if rank == 0 else None, n, n, prec,
+                                           n_min=args.nmin)
         dist.barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
@@ -431,7 +436,8 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": e2e_value, "unit": "2mnl/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps,
                 "api": "paper_1710_01839_b200.matmul_block(host, host) -> C-ABI mpmm_gemm_host "
-                       "(k-panel H2D overlapped with the GEMM)" if world == 1 else
+                       "(one GEMM launch consuming 64-column k-panels as their H2D lands, C "
+                       "written to the page-locked result from the epilogues)" if world == 1 else
                        "shard.sharded_matmul_host"},
         "roofline": roofline,
         "gpu_launches": gemm_launches,

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -166,6 +167,97 @@ int block_cells_impl(int comps, int64_t n_min, int64_t cell0, int64_t cell1, int
   return rect(ib1 * n_min, (ib1 + 1) * n_min, 0, (jb1 + 1) * n_min);
 }
 
+// ---------------------------------------------------------------------------
+// Streamed host product: ONE GEMM launch whose CTAs consume k-panels as
+// their H2D copies land, writing C straight into the caller's page-locked
+// buffer.  The copy stream copies A/B panel by panel and after each sets
+// the panel's ready flag with a 4-byte copy from page-locked memory (copy
+// engine, no kernel, so the GEMM CTAs spinning on the flags can never
+// block it); the GEMM (gemm_tiled, wait_k_panel) needs no event between the
+// streams, so the only exposed copy is the first 64-column panel, there is
+// one launch tail instead of one per panel, and C leaves over PCIe from the
+// epilogues while later tiles compute.  Per element the k order is the
+// same (bit-identical).  Used when A, B and C are page-locked; otherwise
+// the panelled path below.
+// ---------------------------------------------------------------------------
+
+// A page-locked 1: the source of every panel flag.  A 4-byte H2D copy
+// from it runs on the copy engine, never on an SM, so the GEMM CTAs
+// spinning on the flags cannot block it (a memset or a kernel could be).
+const int* pinned_one() {
+  static int* one = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    if (const char* env = std::getenv("MPMM_HOST_STREAMED"))   // measurement knob: 0 = off
+      if (env[0] == '0') return;
+    int* p = nullptr;
+    if (cudaHostAlloc(reinterpret_cast<void**>(&p), sizeof(int), cudaHostAllocDefault) ==
+        cudaSuccess) {
+      *p = 1;
+      one = p;
+    } else {
+      cudaGetLastError();
+    }
+  });
+  return one;
+}
+
+// page-locked host memory: its device alias (nullptr otherwise)
+void* pinned_alias(const void* host) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, host) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
+constexpr int64_t kStreamPanel = 64;   // k columns per streamed panel
+
+// MPMM_OK, an error, or -1: not applicable (the caller takes the panelled path)
+int host_rows_gemm_streamed(int comps, int tile, int64_t rows, int64_t l, int64_t n,
+                            const double* a_rows, const double* b, double* c_rows,
+                            int* nonfinite_host, HostStreams* hs) {
+  const int* one = pinned_one();
+  if (one == nullptr || tile == TILE_LPT || l < 2 * kStreamPanel) return -1;
+  if (pinned_alias(a_rows) == nullptr || pinned_alias(b) == nullptr) return -1;
+  double* dCh = static_cast<double*>(pinned_alias(c_rows));
+  if (dCh == nullptr) return -1;
+  const size_t el = comps * sizeof(double);
+  const int npan = static_cast<int>((l + kStreamPanel - 1) / kStreamPanel);
+  DevBuf dA, dB;
+  int* dint = nullptr;   // [0]: non-finite flag, [1 .. npan]: panel flags
+  CU(dA.alloc(rows * l * comps, hs->comp));
+  CU(dB.alloc(l * n * comps, hs->comp));
+  CU(cudaMallocAsync(reinterpret_cast<void**>(&dint), (npan + 1) * sizeof(int), hs->comp));
+  CU(cudaMemsetAsync(dint, 0, (npan + 1) * sizeof(int), hs->comp));
+  Event ready;
+  CU(ready.make());
+  CU(cudaEventRecord(ready.e, hs->comp));
+  CU(cudaStreamWaitEvent(hs->copy, ready.e, 0));
+  for (int p = 0; p < npan; ++p) {
+    const int64_t k0 = p * kStreamPanel, k1 = std::min<int64_t>(l, k0 + kStreamPanel);
+    CU(cudaMemcpy2DAsync(dA.p + k0 * comps, l * el, a_rows + k0 * comps, l * el, (k1 - k0) * el,
+                         rows, cudaMemcpyHostToDevice, hs->copy));
+    CU(cudaMemcpyAsync(dB.p + k0 * n * comps, b + k0 * n * comps, (k1 - k0) * n * el,
+                       cudaMemcpyHostToDevice, hs->copy));
+    CU(cudaMemcpyAsync(dint + 1 + p, one, sizeof(int), cudaMemcpyHostToDevice, hs->copy));
+  }
+  GemmArgs g{ALGO_BLOCK, tile, (int)rows, (int)n, (int)l, dA.p, l, dB.p, n, dCh, n, 0, dint,
+             hs->comp};
+  g.kready = dint + 1;
+  g.kpanel = static_cast<int>(kStreamPanel);
+  CU(gemm(comps, g));
+  int status = 0;   // pageable target: the copy completes before cudaMemcpyAsync returns
+  CU(cudaMemcpyAsync(&status, dint, sizeof(int), cudaMemcpyDeviceToHost, hs->comp));
+  CU(cudaFreeAsync(dint, hs->comp));
+  CU(cudaStreamSynchronize(hs->copy));
+  CU(cudaStreamSynchronize(hs->comp));
+  if (status & 4) return fail(MPMM_ERR_CUDA, "streamed product: an operand panel never landed");
+  if (nonfinite_host) *nonfinite_host = status & 1;
+  return MPMM_OK;
+}
+
 // rows x n block of C (host, row pitch n) = A rows (host, pitch l) * B
 // (host, l x n), through the device, with the H2D of A and B split into
 // k-panels on the copy stream so the GEMM of panel p overlaps the copy of
@@ -179,6 +271,13 @@ int host_rows_gemm(int comps, int algo, int64_t n_min, int64_t rows, int64_t l, 
   if (rows == 0 || n == 0) return MPMM_OK;
   HostStreams* hs = nullptr;
   CU(host_streams(&hs));
+  if (algo == ALGO_BLOCK && !accumulate_c) {
+    int tile0 = TILE_16, super0 = 1;
+    tile_for(n_min, &tile0, &super0);
+    const int rc = host_rows_gemm_streamed(comps, tile0, rows, l, n, a_rows, b, c_rows,
+                                           nonfinite_host, hs);
+    if (rc != -1) return rc;
+  }
   const size_t el = comps * sizeof(double);
   int* dflag = nullptr;
   if (nonfinite_host) {

@@ -80,12 +80,46 @@ struct TileSmem {
   static constexpr int TOTAL = 2 * (A_STAGE + B_STAGE);
 };
 
+// Streamed operands: k-panel q (kpanel columns of k) is readable once
+// flags[q] != 0; flags[-1] is the launch's status word.  The flags are
+// written by the copy stream (a 4-byte copy-engine H2D) after the panel's
+// H2D, so a CTA spinning here never waits on another kernel; the operand
+// tiles are then read through L2 (cp.async.cg), where the DMA writes land.
+struct KReady {
+  const int* flags;
+  int panel_k;
+};
+
+__device__ __forceinline__ void wait_k_panel(const KReady& kr, int k0, int& seen) {
+  if (kr.flags == nullptr) return;
+  const int q = k0 / kr.panel_k;
+  if (q <= seen) return;
+  if (threadIdx.x == 0) {
+    // bounded: a panel that never lands (a broken copy stream) sets bit 2 of
+    // the word before the flags and lets the kernel finish instead of
+    // hanging the GPU; the host reports it as an error
+    const volatile int* f = kr.flags + q;
+    const long long t0 = clock64();
+    while (*f == 0) {
+      __nanosleep(200);
+      if (clock64() - t0 > (1ll << 35)) {   // ~17 s at 1.965 GHz
+        atomicOr(const_cast<int*>(kr.flags) - 1, 4);
+        break;
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  seen = q;
+}
+
 // One CTA computes the BM x BN output tile at (m0, n0) of problem `pr`.
 // NT threads: thread (tx, ty) owns rows ty + r*NTY, cols tx + c*NTX.
 // accumulate: the accumulator starts at C's value (read through L2).
 template <class Ops, int BM, int BN, int BK, int TM, int TN, int NT>
 __device__ __forceinline__ void gemm_tile(const Prob& pr, int m, int n, int l, int accumulate,
-                                          int m0, int n0, double2* smem, bool& bad) {
+                                          int m0, int n0, double2* smem, bool& bad,
+                                          const KReady kr = KReady{nullptr, 0}) {
   constexpr int V = Ops::V;
   constexpr int NTX = BN / TN, NTY = BM / TM;
   static_assert(NTX * NTY == NT, "thread tile does not cover the CTA tile");
@@ -139,13 +173,16 @@ __device__ __forceinline__ void gemm_tile(const Prob& pr, int m, int n, int l, i
     }
   };
 
+  int seen = -1;   // highest k-panel known to have landed (streamed operands)
   if (ktiles > 0) {
+    wait_k_panel(kr, 0, seen);
     load(0, 0);
     cp_async_commit();
   }
   for (int kt = 0; kt < ktiles; ++kt) {
     const int st = kt & 1;
     if (kt + 1 < ktiles) {
+      wait_k_panel(kr, (kt + 1) * BK, seen);
       load(kt + 1, st ^ 1);
       cp_async_commit();
       cp_async_wait<1>();
@@ -198,7 +235,7 @@ __device__ __forceinline__ void gemm_tile(const Prob& pr, int m, int n, int l, i
 template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
 gemm_tiled(const GemmProblem* __restrict__ probs, Prob single, int m, int n, int l,
-           int accumulate, int* __restrict__ nonfinite) {
+           int accumulate, int* __restrict__ nonfinite, const KReady kr) {
   constexpr int NT = (BM / TM) * (BN / TN);
   __shared__ __align__(16) double2 smem[TileSmem<Ops, BM, BN, BK>::TOTAL];
   const int tiles_n = (n + BN - 1) / BN, tiles_m = (m + BM - 1) / BM;
@@ -207,7 +244,7 @@ gemm_tiled(const GemmProblem* __restrict__ probs, Prob single, int m, int n, int
   const Prob pr = get_prob(probs, single, p);
   bool bad = false;
   gemm_tile<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, (t / tiles_n) * BM,
-                                         (t % tiles_n) * BN, smem, bad);
+                                         (t % tiles_n) * BN, smem, bad, kr);
   if (nonfinite != nullptr && bad) atomicOr(nonfinite, 1);
 }
 
@@ -308,7 +345,8 @@ cudaError_t launch_tiled(const GemmArgs& g) {
   if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
   gemm_tiled<Ops, BM, BN, BK, TM, TN, MINB><<<(unsigned)tiles, (BM / TM) * (BN / TN), 0,
                                                g.stream>>>(g.probs, single_prob(g), g.m, g.n,
-                                                           g.l, g.accumulate, g.nonfinite);
+                                                           g.l, g.accumulate, g.nonfinite,
+                                                           KReady{g.kready, g.kpanel});
   return cudaGetLastError();
 }
 

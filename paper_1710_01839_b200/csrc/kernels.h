@@ -39,6 +39,11 @@ struct GemmArgs {
   cudaStream_t stream;
   int batch = 1;                         // number of problems
   const GemmProblem* probs = nullptr;    // device array of `batch` problems, or null: A/B/C above
+  // Streamed operands (gemm_tiled only): k-panel q of A and B is usable once
+  // kready[q] != 0 (set by the copy stream after the panel's H2D); panels
+  // are kpanel columns of k.  Null: the operands are already resident.
+  const int* kready = nullptr;
+  int kpanel = 0;
 };
 
 cudaError_t dd_gemm_launch(const GemmArgs& g);
