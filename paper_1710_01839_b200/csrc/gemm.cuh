@@ -231,8 +231,10 @@ __device__ __forceinline__ void gemm_tile(const Prob& pr, int m, int n, int l, i
     }
 }
 
-// Plain tiled kernel: one CTA per (problem, tile).
-template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB>
+// Plain tiled kernel: one CTA per (problem, tile).  STREAM: the operands
+// arrive while it runs (wait_k_panel); a separate instantiation, so the
+// resident-operand kernel keeps its code unchanged.
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB, bool STREAM = false>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
 gemm_tiled(const GemmProblem* __restrict__ probs, Prob single, int m, int n, int l,
            int accumulate, int* __restrict__ nonfinite, const KReady kr) {
@@ -244,7 +246,8 @@ gemm_tiled(const GemmProblem* __restrict__ probs, Prob single, int m, int n, int
   const Prob pr = get_prob(probs, single, p);
   bool bad = false;
   gemm_tile<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, (t / tiles_n) * BM,
-                                         (t % tiles_n) * BN, smem, bad, kr);
+                                         (t % tiles_n) * BN, smem, bad,
+                                         STREAM ? kr : KReady{nullptr, 0});
   if (nonfinite != nullptr && bad) atomicOr(nonfinite, 1);
 }
 
@@ -343,10 +346,14 @@ cudaError_t launch_tiled(const GemmArgs& g) {
   int64_t tiles = (int64_t)((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN) * g.batch;
   if (tiles == 0) return cudaSuccess;
   if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
-  gemm_tiled<Ops, BM, BN, BK, TM, TN, MINB><<<(unsigned)tiles, (BM / TM) * (BN / TN), 0,
-                                               g.stream>>>(g.probs, single_prob(g), g.m, g.n,
-                                                           g.l, g.accumulate, g.nonfinite,
-                                                           KReady{g.kready, g.kpanel});
+  const unsigned grid = (unsigned)tiles, nt = (BM / TM) * (BN / TN);
+  const KReady kr{g.kready, g.kpanel};
+  if (g.kready != nullptr)
+    gemm_tiled<Ops, BM, BN, BK, TM, TN, MINB, true><<<grid, nt, 0, g.stream>>>(
+        g.probs, single_prob(g), g.m, g.n, g.l, g.accumulate, g.nonfinite, kr);
+  else
+    gemm_tiled<Ops, BM, BN, BK, TM, TN, MINB, false><<<grid, nt, 0, g.stream>>>(
+        g.probs, single_prob(g), g.m, g.n, g.l, g.accumulate, g.nonfinite, kr);
   return cudaGetLastError();
 }
 
