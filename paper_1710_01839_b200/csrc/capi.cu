@@ -235,19 +235,30 @@ int host_rows_gemm_streamed(int comps, int tile, int64_t rows, int64_t l, int64_
   CU(ready.make());
   CU(cudaEventRecord(ready.e, hs->comp));
   CU(cudaStreamWaitEvent(hs->copy, ready.e, 0));
-  for (int p = 0; p < npan; ++p) {
-    const int64_t k0 = p * kStreamPanel, k1 = std::min<int64_t>(l, k0 + kStreamPanel);
-    CU(cudaMemcpy2DAsync(dA.p + k0 * comps, l * el, a_rows + k0 * comps, l * el, (k1 - k0) * el,
-                         rows, cudaMemcpyHostToDevice, hs->copy));
-    CU(cudaMemcpyAsync(dB.p + k0 * n * comps, b + k0 * n * comps, (k1 - k0) * n * el,
-                       cudaMemcpyHostToDevice, hs->copy));
-    CU(cudaMemcpyAsync(dint + 1 + p, one, sizeof(int), cudaMemcpyHostToDevice, hs->copy));
-  }
+  // The GEMM is enqueued FIRST: its CTAs start as soon as the flags are
+  // zeroed and wait for each panel, so the ~50 copy/flag API calls below
+  // no longer delay the launch.
   GemmArgs g{ALGO_BLOCK, tile, (int)rows, (int)n, (int)l, dA.p, l, dB.p, n, dCh, n, 0, dint,
              hs->comp};
   g.kready = dint + 1;
   g.kpanel = static_cast<int>(kStreamPanel);
   CU(gemm(comps, g));
+  for (int p = 0; p < npan; ++p) {
+    const int64_t k0 = p * kStreamPanel, k1 = std::min<int64_t>(l, k0 + kStreamPanel);
+    cudaError_t e = cudaMemcpy2DAsync(dA.p + k0 * comps, l * el, a_rows + k0 * comps, l * el,
+                                      (k1 - k0) * el, rows, cudaMemcpyHostToDevice, hs->copy);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(dB.p + k0 * n * comps, b + k0 * n * comps, (k1 - k0) * n * el,
+                          cudaMemcpyHostToDevice, hs->copy);
+    if (e != cudaSuccess) {
+      // release the launched GEMM (it must not wait out its bound), then report
+      for (int q = p; q < npan; ++q)
+        cudaMemcpyAsync(dint + 1 + q, one, sizeof(int), cudaMemcpyHostToDevice, hs->copy);
+      cudaStreamSynchronize(hs->comp);
+      return cuda_fail(e, "streamed product: operand panel copy");
+    }
+    CU(cudaMemcpyAsync(dint + 1 + p, one, sizeof(int), cudaMemcpyHostToDevice, hs->copy));
+  }
   int status = 0;   // pageable target: the copy completes before cudaMemcpyAsync returns
   CU(cudaMemcpyAsync(&status, dint, sizeof(int), cudaMemcpyDeviceToHost, hs->comp));
   CU(cudaFreeAsync(dint, hs->comp));
