@@ -5,6 +5,7 @@
 // argument meaning on host pointers, and device-resident whole-GEMM /
 // elementwise entry points serve the multiply/predict/tune layers.
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -184,7 +185,13 @@ int block_cells_impl(int comps, int64_t n_min, int64_t cell0, int64_t cell1, int
 // A page-locked 1: the source of every panel flag.  A 4-byte H2D copy
 // from it runs on the copy engine, never on an SM, so the GEMM CTAs
 // spinning on the flags cannot block it (a memset or a kernel could be).
+// Set when a streamed product timed out waiting for a panel (a tool that
+// serialises kernels against the copy stream): later products take the
+// panelled path.
+std::atomic<bool> g_streamed_off{false};
+
 const int* pinned_one() {
+  if (g_streamed_off.load(std::memory_order_relaxed)) return nullptr;
   static int* one = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -264,7 +271,13 @@ int host_rows_gemm_streamed(int comps, int tile, int64_t rows, int64_t l, int64_
   CU(cudaFreeAsync(dint, hs->comp));
   CU(cudaStreamSynchronize(hs->copy));
   CU(cudaStreamSynchronize(hs->comp));
-  if (status & 4) return fail(MPMM_ERR_CUDA, "streamed product: an operand panel never landed");
+  if (status & 4) {
+    // the panels never landed while the GEMM waited (its result is
+    // incomplete): switch the process to the panelled path and let the
+    // caller recompute with it
+    g_streamed_off.store(true);
+    return -1;
+  }
   if (nonfinite_host) *nonfinite_host = status & 1;
   return MPMM_OK;
 }

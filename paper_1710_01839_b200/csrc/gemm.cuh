@@ -102,7 +102,7 @@ __device__ __forceinline__ void wait_k_panel(const KReady& kr, int k0, int& seen
     const long long t0 = clock64();
     while (*f == 0) {
       __nanosleep(200);
-      if (clock64() - t0 > (1ll << 35)) {   // ~17 s at 1.965 GHz
+      if (clock64() - t0 > (1ll << 32)) {   // ~2.2 s at 1.965 GHz
         atomicOr(const_cast<int*>(kr.flags) - 1, 4);
         break;
       }

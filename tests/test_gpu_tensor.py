@@ -214,3 +214,63 @@ def test_fallback_paths_bit_identical(gpu, tmp_path, env, tok, n):
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(path))
     assert np.array_equal(outs[0], outs[1])
+
+
+def _exact_scaled(x_comps, shift):
+    """sum of the components times 2^shift as an exact integer"""
+    from fractions import Fraction
+    v = sum(Fraction(float(c)) for c in x_comps) * (Fraction(2) ** shift)
+    assert v.denominator == 1
+    return v.numerator
+
+
+@pytest.mark.parametrize("by_cols", [0, 1])
+@pytest.mark.parametrize("tok", ["dd", "qd"])
+def test_residue_kernels_exact(gpu, by_cols, tok):
+    """mpmm_oz_residues_dev (the residue kernels) against exact
+    big-integer residues, centred into int8, for a ragged operand with
+    signs, zeros and a wide exponent spread: every byte."""
+    import torch
+    from paper_1710_01839_b200 import _cuda
+    from paper_1710_01839_b200.tensor import MODULI
+    comps = 2 if tok == "dd" else 4
+    rows, cols = 37, 150
+    a, _ = inputs.gemm_inputs(tok, rows, cols, 3, seed=21)
+    a[3, 7] = 0.0
+    a[5] *= 2.0 ** 40
+    a[:, 11] *= -1.0
+    X = torch.from_numpy(a).cuda()
+    # the shift makes every entry of a row (column) an integer: -min low bit
+    odim = cols if by_cols else rows
+    shifts = []
+    for o in range(odim):
+        vals = a[:, o] if by_cols else a[o]
+        low = min((int(np.frexp(v)[1]) - 53 for e in vals for v in e if v != 0.0), default=0)
+        shifts.append(-low)
+    sh = torch.tensor(shifts, dtype=torch.int32, device="cuda")
+    ints = [[_exact_scaled(a[r, c], shifts[c if by_cols else r]) for c in range(cols)]
+            for r in range(rows)]
+    bits = max(abs(v).bit_length() for row in ints for v in row) + 1
+    words = (bits + 31) // 32
+    N = 39
+    if by_cols:
+        R = torch.zeros((N, cols, rows + 11), dtype=torch.int8, device="cuda")   # pitch 48
+        rp, rpl = rows + 11, cols * (rows + 11)
+    else:
+        R = torch.zeros((N, rows, cols + 10), dtype=torch.int8, device="cuda")
+        rp, rpl = cols + 10, rows * (cols + 10)
+    _cuda.oz_residues_dev(by_cols, comps, 0, comps, rows, cols, X.data_ptr(), cols, sh.data_ptr(),
+                          N, words, R.data_ptr(), rp, rpl)
+    torch.cuda.synchronize()
+    got = R.cpu().numpy()
+    for t in range(N):
+        p = MODULI[t]
+        for r in range(rows):
+            for c in range(cols):
+                v = ints[r][c] % p
+                if v > p // 2:
+                    v -= p
+                if v > 127:
+                    v -= p
+                g = got[t, c, r] if by_cols else got[t, r, c]
+                assert g == v, (t, r, c, g, v)
