@@ -97,11 +97,14 @@ int mpmm_qd_ewise_sub(const double *x, const double *y, double *out, int64_t row
                       int64_t cols, int64_t i0, int64_t i1);
 
 /* Whole product on HOST buffers: c (m x n) = a*b (accumulate=0) or
- * c += a*b (accumulate=1), computed on the current device.  The H2D copies
- * of a and b are split into k-panels on a copy stream so the GEMM of one
- * panel overlaps the copy of the next (page-locked host memory makes the
- * copies asynchronous).  nonfinite (host int, may be NULL) receives 1 when
- * an output component is not finite (multiply.py:124-127). */
+ * c += a*b (accumulate=1), computed on the current device.  When a, b and
+ * c are all page-locked (blocked algorithm, accumulate=0) it is ONE GEMM
+ * launch that consumes 64-column k-panels of a and b as their H2D copies
+ * land and writes c straight into the page-locked buffer; otherwise the
+ * H2D copies are split into k-panels on a copy stream so the GEMM of one
+ * panel overlaps the copy of the next.  Same bits either way.  nonfinite
+ * (host int, may be NULL) receives 1 when an output component is not
+ * finite (multiply.py:124-127). */
 int mpmm_gemm_host(int comps, int algo, int64_t n_min, int64_t m, int64_t l, int64_t n,
                    const double *a, const double *b, double *c, int accumulate, int *nonfinite);
 

@@ -99,8 +99,10 @@ __device__ __forceinline__ void wait_k_panel(const KReady& kr, int k0, int& seen
     // the word before the flags and lets the kernel finish instead of
     // hanging the GPU; the host reports it as an error
     const volatile int* f = kr.flags + q;
+    const volatile int* st = kr.flags - 1;
     const long long t0 = clock64();
-    while (*f == 0) {
+    // once any CTA has timed out, nobody waits again (one bound per launch)
+    while (*f == 0 && (*st & 4) == 0) {
       __nanosleep(200);
       if (clock64() - t0 > (1ll << 32)) {   // ~2.2 s at 1.965 GHz
         atomicOr(const_cast<int*>(kr.flags) - 1, 4);

@@ -1245,68 +1245,98 @@ template <int COMPS>
 __device__ __forceinline__ void window_round(int64_t* wbuf, int tid, int win, int ebase,
                                              double* __restrict__ C, int64_t e, int* status) {
 #define WIN(q) wbuf[(q) * kMTB + tid]
-auto normalize = [&]() -> bool {
+  // Full normalisation once (digits to [0, 2^32), sign out), then per
+  // component: round the top 96 bits (+ sticky), subtract the double from
+  // the digits it covers and propagate the borrow upward only as far as it
+  // goes (the digits below are untouched and stay normalised); a negative
+  // remainder is negated over its nonzero span [low, top] only (two's
+  // complement leaves the zero digits below `low` zero).
   int64_t carry = 0;
   for (int q = 0; q < win; ++q) {
-    int64_t v = WIN(q) + carry;
+    const int64_t v = WIN(q) + carry;
     carry = v >> 32;
     WIN(q) = v - (carry << 32);
   }
-  if (carry >= 0) return false;
-  int64_t c = 1;
-  for (int q = 0; q < win; ++q) {
-    int64_t v = (0xffffffffll - WIN(q)) + c;
-    c = v >> 32;
-    WIN(q) = v & 0xffffffffll;
-  }
-  return true;
-};
-bool neg = normalize();
-double out[COMPS];
-for (int c = 0; c < COMPS; ++c) {
-  // round-to-nearest of the magnitude
+  auto negate = [&](int lo, int hi) {   // two's complement of digits lo..hi
+    int64_t c = 1;
+    for (int q = lo; q <= hi; ++q) {
+      const int64_t v = (0xffffffffll - WIN(q)) + c;
+      c = v >> 32;
+      WIN(q) = v & 0xffffffffll;
+    }
+  };
+  bool neg = carry < 0;
   int top = win - 1;
   while (top >= 0 && WIN(top) == 0) --top;
-  double d = 0.0;
-  if (top >= 0) {
-    uint64_t hi = static_cast<uint64_t>(WIN(top));
-    uint64_t mid = top >= 1 ? static_cast<uint64_t>(WIN(top - 1)) : 0;
-    uint64_t lo = top >= 2 ? static_cast<uint64_t>(WIN(top - 2)) : 0;
-    bool sticky = false;
-    for (int q = top - 3; q >= 0; --q) sticky |= (WIN(q) != 0);
-    int lz = __clzll(static_cast<long long>(hi)) - 32;
-    unsigned __int128 w = (static_cast<unsigned __int128>(hi) << 64) |
-                          (static_cast<unsigned __int128>(mid) << 32) | lo;
-    w <<= lz;
-    uint64_t top64 = static_cast<uint64_t>(w >> 32);
-    if ((static_cast<uint64_t>(w) & 0xffffffffull) != 0 || sticky) top64 |= 1ull;
-    d = ldexp(__ull2double_rn(top64), 32 * (top - 2) - lz + 32 + ebase);
+  int low = 0;
+  while (low <= top && WIN(low) == 0) ++low;
+  if (neg) {                       // the whole window was negative
+    negate(low, win - 1);
+    top = win - 1;
+    while (top >= 0 && WIN(top) == 0) --top;
   }
-  out[c] = neg ? -d : d;
-  if (d != 0.0) {   // subtract d (a multiple of 2^ebase) from the magnitude
-    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(d));
-    int be = static_cast<int>((b >> 52) & 0x7ff);
-    unsigned long long mm = b & ((1ull << 52) - 1);
-    if (be > 0) mm |= (1ull << 52);
-    int ee = (be > 0 ? be - 1075 : -1074) - ebase;
-    int tz = __ffsll(static_cast<long long>(mm)) - 1;
-    mm >>= tz;
-    ee += tz;
-    int q0 = ee >> 5, rr = ee & 31;
-    unsigned __int128 ww = static_cast<unsigned __int128>(mm) << rr;
-    for (int u = 0; u < 3; ++u)
-      if (q0 + u < win)
-        WIN(q0 + u) -= static_cast<int64_t>(static_cast<uint32_t>(ww >> (32 * u)));
+  double out[COMPS];
+  for (int c = 0; c < COMPS; ++c) {
+    double d = 0.0;
+    if (top >= 0) {
+      const uint64_t hi = static_cast<uint64_t>(WIN(top));
+      const uint64_t mid = top >= 1 ? static_cast<uint64_t>(WIN(top - 1)) : 0;
+      const uint64_t lo = top >= 2 ? static_cast<uint64_t>(WIN(top - 2)) : 0;
+      const bool sticky = top - 3 >= low;   // digits [low, top-3]: low is nonzero
+      const int lz = __clzll(static_cast<long long>(hi)) - 32;
+      unsigned __int128 w = (static_cast<unsigned __int128>(hi) << 64) |
+                            (static_cast<unsigned __int128>(mid) << 32) | lo;
+      w <<= lz;
+      uint64_t top64 = static_cast<uint64_t>(w >> 32);
+      if ((static_cast<uint64_t>(w) & 0xffffffffull) != 0 || sticky) top64 |= 1ull;
+      d = ldexp(__ull2double_rn(top64), 32 * (top - 2) - lz + 32 + ebase);
+    }
+    out[c] = neg ? -d : d;
+    if (d != 0.0) {   // subtract d (a multiple of 2^ebase) from the magnitude
+      const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(d));
+      const int be = static_cast<int>((b >> 52) & 0x7ff);
+      unsigned long long mm = b & ((1ull << 52) - 1);
+      if (be > 0) mm |= (1ull << 52);
+      int ee = (be > 0 ? be - 1075 : -1074) - ebase;
+      const int tz = __ffsll(static_cast<long long>(mm)) - 1;
+      mm >>= tz;
+      ee += tz;
+      const int q0 = ee >> 5, rr = ee & 31;
+      const unsigned __int128 ww = static_cast<unsigned __int128>(mm) << rr;
+      for (int u = 0; u < 3; ++u)
+        if (q0 + u < win)
+          WIN(q0 + u) -= static_cast<int64_t>(static_cast<uint32_t>(ww >> (32 * u)));
+      // borrow upward from q0 (d's digits span q0 .. q0 + 2 <= top)
+      int64_t br = 0;
+      int q = q0;
+      for (; q < win; ++q) {
+        const int64_t v = WIN(q) + br;
+        br = v >> 32;
+        WIN(q) = v - (br << 32);
+        if (q >= q0 + 2 && br == 0) break;
+      }
+      if (br < 0) {           // d exceeded the remainder: flip the sign
+        neg = !neg;
+        negate(low, win - 1);
+      }
+      if (q0 < low) {         // (not expected: d's lowest bit is above `low`)
+        low = q0;
+      }
+      while (low <= top && WIN(low) == 0) ++low;
+      if (low > top) {        // remainder exactly zero
+        top = -1;
+      } else {
+        while (top >= 0 && WIN(top) == 0) --top;
+      }
+    }
   }
-  neg = neg ^ normalize();
-}
 #undef WIN
-bool bad = false;
-for (int c = 0; c < COMPS; ++c) {
-  C[e * COMPS + c] = out[c];
-  bad |= !isfinite(out[c]);
-}
-if (bad) atomicOr(status, 1);
+  bool bad = false;
+  for (int c = 0; c < COMPS; ++c) {
+    C[e * COMPS + c] = out[c];
+    bad |= !isfinite(out[c]);
+  }
+  if (bad) atomicOr(status, 1);
 }
 
 template <int COMPS, int K, bool RES8>
