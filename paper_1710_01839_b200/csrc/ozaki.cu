@@ -95,12 +95,19 @@ constexpr int kEmptyE = -100000, kEmptyL = 100000;
 // component c, E[c] = max top_exp and L[c] = min low_bit over the nonzero
 // entries; any non-finite component sets bit 0 of *status.  EL layout:
 // E[comps][odim] then L[comps][odim].
+//
+// Rows: one block of kScanWarps warps per row (the warps split the row's
+// columns, then combine through shared memory): one warp per row left a
+// 1024-row operand at 7 warps per SM, latency-bound.
+constexpr int kScanWarps = 4;
+
 template <int NC>
-__global__ void scan_rows_kernel(const double* __restrict__ X, int64_t ld, int rows, int cols,
-                                 int* __restrict__ EL, int* __restrict__ status) {
-  const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (r >= rows) return;
+__global__ void __launch_bounds__(32 * kScanWarps)
+scan_rows_kernel(const double* __restrict__ X, int64_t ld, int rows, int cols,
+                 int* __restrict__ EL, int* __restrict__ status) {
+  __shared__ int sEL[kScanWarps][2 * NC];
+  const int r = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int e[NC], lo[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) e[c] = kEmptyE, lo[c] = kEmptyL;
@@ -108,7 +115,7 @@ __global__ void scan_rows_kernel(const double* __restrict__ X, int64_t ld, int r
   // four k per lane per step: independent loads in flight (one warp per row
   // leaves few warps per SM, so latency, not bandwidth, bounds this loop)
   constexpr int U = 8;
-  for (int k0 = lane; k0 < cols; k0 += 32 * U) {
+  for (int k0 = warp * 32 * U + lane; k0 < cols; k0 += kScanWarps * 32 * U) {
     double v[U][NC];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -138,9 +145,21 @@ __global__ void scan_rows_kernel(const double* __restrict__ X, int64_t ld, int r
   if (lane == 0) {
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-      EL[c * rows + r] = e[c];
-      EL[(NC + c) * rows + r] = lo[c];
+      sEL[warp][c] = e[c];
+      sEL[warp][NC + c] = lo[c];
     }
+  }
+  __syncthreads();
+  if (threadIdx.x < NC) {
+    const int c = threadIdx.x;
+    int ee = sEL[0][c], ll = sEL[0][NC + c];
+#pragma unroll
+    for (int w = 1; w < kScanWarps; ++w) {
+      ee = max(ee, sEL[w][c]);
+      ll = min(ll, sEL[w][NC + c]);
+    }
+    EL[c * rows + r] = ee;
+    EL[(NC + c) * rows + r] = ll;
   }
 }
 
@@ -1426,12 +1445,11 @@ cudaError_t oz_scan_launch(int by_cols, const double* X, int64_t ld, int rows, i
     else
       scan_cols_kernel<4><<<grid, 256, 0, s>>>(X, ld, rows, cols, EL, status);
   } else {
-    const int64_t threads = static_cast<int64_t>(rows) * 32;
-    const unsigned blocks = static_cast<unsigned>((threads + 127) / 128);
+    const unsigned blocks = static_cast<unsigned>(rows);
     if (comps == 2)
-      scan_rows_kernel<2><<<blocks, 128, 0, s>>>(X, ld, rows, cols, EL, status);
+      scan_rows_kernel<2><<<blocks, 32 * kScanWarps, 0, s>>>(X, ld, rows, cols, EL, status);
     else
-      scan_rows_kernel<4><<<blocks, 128, 0, s>>>(X, ld, rows, cols, EL, status);
+      scan_rows_kernel<4><<<blocks, 32 * kScanWarps, 0, s>>>(X, ld, rows, cols, EL, status);
   }
   return cudaGetLastError();
 }
