@@ -219,13 +219,26 @@ void* pinned_alias(const void* host) {
   return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
 }
 
-constexpr int64_t kStreamPanel = 64;   // k columns per streamed panel
+// k columns per streamed panel (MPMM_STREAM_PANEL: measurement knob, a
+// multiple of 16)
+int64_t stream_panel() {
+  static const int64_t v = [] {
+    int64_t p = 64;
+    if (const char* env = std::getenv("MPMM_STREAM_PANEL")) {
+      const int64_t q = std::atoll(env);
+      if (q >= 16 && q % 16 == 0) p = q;
+    }
+    return p;
+  }();
+  return v;
+}
 
 // MPMM_OK, an error, or -1: not applicable (the caller takes the panelled path)
 int host_rows_gemm_streamed(int comps, int tile, int64_t rows, int64_t l, int64_t n,
                             const double* a_rows, const double* b, double* c_rows,
                             int* nonfinite_host, HostStreams* hs) {
   const int* one = pinned_one();
+  const int64_t kStreamPanel = stream_panel();
   if (one == nullptr || tile == TILE_LPT || l < 2 * kStreamPanel) return -1;
   if (pinned_alias(a_rows) == nullptr || pinned_alias(b) == nullptr) return -1;
   double* dCh = static_cast<double*>(pinned_alias(c_rows));
