@@ -90,3 +90,24 @@ def test_streamed_equals_panelled_path(gpu, tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(path))
     assert np.array_equal(outs[0], outs[1])
+
+
+def test_streamed_host_products_from_concurrent_threads(gpu):
+    """Four host threads issue streamed products at once (each thread owns
+    its streams; the panel flags and buffers are per call): every result
+    is the oracle's."""
+    from concurrent.futures import ThreadPoolExecutor
+    cases = []
+    for s in range(4):
+        a, b = inputs.gemm_inputs("dd", 96, 256, 80, seed=30 + s)
+        cases.append((DenseMatrix(96, 256, mp.PrecisionSpec.dd(), _pinned(a)),
+                      DenseMatrix(256, 80, mp.PrecisionSpec.dd(), _pinned(b)),
+                      oracle.matmul_simple(a, b)))
+
+    def work(k):
+        A, B, want = cases[k % 4]
+        return all(np.array_equal(mp.matmul_block(A, B, 32).host_array(), want)
+                   for _ in range(5))
+
+    with ThreadPoolExecutor(4) as ex:
+        assert all(ex.map(work, range(8)))
