@@ -144,3 +144,130 @@ def sharded_matmul_host(a_rows, b, l, n, prec, *, n_min=64, simple=False, group=
     if flag.item():
         raise RangeError("matrix product overflowed the working precision")
     return out
+
+
+# ---------------------------------------------------------------------------
+# Strassen's seven top-level products spread over ranks (SURVEY.md s8f-2:
+# the alternative to row sharding)
+# ---------------------------------------------------------------------------
+
+def strassen_operands(a11, a12, a21, a22, b11, b12, b21, b22, add):
+    """The seven (left, right) operand pairs of the reference's recursion
+    (multiply.py:300-318), in its order and with its sums; add(x, y,
+    subtract) is one reference ewise op."""
+    return (
+        (add(a11, a22, False), add(b11, b22, False)),
+        (add(a21, a22, False), b11),
+        (a11, add(b12, b22, True)),
+        (a22, add(b21, b11, True)),
+        (add(a11, a12, False), b22),
+        (add(a21, a11, True), add(b11, b12, False)),
+        (add(a12, a22, True), add(b21, b22, False)),
+    )
+
+
+def strassen_combine(p, add):
+    """C quadrants from the seven products, the reference's chains
+    (multiply.py:320-331)."""
+    p1, p2, p3, p4, p5, p6, p7 = p
+    c11 = add(add(add(p1, p4, False), p5, True), p7, False)
+    c12 = add(p3, p5, False)
+    c21 = add(p2, p4, False)
+    c22 = add(add(add(p1, p3, False), p2, True), p6, False)
+    return c11, c12, c21, c22
+
+
+def strassen_distributed(a, b, *, product, add, group=None):
+    """C = A B (square, both operands on every rank, torch tensors of shape
+    (n, n, comps)) with the seven top-level Strassen products computed on
+    ranks i mod world: rank r forms the operand sums of its products,
+    multiplies them with ``product`` (the recursion below the top level:
+    matmul_strassen with the same cutoff, or the blocked kernel at a leaf),
+    and each product is broadcast from its owner (the exchange step; the
+    only collective).  Every rank then combines the quadrants in the
+    reference's order, so C is bitwise the single-process Strassen's.
+    ``add(x, y, subtract)``: one reference ewise op on same-shape tensors.
+    The caller handles n <= cutoff (no top level to split)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    n, comps = a.shape[0], a.shape[2]
+    even = n + (n & 1)
+    if even != n:   # the reference pads an odd dimension with zeros (multiply.py:293-299)
+        ap = a.new_zeros((even, even, comps))
+        bp = b.new_zeros((even, even, comps))
+        ap[:n, :n] = a
+        bp[:n, :n] = b
+        a, b = ap, bp
+    h = even // 2
+
+    def q(m, i, j):
+        return m[i * h:(i + 1) * h, j * h:(j + 1) * h].contiguous()
+
+    mine = [i for i in range(7) if i % world == rank]
+    # only the sums this rank's products need (the rest are never formed)
+    ops = strassen_operands(q(a, 0, 0), q(a, 0, 1), q(a, 1, 0), q(a, 1, 1),
+                            q(b, 0, 0), q(b, 0, 1), q(b, 1, 0), q(b, 1, 1),
+                            _Lazy.add(add))
+    prods = []
+    for i in range(7):
+        if i in mine:
+            x, y = ops[i]
+            prods.append(product(_Lazy.force(x), _Lazy.force(y)).contiguous())
+        else:
+            prods.append(a.new_empty((h, h, comps)))
+    if world > 1:
+        for i in range(7):
+            dist.broadcast(prods[i], src=_group_rank_to_global(group, i % world), group=group)
+    c11, c12, c21, c22 = strassen_combine(prods, add)
+    c = torch.cat([torch.cat([c11, c12], dim=1), torch.cat([c21, c22], dim=1)], dim=0)
+    return c[:n, :n].contiguous()
+
+
+def _group_rank_to_global(group, r):
+    import torch.distributed as dist
+    if group is None:
+        return r
+    return dist.get_global_rank(group, r)
+
+
+class _Lazy:
+    """A deferred ewise op, formed only when a product needs it."""
+
+    def __init__(self, fn, args):
+        self.fn, self.args = fn, args
+
+    @staticmethod
+    def add(add):
+        return lambda x, y, subtract: _Lazy(add, (x, y, subtract))
+
+    @staticmethod
+    def force(v):
+        if isinstance(v, _Lazy):
+            x, y, s = v.args
+            return v.fn(_Lazy.force(x), _Lazy.force(y), s)
+        return v
+
+
+def cuda_strassen_ops(prec, cutoff, leaf_n_min):
+    """(product, add) on device tensors through the sm_100a kernels: the
+    product is matmul_strassen at the same cutoff (the blocked kernel when
+    the half size is at or below it), add one batched ewise launch."""
+    from .matrix import DenseMatrix
+    from . import multiply as mul
+
+    def product(x, y):
+        X = DenseMatrix(x.shape[0], x.shape[1], prec, x)
+        Y = DenseMatrix(y.shape[0], y.shape[1], prec, y)
+        if x.shape[0] <= cutoff:
+            return mul.matmul_block(X, Y, leaf_n_min).data
+        return mul.matmul_strassen(X, Y, cutoff, leaf_n_min).data
+
+    def add(x, y, subtract):
+        X = DenseMatrix(x.shape[0], x.shape[1], prec, x)
+        Y = DenseMatrix(y.shape[0], y.shape[1], prec, y)
+        return mul._ewise(X, Y, subtract).data
+
+    return product, add

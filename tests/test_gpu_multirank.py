@@ -93,3 +93,47 @@ def test_bench_two_ranks_json(gpu):
     assert r2.returncode == 0, r2.stderr[-3000:]
     lines = [ln for ln in r2.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1 and json.loads(lines[0])["impl"] == "reference"
+
+
+STRASSEN_WORKER = r'''
+import os, sys
+sys.path.insert(0, os.environ["REPO"])
+import numpy as np, torch, torch.distributed as dist
+from paper_1710_01839_b200 import inputs, shard, PrecisionSpec
+dist.init_process_group("gloo")
+r = dist.get_rank()
+torch.cuda.set_device(0)
+tok, n = os.environ["TOK"], int(os.environ["N"])
+a, b = inputs.gemm_inputs(tok, n, n, n, seed=12)
+product, add = shard.cuda_strassen_ops(PrecisionSpec.parse(tok), 64, 32)
+c = shard.strassen_distributed(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
+                               product=product, add=add)
+np.save(os.environ["OUT"] + f".{r}.npy", c.cpu().numpy())
+dist.destroy_process_group()
+'''
+
+
+@pytest.mark.parametrize("tok,n", [("dd", 300), ("qd", 129)])
+def test_two_ranks_strassen_products_equal_single_gpu_strassen(gpu, tmp_path, tok, n):
+    """The seven top-level products split over two ranks (sharing cuda:0,
+    gloo moving the products through the host): C on every rank is bitwise
+    the single-GPU matmul_strassen at the same cutoff."""
+    import torch
+    import paper_1710_01839_b200 as mp
+    from paper_1710_01839_b200 import inputs
+    from paper_1710_01839_b200.matrix import DenseMatrix
+    out = str(tmp_path / "s")
+    script = tmp_path / "ws.py"
+    script.write_text(STRASSEN_WORKER)
+    env = dict(os.environ, REPO=ROOT, TOK=tok, N=str(n), OUT=out)
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node=2", "--master-addr=127.0.0.1",
+                        f"--master-port={_port()}", str(script)], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    a, b = inputs.gemm_inputs(tok, n, n, n, seed=12)
+    prec = mp.PrecisionSpec.parse(tok)
+    want = mp.matmul_strassen(DenseMatrix(n, n, prec, a).to_device(),
+                              DenseMatrix(n, n, prec, b).to_device(), 64, 32).host_array()
+    for rank in range(2):
+        assert np.array_equal(np.load(f"{out}.{rank}.npy"), want)

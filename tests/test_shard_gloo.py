@@ -67,3 +67,59 @@ def test_two_rank_broadcast_matmul_is_bitwise_invariant(tmp_path, tok, m, l, n, 
     c = np.concatenate(parts, axis=0)
     a, b = inputs.gemm_inputs(tok, m, l, n, seed=5)
     assert np.array_equal(c, oracle.matmul_simple(a, b))
+
+
+# ---------------------------------------------------------------------------
+# Strassen's seven top-level products spread over ranks
+# ---------------------------------------------------------------------------
+
+def _oracle_strassen_ops(cutoff, leaf):
+    def product(x, y):
+        return torch.from_numpy(oracle.strassen(x.numpy(), y.numpy(), cutoff, leaf))
+
+    def add(x, y, subtract):
+        return torch.from_numpy(oracle.ewise_new(np.ascontiguousarray(x.numpy()),
+                                                 np.ascontiguousarray(y.numpy()), subtract))
+    return product, add
+
+
+def _strassen_worker(rank, world, port, tok, n, cutoff, leaf, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a, b = inputs.gemm_inputs(tok, n, n, n, seed=8)
+        product, add = _oracle_strassen_ops(cutoff, leaf)
+        c = shard.strassen_distributed(torch.from_numpy(a), torch.from_numpy(b),
+                                       product=product, add=add)
+        np.save(f"{out_path}.{rank}.npy", c.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,tok,n,cutoff", [(2, "dd", 24, 6), (3, "dd", 17, 4),
+                                                (2, "qd", 10, 3)])
+def test_strassen_products_over_ranks_bitwise(tmp_path, world, tok, n, cutoff):
+    """Every rank's C equals the single-process Strassen (the reference's
+    recursion restated in the oracle), bit for bit, for even and odd n."""
+    out = str(tmp_path / "s")
+    tmp.spawn(_strassen_worker, args=(world, _free_port(), tok, n, cutoff, 4, out), nprocs=world,
+              join=True)
+    a, b = inputs.gemm_inputs(tok, n, n, n, seed=8)
+    want = oracle.strassen(a, b, cutoff, 4)
+    for r in range(world):
+        assert np.array_equal(np.load(f"{out}.{r}.npy"), want)
+
+
+def test_strassen_operand_and_combine_order():
+    """strassen_operands / strassen_combine reproduce the oracle's top level
+    (the reference's operand sums and combination chains)."""
+    a, b = inputs.gemm_inputs("dd", 8, 8, 8, seed=3)
+    product, add = _oracle_strassen_ops(4, 2)   # the recursion below: same cutoff
+    A, B = torch.from_numpy(a), torch.from_numpy(b)
+    q = lambda m, i, j: m[i * 4:(i + 1) * 4, j * 4:(j + 1) * 4].contiguous()
+    ops = shard.strassen_operands(q(A, 0, 0), q(A, 0, 1), q(A, 1, 0), q(A, 1, 1),
+                                  q(B, 0, 0), q(B, 0, 1), q(B, 1, 0), q(B, 1, 1), add)
+    quads = shard.strassen_combine([product(x, y) for x, y in ops], add)
+    c = torch.cat([torch.cat(quads[:2], dim=1), torch.cat(quads[2:], dim=1)], dim=0)
+    assert np.array_equal(c.numpy(), oracle.strassen(a, b, 4, 2))
