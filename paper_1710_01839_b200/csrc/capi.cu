@@ -182,14 +182,14 @@ int block_cells_impl(int comps, int64_t n_min, int64_t cell0, int64_t cell1, int
 // the panelled path below.
 // ---------------------------------------------------------------------------
 
-// A page-locked 1: the source of every panel flag.  A 4-byte H2D copy
-// from it runs on the copy engine, never on an SM, so the GEMM CTAs
-// spinning on the flags cannot block it (a memset or a kernel could be).
 // Set when a streamed product timed out waiting for a panel (a tool that
 // serialises kernels against the copy stream): later products take the
 // panelled path.
 std::atomic<bool> g_streamed_off{false};
 
+// A page-locked 1: the source of every panel flag.  A 4-byte H2D copy
+// from it runs on the copy engine, never on an SM, so the GEMM CTAs
+// spinning on the flags cannot block it (a memset or a kernel could be).
 const int* pinned_one() {
   if (g_streamed_off.load(std::memory_order_relaxed)) return nullptr;
   static int* one = nullptr;
@@ -245,11 +245,13 @@ int host_rows_gemm_streamed(int comps, int tile, int64_t rows, int64_t l, int64_
   if (dCh == nullptr) return -1;
   const size_t el = comps * sizeof(double);
   const int npan = static_cast<int>((l + kStreamPanel - 1) / kStreamPanel);
-  DevBuf dA, dB;
-  int* dint = nullptr;   // [0]: non-finite flag, [1 .. npan]: panel flags
+  DevBuf dA, dB, dflags;
   CU(dA.alloc(rows * l * comps, hs->comp));
   CU(dB.alloc(l * n * comps, hs->comp));
-  CU(cudaMallocAsync(reinterpret_cast<void**>(&dint), (npan + 1) * sizeof(int), hs->comp));
+  // [0]: status (bit 0 non-finite, bit 2 panel wait timed out), [1 .. npan]:
+  // panel flags; freed (stream-ordered) on every return path
+  CU(dflags.alloc((npan + 2) / 2, hs->comp));
+  int* dint = reinterpret_cast<int*>(dflags.p);
   CU(cudaMemsetAsync(dint, 0, (npan + 1) * sizeof(int), hs->comp));
   Event ready;
   CU(ready.make());
@@ -281,7 +283,6 @@ int host_rows_gemm_streamed(int comps, int tile, int64_t rows, int64_t l, int64_
   }
   int status = 0;   // pageable target: the copy completes before cudaMemcpyAsync returns
   CU(cudaMemcpyAsync(&status, dint, sizeof(int), cudaMemcpyDeviceToHost, hs->comp));
-  CU(cudaFreeAsync(dint, hs->comp));
   CU(cudaStreamSynchronize(hs->copy));
   CU(cudaStreamSynchronize(hs->comp));
   if (status & 4) {
