@@ -431,7 +431,10 @@ __global__ void __launch_bounds__(256)
 residues_cols_kernel(const double* __restrict__ X, int64_t ld, int rows, int cols, int comps,
                      int c0, const int* __restrict__ shift, int N, int8_t* __restrict__ R,
                      int64_t rpitch, int64_t rplane) {
-  __shared__ uint32_t S[2][32][9];
+  // the packed words of kColChunk moduli go through shared memory per
+  // barrier (one barrier per modulus left the kernel barrier/issue bound)
+  constexpr int kColChunk = 8;
+  __shared__ uint32_t S[kColChunk][32][9];
   const int lane = threadIdx.x & 31, wq = threadIdx.x >> 5;
   const int o = blockIdx.x * 32 + lane;
   const int k0 = blockIdx.y * 32 + wq * 4;
@@ -454,15 +457,23 @@ residues_cols_kernel(const double* __restrict__ X, int64_t ld, int rows, int col
   uint32_t wt[W];
   ResidueConsts k = load_weights<W>(0, wt);
 #pragma unroll 1
-  for (int t = 0; t < N; ++t) {
-    uint32_t wn[W];
-    const ResidueConsts kn = load_weights<W>(t + 1 < N ? t + 1 : t, wn);
-    S[t & 1][lane][wq] = residue_word<W>(Xw, neg, k, wt);
-    k = kn;
+  for (int t0 = 0; t0 < N; t0 += kColChunk) {
+    const int cn = N - t0 < kColChunk ? N - t0 : kColChunk;
+#pragma unroll 1
+    for (int u = 0; u < cn; ++u) {
+      const int t = t0 + u;
+      uint32_t wn[W];
+      const ResidueConsts kn = load_weights<W>(t + 1 < N ? t + 1 : t, wn);
+      S[u][lane][wq] = residue_word<W>(Xw, neg, k, wt);
+      k = kn;
 #pragma unroll
-    for (int w = 0; w < W; ++w) wt[w] = wn[w];
+      for (int w = 0; w < W; ++w) wt[w] = wn[w];
+    }
     __syncthreads();
-    if (store) *reinterpret_cast<uint32_t*>(dst + t * rplane) = S[t & 1][oc][qq];
+    if (store)
+      for (int u = 0; u < cn; ++u)
+        *reinterpret_cast<uint32_t*>(dst + (t0 + u) * rplane) = S[u][oc][qq];
+    __syncthreads();
   }
 }
 
