@@ -72,6 +72,25 @@ def main():
         check(False, "range error not raised")
     except mp.RangeError:
         pass
+    # the exact tensor mode (residues, tcgen05 residue GEMMs, tensor-core CRT)
+    from paper_1710_01839_b200.tensor import matmul_exact
+    from oracle import exact
+    for tok, (m, l, n) in (("dd", (40, 72, 36)), ("qd", (17, 33, 20))):
+        prec = mp.PrecisionSpec.parse(tok)
+        a, b = inputs.gemm_inputs(tok, m, l, n, seed=6)
+        c = matmul_exact(DenseMatrix(m, l, prec, a).to_device(),
+                         DenseMatrix(l, n, prec, b).to_device()).host_array()
+        ratio, _ = exact.bound_ratio(a, b, c, range(0, m, 5), range(0, n, 7),
+                                     104 if tok == "dd" else 209)
+        check(ratio <= 1.0, f"{tok} exact mode bound")
+    # page-locked host operands: the streamed single-launch product (under a
+    # tool that serialises kernels it times out once and falls back)
+    a, b = inputs.gemm_inputs("dd", 48, 160, 40, seed=7)
+    pa = torch.from_numpy(a).pin_memory().numpy()
+    pb = torch.from_numpy(b).pin_memory().numpy()
+    c = mp.matmul_block(DenseMatrix(48, 160, mp.PrecisionSpec.dd(), pa),
+                        DenseMatrix(160, 40, mp.PrecisionSpec.dd(), pb), 32).host_array()
+    check(np.array_equal(c, oracle.matmul_simple(a, b)), "streamed host product")
     s = torch.zeros(64, dtype=torch.float64, device="cuda")
     _cuda.fp64_burn_dev(0, 4, 64, 10, s.data_ptr())
     torch.cuda.synchronize()
