@@ -84,6 +84,22 @@ def test_tune_grid_and_report(gpu, tmp_path, capsys):
 
 
 @pytest.mark.gpu
+def test_tune_exact_mode_v3_table_and_report(gpu, tmp_path, capsys):
+    out = tmp_path / "x.tbl"
+    rc = main(["tune", "--prec", "dd", "--dims", "128,256", "--nmin", "16,32", "--threads", "1",
+               "--out", str(out), "--cutoffs", "64", "--exact-mode", "--warmup", "1"])
+    assert rc == EX_OK
+    assert open(out).read().startswith("mpmmtune v3")
+    table = mp.load_table(str(out))
+    assert len(table.rows) == 2 and all(r.exact_time_s > 0 for r in table.rows)
+    with open(str(out) + ".csv") as fp:
+        hdr = next(ln for ln in fp if not ln.startswith("#"))
+    assert "exact_s" in hdr
+    assert main(["report", "--in", str(out), "--format", "winners"]) == EX_OK
+    assert "?" not in capsys.readouterr().out
+
+
+@pytest.mark.gpu
 def test_verify_ok_and_detects_injected_fault(gpu, monkeypatch, capsys):
     assert main(["verify", "--prec", "dd,qd", "--dims", "17,32", "--nmin", "8", "--cutoff", "8",
                  "--exact"]) == EX_OK
