@@ -454,9 +454,9 @@ def run_ours(args, rank, world, local_rank):
             "roofline_frac": 18 * float(n) ** 3 / fast_s / 1e12 / peak["dfma"]}
     if tensor_s is not None:
         line["tensor_mode"] = {
-            "what": "opt-in exact mode: int8 tensor-core residue GEMMs (CRT, cuBLASLt IMMA) + "
-                    "exact reconstruction, product rounded once; more accurate than, not "
-                    "bit-identical to, the reference",
+            "what": "opt-in exact mode: int8 tensor-core residue GEMMs (CRT, hand-written tcgen05) + "
+                    "tensor-core CRT sums (mma.sync) + exact reconstruction, product rounded "
+                    "once; more accurate than, not bit-identical to, the reference",
             "value": 2.0 * float(n) ** 3 * world / tensor_s, "unit": "2mnl/s",
             "ms": tensor_s * 1e3,
             "jobs": [{"a_comps": list(ra), "b_comps": list(rb), "moduli": N}

@@ -5,7 +5,8 @@ rounded once to the nearest DD/QD expansion -- more accurate than the
 reference's step-by-step rounding (so not bit-identical to it), and far
 inside the north_star bound 4 l u (|A||B|)_ij.
 
-How (csrc/ozaki.cu, int8gemm.cpp; the CRT variant of the Ozaki scheme):
+How (csrc/ozaki.cu, tc_i8.cu, exact.cpp; the CRT variant of the Ozaki
+scheme):
 
 1. scan (one pass per operand, one host sync): per row of A (column of
    B) and component the largest exponent E and the lowest set bit L; for a
@@ -15,8 +16,11 @@ How (csrc/ozaki.cu, int8gemm.cpp; the CRT variant of the Ozaki scheme):
    modulo N pairwise-coprime prime powers p_t <= 256 by byte dot products
    (dp4a) with 2^(8j) mod p_t, centred into int8; N is the smallest count
    whose product P exceeds 2 l 2^(beta_A + beta_B);
-3. one batched int8 GEMM per modulus (exact int32 accumulation);
-4. CRT: per output, X = sum_t r_t W_t mod P rebuilt in 32-bit limbs,
+3. one int8 GEMM per modulus (exact int32 accumulation), hand-written on
+   tcgen05 (TMA, TMEM accumulators), reduced mod p_t in its epilogue to
+   bytes (cuBLASLt int32 products as the fallback);
+4. CRT: per output, X = sum_t r_t W_t mod P rebuilt in 32-bit limbs (the
+   sums as a u8 tensor-core product of residues and weight-limb bytes),
    scaled by 2^-(s_i + t_j), summed over jobs, rounded to DD/QD.
 
 When beta_A + beta_B does not fit the 54 available moduli (363 bits) the
