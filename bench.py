@@ -1,26 +1,41 @@
 #!/usr/bin/env python3
 """Benchmark: DD/QD GEMM 2mnl/s on B200 (BASELINE.json metric).
 
-Workload (``config.workload``): BASELINE.json configs[1], the blocked DD
-GEMM m = l = n = 1024 on the seeded uniform inputs, one
-product per step.  Under torchrun with N ranks the problem is weak-scaled:
-every rank owns its own 1024 rows of A and C, and B (1024 x 1024 DD) is
-broadcast from rank 0 over NCCL inside every step, pipelined in k-panels
-(``shard.broadcast_matmul``).
+Workload (``config.workload``): BASELINE.json configs[4] at its largest
+size, the DD GEMM m = l = n = 8192 on the seed-1 uniform inputs (SURVEY.md
+s8d), computed by the bit-identical blocked mirror kernel (the kernel the
+north_star's 50 % FP64-roofline target names) at the block size the GPU
+predictor picks.  One product per step.  Inputs are 1 GiB per matrix, far
+larger than the 126 MB L2, so no L2 flush is needed between steps.
 
-Printed (rank 0, one JSON line): ``value`` = device throughput (whole job,
-CUDA events around each step on the launching stream, L2 flushed between
-steps, max over ranks), ``e2e`` = the same metric through the public API
-with host buffers (H2D of A and B, D2H of C inside the timed region),
-``roofline`` against the FP64 pipe (peak measured in-run with a DFMA
-micro-benchmark; spec 148 SMs x 64 lanes x 2 x 1.965 GHz = 37.2 TFLOP/s),
-``cpu_baseline`` = the reference's own compiled kernels (oracle/_ref) on
-the host cores, on a bounded leading-rows sample.
+Under torchrun with N ranks the problem is STRONG-scaled (north_star:
+"near-linear scaling to 8 GPUs at m=n=l=8192"): rank r owns a contiguous
+64-row-aligned block of C's rows and the matching rows of A; B (8192 x
+8192 DD, 1 GiB) is broadcast from rank 0 over NCCL inside every step in
+k-panels, each panel's GEMM accumulating as soon as it lands
+(``shard.broadcast_matmul``).  ``value`` = 2mnl of the whole product / the
+max over ranks of the device time.
 
-``--impl reference`` times that reference CPU implementation alone.
+Printed (rank 0, one JSON line):
+* ``value``: device throughput (CUDA events on the launching stream);
+* ``e2e``: the same metric through the public API with host buffers --
+  ``matmul_block(host, host)`` at N = 1 (H2D of A and B and D2H of C inside
+  the timed region), ``shard.sharded_matmul_host`` per rank at N > 1;
+* ``roofline``: the GEMM kernel against the FP64 pipe.  MEASURED_PEAKS.json
+  has no FP64 entry, so the peak is a DFMA burst measured in this run
+  (spec: 148 SMs x 64 lanes x 2 flop x 1.965 GHz = 37.2 TFLOP/s);
+* ``cpu_baseline``: the reference's own compiled kernels (oracle/_ref) on
+  all host cores, on the reference's own leading-rows slice, extrapolated
+  with the reference's own predictor (predict.py:37-50) -- "CPU, predicted";
+* sub-fields: the tuner's bit-identical pick (blocked or Strassen, effective
+  2mnl/s), QD 8192^3, and BASELINE configs[1] (DD 1024^3).
+
+``--impl reference`` times that reference CPU implementation alone, on the
+same config, and loads nothing from this repo's package (no repo .so).
 """
 
 import argparse
+import importlib.util
 import json
 import math
 import os
@@ -33,36 +48,41 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+METRIC = "DD/QD GEMM 2mnl/s at 1/2/4/8 B200; % of FP64 roofline; vs host-CPU ref"
 F_DD = 53    # flops per DD multiply-add of the mirror kernel (4 DMUL, 3 DFMA, 43 DADD)
 I_DD = 50    # FP64 instructions per DD multiply-add
 F_QD = 796   # flops per QD multiply-add (10 DFMA, 13 DMUL, 763 DADD)
 SPEC_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
-
+CFG4_SEED = 1          # BASELINE configs[4]: "inputs as config 0 with seed 1"
+REF_N_MIN = 64         # the reference's DEFAULT_BLOCK_SIZE (multiply.py:32)
+ROW_ALIGN = 64         # shard alignment: the largest CTA tile height
 
 # ~5 ms of GPU spin before each timed step (outside the events): the host
-# enqueue of a step (plus the clock sampler's nvidia-smi forks competing
-# for the host) must finish before the device reaches the start event, or
-# host time leaks into the device-timed step (seen with 1 ms: +0.7 ms/step)
+# enqueue of a step must finish before the device reaches the start event
 HOST_SLACK_CYCLES = 10_000_000
+
 
 def parse():
     p = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--prec", default="dd", choices=["dd", "qd"])
-    p.add_argument("--size", type=int, default=1024, help="m = l = n per rank")
+    p.add_argument("--size", type=int, default=8192, help="m = l = n of the whole product")
+    p.add_argument("--seed", type=int, default=CFG4_SEED)
     p.add_argument("--nmin", type=int, default=0,
                    help="block size; 0 = let the GPU predictor pick from 16..256")
-    p.add_argument("--panel", type=int, default=0, help="k-panel rows for the B broadcast")
+    p.add_argument("--panel", type=int, default=1024,
+                   help="k-panel rows of the B broadcast at N > 1 (0 = one panel)")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-seconds", type=float, default=8.0)
-    p.add_argument("--dist-backend", default="nccl",
-                   help="torch.distributed backend for N>1 (nccl; gloo only to test the "
-                        "multi-rank logic with all ranks on one GPU)")
+    p.add_argument("--no-extras", action="store_true",
+                   help="skip the tuner-pick / QD / configs[1] sub-fields")
+    p.add_argument("--cpu-budget", type=float, default=200.0,
+                   help="seconds the reference arm may spend in total")
+    p.add_argument("--dist-backend", default="nccl")
     p.add_argument("--same-device", action="store_true",
-                   help="put every rank on cuda:0 (multi-rank logic test on one GPU, gloo)")
+                   help="every rank on cuda:0 (multi-rank logic test on one GPU, gloo)")
     return p.parse_args()
 
 
@@ -84,7 +104,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -127,77 +147,113 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the reference's compiled kernels (oracle/_ref) on the host
+# the reference CPU implementation (oracle/_ref) -- "CPU, predicted"
 # ---------------------------------------------------------------------------
 
-def cpu_reference_run(prec_tok, n, n_min, seconds):
-    """Time the reference's own blocked kernel (multiply.py:_block_into
-    partitioning over _kernels.dd_block_cells) on the leading rows of A
-    against all of B, doubling the slice until it runs ~``seconds``.
-    Returns (value 2mnl/s, cores, kind, sample description)."""
-    import numpy as np
+def _inputs_module():
+    """paper_1710_01839_b200/inputs.py loaded by file path: numpy only, so
+    the reference arm never imports the package (which would map the repo's
+    CUDA library into the process)."""
+    path = os.path.join(ROOT, "paper_1710_01839_b200", "inputs.py")
+    spec = importlib.util.spec_from_file_location("_bench_inputs", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
 
-    import oracle
-    from paper_1710_01839_b200 import inputs
-    kern = oracle.ref_kernels()
-    kind = "reference" if kern is not None else "port"
-    cores = len(os.sched_getaffinity(0))
-    a, b = inputs.gemm_inputs(prec_tok, n, n, n, seed=0)
-    rows = n_min
-    while True:
-        sl = np.ascontiguousarray(a[:rows])
+
+class ReferenceCPU:
+    """The reference's blocked product (multiply.py:148-160 partitioning
+    over its compiled _kernels.dd_block_cells, all host threads) on its own
+    predictor slice: the leading slice_rows_for(n_min, m) rows of A times
+    all of B, extrapolated by predict_full_time (predict.py:37-50)."""
+
+    def __init__(self, prec, size, seed, n_min=REF_N_MIN, a=None, b=None):
+        import oracle
+        self.oracle = oracle
+        self.kern = oracle.ref_kernels()
+        self.kind = "reference" if self.kern is not None else "port"
+        self.cores = len(os.sched_getaffinity(0))
+        self.prec, self.size, self.n_min = prec, size, n_min
+        self.mult = oracle.DEFAULT_SLICE_MULTIPLIER
+        if a is None or b is None:
+            a, b = _inputs_module().gemm_inputs(prec, size, size, size, seed=seed)
+        self.a, self.b = a, b
+
+    def rows(self):
+        return self.oracle.slice_rows_for(self.n_min, self.size, self.mult)
+
+    def step(self, rows=None):
+        """One timed slice; returns (predicted full seconds, slice seconds)."""
+        import numpy as np
+        rows = rows or self.rows()
+        sl = np.ascontiguousarray(self.a[:rows])
         t0 = time.perf_counter()
-        oracle.matmul_block(sl, b, n_min, threads=cores, kernels=kern)
+        self.oracle.matmul_block(sl, self.b, self.n_min, threads=self.cores, kernels=self.kern)
         dt = time.perf_counter() - t0
-        if dt >= seconds / 2 or rows >= n:
-            break
-        rows = min(n, rows * 2 if dt > 0.05 else rows * 8)
-    value = 2.0 * rows * n * n / dt
-    sample = (f"{prec_tok.upper()} blocked n_min={n_min}: leading {rows} rows of A ({n}x{n}) "
-              f"times all of B, {dt:.2f} s, threads={cores} (reference multiply.py "
-              f"_run_partitioned over {'oracle/_ref _kernels' if kern else 'oracle C port'})")
-    return value, cores, kind, sample, dt
+        full = dt * self.size / rows   # predict_full_time with this slice's rows
+        return full, dt
+
+    def fit_budget(self, steps, budget_s):
+        """Pick the slice multiplier so steps x slice fits the budget (the
+        reference's predictor takes k as a parameter, predict.py:37)."""
+        _, dt = self.step(rows=self.rows())
+        while self.mult > 1 and dt * steps > budget_s:
+            self.mult //= 2
+            dt = dt / 2
+        return dt
+
+    def sample(self, slice_s):
+        return (f"{self.prec.upper()} blocked n_min={self.n_min}, threads={self.cores}: the "
+                f"reference's predictor slice (leading {self.rows()} = {self.mult}*n_min rows "
+                f"of A, {self.size}x{self.size}) times all of B in {slice_s:.2f} s, scaled by "
+                f"m/rows = {self.size / self.rows():g} (predict.py:37-50): CPU, predicted; "
+                f"kernels: {'oracle/_ref (the reference _kernels.pyx, compiled)' if self.kern else 'oracle C port'}")
+
+    def value(self, full_s):
+        return 2.0 * float(self.size) ** 3 / full_s
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    if args.nmin <= 0:
-        args.nmin = 64   # the reference's DEFAULT_BLOCK_SIZE (multiply.py:32)
     steps = max(1, args.steps)
-    per_step = max(1.0, min(args.cpu_seconds, 60.0 / (steps + args.warmup)))
-    vals = []
-    for i in range(args.warmup + steps):
-        v, cores, kind, sample, _ = cpu_reference_run(args.prec, args.size, args.nmin, per_step)
-        if i >= args.warmup:
-            vals.append(v)
-    value = statistics.median(vals)
+    ref = ReferenceCPU(args.prec, args.size, args.seed)
+    ref.fit_budget(steps + args.warmup, args.cpu_budget)
+    for _ in range(args.warmup):
+        ref.step()
+    fulls, slices = [], []
+    for _ in range(steps):
+        full, dt = ref.step()
+        fulls.append(full)
+        slices.append(dt)
+    full = statistics.median(fulls)
+    value = ref.value(full)
     line = {
-        "impl": "reference", "metric": metric_name(args), "value": value, "unit": "2mnl/s",
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "2mnl/s",
         "n_gpus": world, "steps": steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": full * 1e3, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, world),
-        "cpu_baseline": {"value": value, "unit": "2mnl/s", "cores": cores, "kind": kind,
-                         "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "2mnl/s", "cores": ref.cores,
+                         "kind": ref.kind, "sample": ref.sample(statistics.median(slices)),
+                         "predicted_full_s": full},
         "e2e": {"value": value, "unit": "2mnl/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def metric_name(args):
-    return f"{args.prec.upper()} GEMM 2mnl/s (blocked, m=l=n={args.size})"
-
-
 def workload_config(args, world):
-    # n_min is each arm's own tuned block size (results never depend on it:
-    # blocked == simple bitwise); the workload itself is the same for both
-    return {"workload": f"BASELINE configs[1]: {args.prec.upper()} blocked GEMM "
-                        f"m=l=n={args.size}, seeded uniform inputs (seed 0)",
-            "prec": args.prec, "m_per_rank": args.size, "l": args.size, "n": args.size,
-            "n_min": args.nmin, "parallelism": f"row-shard x{world}, B NCCL broadcast",
-            "l2": "flushed between steps (256 MiB write), inputs 16 MiB/matrix"}
+    return {"workload": f"BASELINE configs[4]: {args.prec.upper()} GEMM m=l=n={args.size}, "
+                        f"seeded uniform inputs (seed {args.seed}), blocked algorithm "
+                        "(bit-identical mirror of the reference kernels)",
+            "prec": args.prec, "m": args.size, "l": args.size, "n": args.size,
+            "parallelism": (f"C row-sharded over {world} GPUs (64-row aligned), B NCCL "
+                            f"broadcast in {args.panel}-row k-panels" if world > 1 else
+                            "1 GPU"),
+            "l2": "inputs larger than L2 (1 GiB per DD matrix at 8192); no flush needed"
+                  if args.size >= 4096 else "flushed between steps (256 MiB write)"}
 
 
 # ---------------------------------------------------------------------------
@@ -226,14 +282,31 @@ def fp64_peak(torch, _cuda, dev):
     return out
 
 
-def load_ncu_traffic(prec):
+def load_ncu_traffic(key):
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as fp:
-            data = json.load(fp)
-        return data.get(prec, {}).get("dram_bytes_per_launch")
+            return json.load(fp).get(key, {}).get("dram_bytes_per_launch")
     except (OSError, ValueError):
         return None
+
+
+def timed(torch, fn, reps, flush=None, stream=None):
+    """Per-call device seconds (CUDA events on ``stream``), one list entry
+    per rep; the host enqueue is hidden behind a GPU spin."""
+    stream = stream or torch.cuda.current_stream()
+    evs = []
+    for _ in range(reps):
+        if flush is not None:
+            flush.zero_()
+        torch.cuda._sleep(HOST_SLACK_CYCLES)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        fn()
+        e.record(stream)
+        evs.append((s, e))
+    torch.cuda.synchronize()
+    return [s.elapsed_time(e) / 1e3 for s, e in evs]
 
 
 def run_ours(args, rank, world, local_rank):
@@ -248,37 +321,49 @@ def run_ours(args, rank, world, local_rank):
     _cuda.load()
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream()
     prec = mp.PrecisionSpec.parse(args.prec)
     comps = prec.comps
     n = args.size
     F = F_DD if args.prec == "dd" else F_QD
+    elem = 8 * comps
 
-    # per-rank inputs: rank r owns rows [r*n, (r+1)*n) of A; B from rank 0
-    a_full, b_full = inputs.gemm_inputs(args.prec, n, n, n, seed=0)
-    if rank > 0:
-        a_full = inputs.gemm_inputs(args.prec, n, n, n, seed=1000 + rank)[0]
-    A = torch.from_numpy(a_full).to(dev)
-    B = torch.from_numpy(b_full).to(dev) if rank == 0 else torch.empty(
-        (n, n, comps), dtype=torch.float64, device=dev)
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    panel = args.panel if args.panel > 0 else None
-    panels = len(shard.panel_bounds(n, panel))
+    # inputs on the device, bitwise the numpy generator's (csrc/rng.cu)
+    A_full, B_full = inputs.gemm_inputs_device(args.prec, n, n, n, seed=args.seed, device=dev)
+    shards = shard.row_shards(n, world, align=ROW_ALIGN)
+    r0, r1 = shards[rank]
+    A = A_full[r0:r1].contiguous()
+    B = B_full if rank == 0 else torch.empty_like(B_full)
+    if rank != 0:
+        del B_full
+    torch.cuda.synchronize()
+    flush = None if n >= 4096 else torch.empty(64 * 1024 * 1024, dtype=torch.float32,
+                                              device=dev)
+
+    # step 1 of the reference tuner (tune.py:137-143) on the device, outside
+    # the timed region: wave-aware slice prediction over the BASELINE sweep
     tuner = None
     if args.nmin <= 0:
-        # the reference's step 1 (tune.py:137-143) on the device, outside
-        # the timed region: wave-aware prediction over the BASELINE sweep
-        Bt = B if rank == 0 else torch.from_numpy(b_full).to(dev)
+        Bt = B if rank == 0 else B_full_for_tuning(torch, inputs, args, dev)
+        t0 = time.perf_counter()
         best, recs = mp.select_block_size(
-            DenseMatrix(n, n, prec, A), DenseMatrix(n, n, prec, Bt), [16, 32, 64, 128, 256],
+            DenseMatrix(r1 - r0, n, prec, A) if r1 > r0 else DenseMatrix(n, n, prec, A_full),
+            DenseMatrix(n, n, prec, Bt), [16, 32, 64, 128, 256],
             policy=mp.TimingPolicy(warmup_runs=1, measured_runs=3, aggregator="min"))
+        phase = time.perf_counter() - t0
         if world > 1:
             t_best = torch.tensor([best], dtype=torch.int64, device=dev)
             dist.broadcast(t_best, src=0)
             best = int(t_best.item())
         args.nmin = best
-        tuner = {"chosen_n_min": best, "records": [
+        tuner = {"chosen_n_min": best, "prediction_phase_wall_s": phase, "records": [
             {"n_min": r.n_min, "slice_rows": r.slice_rows, "slice_ms": r.slice_time_s * 1e3,
+             "slice2_rows": r.slice2_rows, "slice2_ms": (r.slice2_time_s or 0.0) * 1e3,
              "predicted_ms": r.predicted_full_s * 1e3} for r in recs]}
+    if rank != 0 and world > 1:
+        del A_full
+    panel = args.panel if (args.panel > 0 and world > 1) else None
+    panels = len(shard.panel_bounds(n, panel))
 
     def step():
         return shard.broadcast_matmul(A, B, n_min=args.nmin, src=0, panel_rows=panel)
@@ -291,183 +376,207 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    stream = torch.cuda.current_stream()
-    evs = []
     t_wall0 = time.perf_counter()
-    for _ in range(args.steps):
-        flush.zero_()
-        # keep the GPU busy (outside the timed region) while the host
-        # enqueues the step, so host launch latency is not device time
-        torch.cuda._sleep(HOST_SLACK_CYCLES)
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record(stream)
-        c = step()
-        e.record(stream)
-        evs.append((s, e))
-    torch.cuda.synchronize()
+    step_s = timed(torch, step, args.steps, flush)
     if world > 1:
         dist.barrier()
     t_wall = time.perf_counter() - t_wall0
-    dev_s = sum(s.elapsed_time(e) for s, e in evs) / 1e3
-    gemm_launches = args.steps * panels
+    dev_s = sum(step_s)
+    # per GEMM launch (one per k-panel): the EFT-domain scan, the DFMA
+    # kernel and the gated Dekker kernel (which exits at once in-domain)
+    gemm_launches = args.steps * panels * 3
 
-    # kernel-only time: the GEMM launch alone (no broadcast), events on its stream
-    kev = []
-    for _ in range(max(3, min(args.steps, 10))):
-        flush.zero_()
-        C = torch.empty((n, n, comps), dtype=torch.float64, device=dev)
-        torch.cuda._sleep(HOST_SLACK_CYCLES)
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record(stream)
-        _cuda.gemm_dev(comps, _cuda.ALGO_BLOCK, args.nmin, n, n, n, A.data_ptr(), n,
-                       B.data_ptr(), n, C.data_ptr(), n, False, None, stream.cuda_stream)
-        e.record(stream)
-        kev.append((s, e))
-    torch.cuda.synchronize()
-    kernel_s = statistics.mean(s.elapsed_time(e) for s, e in kev) / 1e3
-    # the opt-in faithful DD mode on the same workload (not bit-identical;
-    # within the north_star bound -- tests/test_gpu_fast.py)
-    fast_s = None
-    if args.prec == "dd":
-        fev = []
-        for _ in range(max(3, min(args.steps, 10))):
-            flush.zero_()
-            torch.cuda._sleep(HOST_SLACK_CYCLES)
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            C = torch.empty((n, n, comps), dtype=torch.float64, device=dev)
-            s.record(stream)
-            _cuda.gemm_dev(comps, _cuda.ALGO_BLOCK_FAST, args.nmin, n, n, n, A.data_ptr(), n,
-                           B.data_ptr(), n, C.data_ptr(), n, False, None, stream.cuda_stream)
-            e.record(stream)
-            fev.append((s, e))
-        torch.cuda.synchronize()
-        fast_s = statistics.mean(s.elapsed_time(e) for s, e in fev) / 1e3
-    # the opt-in exact tensor mode (int8 tensor cores + CRT; exact product
-    # rounded once): whole pipeline timed with events, same workload
-    tensor_s, tensor_err = None, None
-    try:
-        from paper_1710_01839_b200.tensor import matmul_exact_tensors, plan
-        pl = plan(A, B)
-        for _ in range(3):               # plan, capture, replay
-            matmul_exact_tensors(A, B)
-        torch.cuda.synchronize()
-        tev = []
-        for _ in range(max(3, min(args.steps, 10))):
-            flush.zero_()
-            torch.cuda._sleep(HOST_SLACK_CYCLES)
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record(stream)
-            matmul_exact_tensors(A, B)
-            e.record(stream)
-            tev.append((s, e))
-        torch.cuda.synchronize()
-        # median: each product ends in a host read of its status, so a host
-        # hiccup can land inside one sample
-        tensor_s = statistics.median(s.elapsed_time(e) for s, e in tev) / 1e3
-        tensor_jobs = [(pl.ranges_a[ia], pl.ranges_b[ib], N) for ia, ib, N in pl.jobs]
-    except Exception as ex:  # noqa: BLE001 - reported, the headline is unaffected
-        tensor_err = f"{type(ex).__name__}: {ex}"
-    clocks = sampler.stop() if sampler else None
+    # kernel-only time of the GEMM launch (no broadcast) for the roofline
+    rows_local = r1 - r0
+    Ck = torch.empty((max(rows_local, 1), n, comps), dtype=torch.float64, device=dev)
+
+    def kernel():
+        if rows_local:
+            _cuda.gemm_dev(comps, _cuda.ALGO_BLOCK, args.nmin, rows_local, n, n, A.data_ptr(),
+                           n, B.data_ptr(), n, Ck.data_ptr(), n, False, None,
+                           stream.cuda_stream)
+    kernel_s = statistics.mean(timed(torch, kernel, 2 if n >= 4096 else 10, flush))
+    del Ck
 
     t = torch.tensor([dev_s, t_wall, kernel_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dev_s, t_wall, kernel_s = t.tolist()
-    madds_step = float(n) * n * n * world
-    value = 2.0 * madds_step * args.steps / dev_s
+    madds = float(n) ** 3
+    value = 2.0 * madds * args.steps / dev_s
 
     # end-to-end through the public API with host buffers
-    e2e_steps = max(5, min(args.steps, 20))
-    host_a = torch.from_numpy(a_full).pin_memory().numpy()
-    host_b = torch.from_numpy(b_full).pin_memory().numpy()
-    Ah = DenseMatrix(n, n, prec, host_a)
-    Bh = DenseMatrix(n, n, prec, host_b)
+    e2e_steps = 3 if n >= 4096 else 10
     if world == 1:
-        # warm: pools, streams, and the pinned-host cache in the loop's own
-        # pattern -- `ch` keeps the previous result alive while the next is
-        # allocated, so the steady state holds two page-locked results (the
-        # second cudaHostAlloc, ~7 ms, would otherwise land in the timed loop)
+        host_a = A.cpu().pin_memory().numpy()
+        host_b = B.cpu().pin_memory().numpy()
+        Ah, Bh = DenseMatrix(n, n, prec, host_a), DenseMatrix(n, n, prec, host_b)
         ch = None
-        for _ in range(max(3, args.warmup)):
+        for _ in range(2):   # pools, streams, the page-locked result buffers
             ch = mp.matmul_block(Ah, Bh, args.nmin)
+        del ch
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             ch = mp.matmul_block(Ah, Bh, args.nmin)
         e2e_s = time.perf_counter() - t0
+        api = ("paper_1710_01839_b200.matmul_block(host, host) -> C-ABI mpmm_gemm_host (one "
+               "GEMM launch consuming k-panels as their H2D lands, C written to the "
+               "page-locked result from the epilogues, finite check fused)")
     else:
-        for _ in range(max(3, args.warmup)):
-            ch = shard.sharded_matmul_host(host_a, host_b if rank == 0 else None, n, n, prec,
-                                           n_min=args.nmin)
+        host_a = A.cpu().pin_memory().numpy()
+        host_b = B.cpu().pin_memory().numpy() if rank == 0 else None
+        for _ in range(2):
+            ch = shard.sharded_matmul_host(host_a, host_b, n, n, prec, n_min=args.nmin,
+                                           panel_rows=panel)
         dist.barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
-            ch = shard.sharded_matmul_host(host_a, host_b if rank == 0 else None, n, n, prec,
-                                           n_min=args.nmin)
+            ch = shard.sharded_matmul_host(host_a, host_b, n, n, prec, n_min=args.nmin,
+                                           panel_rows=panel)
         dist.barrier()
         e2e_s = time.perf_counter() - t0
+        api = "shard.sharded_matmul_host (per rank: H2D of its A rows, B on rank 0, NCCL " \
+              "broadcast of B in k-panels, GEMM, finite check, D2H of its C rows)"
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = 2.0 * madds_step * e2e_steps / te.item()
-    elem = 8 * comps
-    h2d = elem * (n * n * world + n * n)
-    d2h = elem * n * n * world + 4 * world
+    e2e_value = 2.0 * madds * e2e_steps / te.item()
+    h2d = elem * (n * n + n * n)           # all of A (over the ranks) + B once
+    d2h = elem * n * n + 4 * world         # C + the finite flags
 
+    extras = {}
+    if rank == 0 and world == 1 and not args.no_extras:
+        extras = run_extras(args, torch, _cuda, mp, inputs, DenseMatrix, A, B, dev, stream,
+                            kernel_s)
+    clocks = sampler.stop() if sampler else None
     if rank != 0:
         return
     peak = fp64_peak(torch, _cuda, dev)
-    achieved = F * float(n) ** 3 / kernel_s / 1e12
+    rows_max = max(hi - lo for lo, hi in shards)
+    achieved = F * float(rows_max) * n * n / kernel_s / 1e12
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak["dfma"],
                 "unit": "TFLOP/s", "frac": achieved / peak["dfma"],
-                "traffic": load_ncu_traffic(args.prec),
+                "traffic": load_ncu_traffic(f"{args.prec}{n}"),
                 "peak_source": "in-run DFMA burst micro-benchmark (MEASURED_PEAKS.json has "
                                "no FP64 entry)",
                 "peak_dadd_tflops": peak["dadd"], "peak_spec_tflops": SPEC_FP64_TFLOPS,
+                "frac_of_spec": achieved / SPEC_FP64_TFLOPS,
                 "flops_per_madd": F, "kernel_ms": kernel_s * 1e3,
-                "fp64_issue_frac_of_dfma_peak": (I_DD if args.prec == "dd" else None) and
-                (I_DD * 2 * float(n) ** 3 / kernel_s / 1e12 / peak["dfma"])}
+                "kernel": f"gemm_* <{args.prec.upper()}Ops> blocked mirror, n_min={args.nmin}",
+                "fp64_issue_frac_of_dfma_peak": (I_DD * 2 * float(rows_max) * n * n / kernel_s
+                                                 / 1e12 / peak["dfma"])
+                if args.prec == "dd" else None}
     line = {
-        "metric": metric_name(args), "value": value, "unit": "2mnl/s", "n_gpus": world,
+        "metric": METRIC, "value": value, "unit": "2mnl/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_s / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
-        "config": workload_config(args, world),
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict(workload_config(args, world), n_min=args.nmin),
         "e2e": {"value": e2e_value, "unit": "2mnl/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-                "api": "paper_1710_01839_b200.matmul_block(host, host) -> C-ABI mpmm_gemm_host "
-                       "(one GEMM launch consuming 64-column k-panels as their H2D lands, C "
-                       "written to the page-locked result from the epilogues)" if world == 1 else
-                       "shard.sharded_matmul_host"},
+                "d2h_bytes_per_step": d2h, "steps": e2e_steps, "api": api},
         "roofline": roofline,
         "gpu_launches": gemm_launches,
         "tuner": tuner,
         "wall_s_timed_region": t_wall,
         "clocks": clocks,
     }
-    if fast_s is not None:
-        line["fast_mode"] = {
-            "what": "opt-in faithful DD sequence (15 FP64 instr, F=18 flop/madd), within "
-                    "4*l*u*(|A||B|), u=2^-104; NOT bit-identical to the reference",
-            "value": 2.0 * float(n) ** 3 * world / fast_s, "unit": "2mnl/s",
-            "kernel_ms": fast_s * 1e3,
-            "roofline_frac": 18 * float(n) ** 3 / fast_s / 1e12 / peak["dfma"]}
-    if tensor_s is not None:
-        line["tensor_mode"] = {
-            "what": "opt-in exact mode: int8 tensor-core residue GEMMs (CRT, hand-written tcgen05) + "
-                    "tensor-core CRT sums (mma.sync) + exact reconstruction, product rounded "
-                    "once; more accurate than, not bit-identical to, the reference",
-            "value": 2.0 * float(n) ** 3 * world / tensor_s, "unit": "2mnl/s",
-            "ms": tensor_s * 1e3,
-            "jobs": [{"a_comps": list(ra), "b_comps": list(rb), "moduli": N}
-                     for ra, rb, N in tensor_jobs]}
-    else:
-        line["tensor_mode"] = {"unavailable": tensor_err}
+    for k, v in extras.items():
+        if k != "peak_needed":
+            line[k] = v
+    for sub in ("qd", "cfg1"):
+        if sub in line and "kernel_s" in line[sub]:
+            ks = line[sub].pop("kernel_s")
+            Fs = F_QD if sub == "qd" else F_DD
+            sz = line[sub]["size"]
+            line[sub]["roofline_frac"] = Fs * float(sz) ** 3 / ks / 1e12 / peak["dfma"]
     if world == 1 and not args.no_cpu_baseline:
-        v, cores, kind, sample, _ = cpu_reference_run(args.prec, n, args.nmin, args.cpu_seconds)
-        line["cpu_baseline"] = {"value": v, "unit": "2mnl/s", "cores": cores, "kind": kind,
-                                "sample": sample}
+        ref = ReferenceCPU(args.prec, n, args.seed, a=host_a[:REF_N_MIN * 2].copy(),
+                           b=host_b)
+        full, dt = ref.step()
+        line["cpu_baseline"] = {"value": ref.value(full), "unit": "2mnl/s", "cores": ref.cores,
+                                "kind": ref.kind, "sample": ref.sample(dt),
+                                "predicted_full_s": full}
     print(json.dumps(line), flush=True)
+
+
+def B_full_for_tuning(torch, inputs, args, dev):
+    """Non-source ranks tune against their own copy of B (generated, not
+    received: the tuner runs before the timed broadcasts)."""
+    return inputs.gemm_inputs_device(args.prec, args.size, args.size, args.size,
+                                     seed=args.seed, device=dev)[1]
+
+
+def run_extras(args, torch, _cuda, mp, inputs, DenseMatrix, A, B, dev, stream, block_s):
+    """Sub-fields on one GPU: the tuner's bit-identical pick (Strassen
+    cutoffs against the blocked time), QD at the same size, and BASELINE
+    configs[1] (DD 1024^3 blocked)."""
+    out = {}
+    n = args.size
+    prec = mp.PrecisionSpec.parse(args.prec)
+    comps = prec.comps
+
+    # (1) the tuner's step 2/3 at this size: blocked vs Strassen(cutoff)
+    Ad, Bd = DenseMatrix(n, n, prec, A), DenseMatrix(n, n, prec, B)
+    cand = [c for c in (n // 8, n // 4, n // 2) if c >= 256]
+    strassen = []
+    for cut in cand:
+        mp.matmul_strassen(Ad, Bd, cut, args.nmin)
+        torch.cuda.synchronize()
+        t = min(timed(torch, lambda: mp.matmul_strassen(Ad, Bd, cut, args.nmin), 1))
+        strassen.append({"cutoff": cut, "ms": t * 1e3, "value": 2.0 * float(n) ** 3 / t})
+    best = min(strassen, key=lambda r: r["ms"]) if strassen else None
+    if best is not None and best["ms"] < block_s * 1e3:
+        pick = {"choice": f"strassen:{best['cutoff']}/{args.nmin}", "ms": best["ms"],
+                "value": best["value"]}
+    else:
+        pick = {"choice": f"block:{args.nmin}", "ms": block_s * 1e3,
+                "value": 2.0 * float(n) ** 3 / block_s}
+    out["tuner_pick"] = dict(pick, unit="effective 2mnl/s", bit_identical=True,
+                             candidates={"block": {"n_min": args.nmin, "ms": block_s * 1e3},
+                                         "strassen": strassen})
+
+    # (2) QD at the same size (one product; the kernel is warmed at 1024)
+    if args.prec == "dd" and os.environ.get("BENCH_SKIP_QD") != "1":
+        qd = mp.PrecisionSpec.qd()
+        qn = n
+        Aq, Bq = inputs.gemm_inputs_device("qd", qn, qn, qn, seed=args.seed, device=dev)
+        q_nmin = 64
+        Cq = torch.empty((qn, qn, 4), dtype=torch.float64, device=dev)
+
+        def qd_gemm(m):
+            _cuda.gemm_dev(4, _cuda.ALGO_BLOCK, q_nmin, m, qn, qn, Aq.data_ptr(), qn,
+                           Bq.data_ptr(), qn, Cq.data_ptr(), qn, False, None,
+                           stream.cuda_stream)
+        qd_gemm(128)
+        torch.cuda.synchronize()
+        tq = min(timed(torch, lambda: qd_gemm(qn), 1))
+        out["qd"] = {"what": f"QD blocked mirror m=l=n={qn}, seed {args.seed}, n_min={q_nmin}",
+                     "size": qn, "value": 2.0 * float(qn) ** 3 / tq, "unit": "2mnl/s",
+                     "ms": tq * 1e3, "kernel_s": tq, "flops_per_madd": F_QD}
+        del Aq, Bq, Cq
+
+    # (3) BASELINE configs[1]: DD 1024^3 blocked, seed 0, L2 flushed
+    if args.prec == "dd":
+        s = 1024
+        a1, b1 = inputs.gemm_inputs_device("dd", s, s, s, seed=0, device=dev)
+        c1 = torch.empty((s, s, 2), dtype=torch.float64, device=dev)
+        flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+        res = {}
+        for nm in (32, 64):
+            def g1():
+                _cuda.gemm_dev(2, _cuda.ALGO_BLOCK, nm, s, s, s, a1.data_ptr(), s,
+                               b1.data_ptr(), s, c1.data_ptr(), s, False, None,
+                               stream.cuda_stream)
+            timed(torch, g1, 3, flush)
+            res[nm] = statistics.mean(timed(torch, g1, 20, flush))
+        nm = min(res, key=res.get)
+        out["cfg1"] = {"what": "BASELINE configs[1]: DD blocked m=l=n=1024, seed 0, L2 flushed",
+                       "size": s, "n_min": nm, "value": 2.0 * s ** 3 / res[nm],
+                       "unit": "2mnl/s", "ms": res[nm] * 1e3, "kernel_s": res[nm]}
+        del a1, b1, c1, flush
+    torch.cuda.empty_cache()
+    return out
 
 
 def main():

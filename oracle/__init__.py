@@ -232,3 +232,25 @@ def ref_kernels():
     mod = importlib.util.module_from_spec(spec)
     loader.exec_module(mod)
     return mod
+
+
+# ---------------------------------------------------------------------------
+# the reference's slice predictor (predict.py:37-50), for the "CPU, predicted"
+# baseline at sizes where a full reference run takes tens of minutes
+# ---------------------------------------------------------------------------
+
+DEFAULT_SLICE_MULTIPLIER = 2   # predict.py:20
+
+
+def slice_rows_for(n_min, m, slice_multiplier=DEFAULT_SLICE_MULTIPLIER):
+    """predict.py:37-42: rows of A in the timed slice, min(k * n_min, m)."""
+    if n_min < 1 or m < 1 or slice_multiplier < 1:
+        raise ValueError("block size, row count and multiplier must be positive")
+    return min(slice_multiplier * n_min, m)
+
+
+def predict_full_time(slice_time_s, m, n_min, slice_multiplier=DEFAULT_SLICE_MULTIPLIER):
+    """predict.py:45-50: the slice time scaled by m / slice rows."""
+    if slice_time_s <= 0.0:
+        raise ValueError("slice time must be positive")
+    return slice_time_s * (m / slice_rows_for(n_min, m, slice_multiplier))

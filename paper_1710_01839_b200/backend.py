@@ -14,6 +14,7 @@ reference's tests switch between ``ext`` and ``python``
 """
 
 import os
+import warnings
 
 from . import _cuda
 from .errors import DeviceError
@@ -24,11 +25,24 @@ PROTOCOL = ("dd_simple_rows", "dd_block_cells", "dd_ewise_add", "dd_ewise_sub",
 _registry = {"cuda": _cuda}
 _active_name = "cuda"
 
-HAVE_EXT = _cuda.available()
 
+def __getattr__(name):
+    # HAVE_EXT is evaluated on first use, not at import: importing the
+    # package must not map libmpmm_cuda.so (a CPU-only caller -- e.g. the
+    # bench's reference arm -- imports helpers without touching the GPU)
+    if name == "HAVE_EXT":
+        return _cuda.available()
+    raise AttributeError(name)
+
+
+# The reference reads MPMM_BACKEND at import (backend.py:22-25): "python"
+# forces its pure-Python kernels, anything else is ignored.  Neither CPU
+# backend exists here, so the variable is ignored with a warning rather than
+# making the package unimportable for environments that set it.
 _env = os.environ.get("MPMM_BACKEND")
 if _env and _env != "cuda":
-    raise ValueError(f"MPMM_BACKEND={_env!r}: only the 'cuda' backend ships with this package")
+    warnings.warn(f"MPMM_BACKEND={_env!r} ignored: this package ships only the 'cuda' "
+                  "backend (no CPU kernels)", RuntimeWarning, stacklevel=2)
 
 
 def kernels():

@@ -84,9 +84,10 @@ void tile_for(int64_t n_min, int* tile, int* super) {
   }
 }
 
-cudaError_t gemm(int comps, const GemmArgs& g) {
-  return comps == 2 ? dd_gemm_launch(g) : qd_gemm_launch(g);
-}
+// Every mirror product goes through the EFT-domain gate (domain.cuh):
+// scan, then the DFMA launch or the Dekker launch, so results equal the
+// reference's on every input.
+cudaError_t gemm(int comps, const GemmArgs& g) { return gemm_checked(comps, g); }
 
 // ---------------------------------------------------------------------------
 // host-pointer protocol plumbing: per-thread streams, stream-ordered buffers
@@ -147,6 +148,12 @@ int block_cells_impl(int comps, int64_t n_min, int64_t cell0, int64_t cell1, int
   if (cell0 < 0 || cell1 > nbc * nbr) return fail(MPMM_ERR_ARG, "cell range out of bounds");
   int tile, super;
   tile_for(n_min, &tile, &super);
+  // one domain scan of A and B covers every rectangle below
+  const int* words = nullptr;
+  if (l > 0) {
+    cudaError_t e = domain_scan(comps, A, lda, (int)m, (int)l, B, ldb, (int)n, &words, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "block_cells domain scan");
+  }
   // The flattened cell range [cell0, cell1) is at most three rectangles:
   // the tail of the first block row, whole block rows, the head of the last.
   auto rect = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) -> int {
@@ -156,7 +163,7 @@ int block_cells_impl(int comps, int64_t n_min, int64_t cell0, int64_t cell1, int
     GemmArgs g{ALGO_BLOCK, tile, (int)(r1 - r0), (int)(c1 - c0), (int)l,
                A + comps * (r0 * lda), lda, B + comps * c0, ldb,
                C + comps * (r0 * ldc + c0), ldc, 1, nullptr, stream};
-    cudaError_t e = gemm(comps, g);
+    cudaError_t e = words ? gemm_gated(comps, g, words) : gemm(comps, g);
     return e == cudaSuccess ? MPMM_OK : cuda_fail(e, "block_cells launch");
   };
   const int64_t ib0 = cell0 / nbc, jb0 = cell0 % nbc;
@@ -281,6 +288,13 @@ int host_rows_gemm_streamed(int comps, int tile, int64_t rows, int64_t l, int64_
     }
     CU(cudaMemcpyAsync(dint + 1 + p, one, sizeof(int), cudaMemcpyHostToDevice, hs->copy));
   }
+  // The streamed launch runs the DFMA kernel before the operands have
+  // landed, so their domain check (domain.cuh) follows the copies on the
+  // copy stream, concurrent with the GEMM's tail.
+  const int* words = nullptr;
+  CU(domain_scan(comps, dA.p, l, (int)rows, (int)l, dB.p, n, (int)n, &words, hs->copy));
+  int w[kDomainWords];
+  CU(cudaMemcpyAsync(w, words, sizeof(w), cudaMemcpyDeviceToHost, hs->copy));
   int status = 0;   // pageable target: the copy completes before cudaMemcpyAsync returns
   CU(cudaMemcpyAsync(&status, dint, sizeof(int), cudaMemcpyDeviceToHost, hs->comp));
   CU(cudaStreamSynchronize(hs->copy));
@@ -291,6 +305,16 @@ int host_rows_gemm_streamed(int comps, int tile, int64_t rows, int64_t l, int64_
     // caller recompute with it
     g_streamed_off.store(true);
     return -1;
+  }
+  // operands outside the DFMA-exact domain: recompute C with the
+  // reference's Dekker sequence (the rare path)
+  if (domain_unsafe(w, 0, 0)) {
+    CU(cudaMemsetAsync(dint, 0, sizeof(int), hs->comp));
+    GemmArgs d{ALGO_BLOCK, tile, (int)rows, (int)n, (int)l, dA.p, l, dB.p, n, dCh, n, 0, dint,
+               hs->comp};
+    CU(comps == 2 ? dd_dekker_launch(d) : qd_dekker_launch(d));
+    CU(cudaMemcpyAsync(&status, dint, sizeof(int), cudaMemcpyDeviceToHost, hs->comp));
+    CU(cudaStreamSynchronize(hs->comp));
   }
   if (nonfinite_host) *nonfinite_host = status & 1;
   return MPMM_OK;
@@ -385,6 +409,11 @@ int host_rows_gemm(int comps, int algo, int64_t n_min, int64_t rows, int64_t l, 
     CU(cudaStreamWaitEvent(hs->comp, ev[p].e, 0));
     const bool last = (k1 >= l);
     const int acc = (accumulate_c || p > 0) ? 1 : 0;
+    // the panel's operands (every row slice below) in one domain scan
+    const int* words = nullptr;
+    if (algo != ALGO_BLOCK_FAST && k1 > k0)
+      CU(domain_scan(comps, dA.p + k0 * comps, l, (int)rows, (int)(k1 - k0),
+                     dB.p + k0 * n * comps, n, (int)n, &words, hs->comp));
     // the finite check only needs the final values: flag the last panel
     const int64_t sstep = last ? srows : rows;
     for (int64_t q0 = 0, si = 0; q0 < rows; q0 += sstep, ++si) {
@@ -392,7 +421,7 @@ int host_rows_gemm(int comps, int algo, int64_t n_min, int64_t rows, int64_t l, 
       GemmArgs g{algo, tile, (int)(q1 - q0), (int)n, (int)(k1 - k0),
                  dA.p + (q0 * l + k0) * comps, l, dB.p + k0 * n * comps, n,
                  dC.p + q0 * n * comps, n, acc, last ? dflag : nullptr, hs->comp};
-      CU(gemm(comps, g));
+      CU(words ? gemm_gated(comps, g, words) : gemm(comps, g));
       if (last && q1 < rows) {   // this slice is final: copy it out under the next one
         CU(sl[si].make());
         CU(cudaEventRecord(sl[si].e, hs->comp));

@@ -77,6 +77,31 @@ __device__ __forceinline__ double two_prod(double a, double b, double& err) {
   return p;
 }
 
+// _kernels.pyx:19-29 _two_prod verbatim: Veltkamp split by 2^27 + 1 and
+// Dekker's product.  Outside the domain where its error is exact (a split
+// overflows for |x| >= ~2^996 -- the NaN the reference then returns --, or
+// the error falls below the subnormal floor) it differs from two_prod; the
+// GEMM launches route such operands here (domain.cuh), so the reference's
+// results are reproduced there too, NaN for NaN.
+__device__ __forceinline__ double two_prod_dekker(double a, double b, double& err) {
+  const double splitter = 134217729.0;   // 2^27 + 1
+  double p = a * b;
+  double t = splitter * a;
+  double ahh = t - (t - a);
+  double ahl = a - ahh;
+  t = splitter * b;
+  double bhh = t - (t - b);
+  double bhl = b - bhh;
+  err = ((ahh * bhh - p) + ahh * bhl + ahl * bhh) + ahl * bhl;
+  return p;
+}
+
+template <bool DEKKER>
+__device__ __forceinline__ double two_prod_t(double a, double b, double& err) {
+  if constexpr (DEKKER) return two_prod_dekker(a, b, err);
+  else return two_prod(a, b, err);
+}
+
 // ---------------------------------------------------------------------------
 // double-double
 // ---------------------------------------------------------------------------
@@ -96,13 +121,13 @@ __device__ __forceinline__ void dd_add(double xh, double xl, double yh, double y
 
 // ddqd.py:77-91 dd_mul, as inlined at _kernels.pyx:140-171
 // (4 DMUL + 3 DFMA + 23 DADD; 17 DADD when ORD).
-template <bool ORD = false>
+template <bool ORD = false, bool DEKKER = false>
 __device__ __forceinline__ void dd_mul(double ah, double al, double bh, double bl,
                                        double& ph, double& pl) {
   double e, e1, e2, r1, r2, w;
-  double p = two_prod(ah, bh, e);
-  double p1 = two_prod(ah, bl, e1);
-  double p2 = two_prod(al, bh, e2);
+  double p = two_prod_t<DEKKER>(ah, bh, e);
+  double p1 = two_prod_t<DEKKER>(ah, bl, e1);
+  double p2 = two_prod_t<DEKKER>(al, bh, e2);
   double tail = (e1 + e2) + al * bl;
   double s = two_sum_t<ORD>(p1, p2, r1);
   s = two_sum_t<ORD>(e, s, r2);
@@ -116,11 +141,13 @@ __device__ __forceinline__ void dd_mul(double ah, double al, double bh, double b
 // c <- dd_add(c, dd_mul(a, b)).  50 FP64 instructions, 53 flops; with
 // ORD the four TwoSums run as two_sum_ord: 38 FP64 instructions (4 DMUL +
 // 3 DFMA + 31 DADD) + 4 FSETP + 16 SEL, same bits.
-template <bool ORD = false>
+// DEKKER: the reference's split TwoProd (two_prod_dekker), for operands
+// outside the DFMA-exact domain.
+template <bool ORD = false, bool DEKKER = false>
 __device__ __forceinline__ void dd_madd(double& ch, double& cl, double ah, double al,
                                         double bh, double bl) {
   double ph, pl;
-  dd_mul<ORD>(ah, al, bh, bl, ph, pl);
+  dd_mul<ORD, DEKKER>(ah, al, bh, bl, ph, pl);
   dd_add<ORD>(ch, cl, ph, pl, ch, cl);
 }
 
@@ -329,19 +356,20 @@ __device__ __forceinline__ void compress4_slow(const double (&v)[N], double out[
 // _kernels.pyx:311-341 _qd_mul_add: cc += x*y, bit-identical.
 // M23 / M8: ORDMASKs of the product's 23-term and the accumulate's 8-term
 // compressions (see compress4_dense).
-template <int M23 = 0, int M8 = 0>
+// DEKKER: the reference's split TwoProd (outside the DFMA-exact domain).
+template <int M23 = 0, int M8 = 0, bool DEKKER = false>
 __device__ __forceinline__ void qd_mul_add(double cc[4], const double x[4], const double y[4]) {
   double t[23];
-  t[0] = two_prod(x[0], y[0], t[1]);
-  t[2] = two_prod(x[0], y[1], t[3]);
-  t[4] = two_prod(x[1], y[0], t[5]);
-  t[6] = two_prod(x[0], y[2], t[7]);
-  t[8] = two_prod(x[1], y[1], t[9]);
-  t[10] = two_prod(x[2], y[0], t[11]);
-  t[12] = two_prod(x[0], y[3], t[13]);
-  t[14] = two_prod(x[1], y[2], t[15]);
-  t[16] = two_prod(x[2], y[1], t[17]);
-  t[18] = two_prod(x[3], y[0], t[19]);
+  t[0] = two_prod_t<DEKKER>(x[0], y[0], t[1]);
+  t[2] = two_prod_t<DEKKER>(x[0], y[1], t[3]);
+  t[4] = two_prod_t<DEKKER>(x[1], y[0], t[5]);
+  t[6] = two_prod_t<DEKKER>(x[0], y[2], t[7]);
+  t[8] = two_prod_t<DEKKER>(x[1], y[1], t[9]);
+  t[10] = two_prod_t<DEKKER>(x[2], y[0], t[11]);
+  t[12] = two_prod_t<DEKKER>(x[0], y[3], t[13]);
+  t[14] = two_prod_t<DEKKER>(x[1], y[2], t[15]);
+  t[16] = two_prod_t<DEKKER>(x[2], y[1], t[17]);
+  t[18] = two_prod_t<DEKKER>(x[3], y[0], t[19]);
   t[20] = x[1] * y[3];
   t[21] = x[2] * y[2];
   t[22] = x[3] * y[1];

@@ -57,6 +57,26 @@ struct QDOps {
   }
 };
 
+// The reference's sequences with its Dekker TwoProd (_kernels.pyx:19-29),
+// for operands outside the DFMA-exact domain (domain.cuh).
+struct DDDekkerOps {
+  static constexpr int V = 1;
+  static constexpr int NACC = 2;
+  __device__ __forceinline__ static void madd(double* acc, const double2* a, const double2* b) {
+    dd_madd<false, true>(acc[0], acc[1], a[0].x, a[0].y, b[0].x, b[0].y);
+  }
+};
+
+struct QDDekkerOps {
+  static constexpr int V = 2;
+  static constexpr int NACC = 4;
+  __device__ __forceinline__ static void madd(double* acc, const double2* a, const double2* b) {
+    const double x[4] = {a[0].x, a[0].y, a[1].x, a[1].y};
+    const double y[4] = {b[0].x, b[0].y, b[1].x, b[1].y};
+    qd_mul_add<0, 0, true>(acc, x, y);
+  }
+};
+
 // Problem descriptor (pointers as double2 views, leading dims in elements).
 struct Prob {
   const double2* A;
@@ -239,9 +259,11 @@ __device__ __forceinline__ void gemm_tile(const Prob& pr, int m, int n, int l, i
 template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB, bool STREAM = false>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
 gemm_tiled(const GemmProblem* __restrict__ probs, Prob single, int m, int n, int l,
-           int accumulate, int* __restrict__ nonfinite, const KReady kr) {
+           int accumulate, int* __restrict__ nonfinite, const KReady kr,
+           const DomainGate gate) {
   constexpr int NT = (BM / TM) * (BN / TN);
   __shared__ __align__(16) double2 smem[TileSmem<Ops, BM, BN, BK>::TOTAL];
+  if (gate_skip(gate)) return;
   const int tiles_n = (n + BN - 1) / BN, tiles_m = (m + BM - 1) / BM;
   const int per = tiles_m * tiles_n;
   const int p = blockIdx.x / per, t = blockIdx.x % per;
@@ -259,10 +281,11 @@ gemm_tiled(const GemmProblem* __restrict__ probs, Prob single, int m, int n, int
 template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
 gemm_lpt(const GemmProblem* __restrict__ probs, Prob single, int P, int m, int n, int l,
-         int accumulate, int* __restrict__ nonfinite) {
+         int accumulate, int* __restrict__ nonfinite, const DomainGate gate) {
   constexpr int NT = (BM / TM) * (BN / TN);
   static_assert(TM % 2 == 0 && TN % 2 == 0, "quarter tiles need even thread tiles");
   __shared__ __align__(16) double2 smem[TileSmem<Ops, BM, BN, BK>::TOTAL];
+  if (gate_skip(gate)) return;
   const int tiles_n = (n + BN - 1) / BN, tiles_m = (m + BM - 1) / BM;
   const int per = tiles_m * tiles_n;
   const int T = P * per;
@@ -299,8 +322,9 @@ gemm_lpt(const GemmProblem* __restrict__ probs, Prob single, int P, int m, int n
 template <class Ops>
 __global__ void __launch_bounds__(256)
 gemm_simple(const GemmProblem* __restrict__ probs, Prob single, int m, int n, int l,
-            int accumulate, int* __restrict__ nonfinite) {
+            int accumulate, int* __restrict__ nonfinite, const DomainGate gate) {
   constexpr int V = Ops::V;
+  if (gate_skip(gate)) return;
   const int p = blockIdx.z;
   const Prob pr = get_prob(probs, single, p);
   int j = blockIdx.x * 32 + (threadIdx.x & 31);
@@ -352,10 +376,10 @@ cudaError_t launch_tiled(const GemmArgs& g) {
   const KReady kr{g.kready, g.kpanel};
   if (g.kready != nullptr)
     gemm_tiled<Ops, BM, BN, BK, TM, TN, MINB, true><<<grid, nt, 0, g.stream>>>(
-        g.probs, single_prob(g), g.m, g.n, g.l, g.accumulate, g.nonfinite, kr);
+        g.probs, single_prob(g), g.m, g.n, g.l, g.accumulate, g.nonfinite, kr, g.gate);
   else
     gemm_tiled<Ops, BM, BN, BK, TM, TN, MINB, false><<<grid, nt, 0, g.stream>>>(
-        g.probs, single_prob(g), g.m, g.n, g.l, g.accumulate, g.nonfinite, kr);
+        g.probs, single_prob(g), g.m, g.n, g.l, g.accumulate, g.nonfinite, kr, g.gate);
   return cudaGetLastError();
 }
 
@@ -376,7 +400,7 @@ cudaError_t launch_lpt(const GemmArgs& g) {
   int64_t units = tiles < slots ? 4 * tiles : slots;
   int grid = (int)(units < slots ? units : slots);
   kern<<<grid, NT, 0, g.stream>>>(g.probs, single_prob(g), g.batch, g.m, g.n, g.l,
-                                  g.accumulate, g.nonfinite);
+                                  g.accumulate, g.nonfinite, g.gate);
   return cudaGetLastError();
 }
 
@@ -385,7 +409,7 @@ cudaError_t launch_simple(const GemmArgs& g) {
   if (g.batch > 65535) return cudaErrorInvalidValue;
   dim3 grid((g.n + 31) / 32, (g.m + 7) / 8, g.batch), block(256);
   gemm_simple<Ops><<<grid, block, 0, g.stream>>>(g.probs, single_prob(g), g.m, g.n, g.l,
-                                                 g.accumulate, g.nonfinite);
+                                                 g.accumulate, g.nonfinite, g.gate);
   return cudaGetLastError();
 }
 

@@ -61,6 +61,12 @@ cudaError_t dd_gemm_launch(const GemmArgs& g) {
   return dd_blocked<DDOps>(g);
 }
 
+cudaError_t dd_dekker_launch(const GemmArgs& g) {
+  if (g.m <= 0 || g.n <= 0 || g.batch <= 0) return cudaSuccess;
+  if (g.kready != nullptr) return cudaErrorNotSupported;
+  return launch_tiled<DDDekkerOps, 32, 32, 16, 2, 2, 2>(g);
+}
+
 cudaError_t dd_gemm_geometry(int algo, int tile, Geometry* geo) {
   if (algo == ALGO_BLOCK_FAST) {
     switch (tile) {

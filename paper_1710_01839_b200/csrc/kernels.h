@@ -7,6 +7,8 @@
 #include <cstdint>
 #include <string>
 
+#include "domain.cuh"
+
 namespace mpmm {
 
 enum Algo { ALGO_SIMPLE = 0, ALGO_BLOCK = 1, ALGO_BLOCK_FAST = 2 };
@@ -44,10 +46,36 @@ struct GemmArgs {
   // are kpanel columns of k.  Null: the operands are already resident.
   const int* kready = nullptr;
   int kpanel = 0;
+  // EFT-domain gate (domain.cuh): with gate.words set, the launch runs only
+  // on the side of the domain test gate.want_unsafe selects.
+  DomainGate gate{};
 };
 
+// The DFMA mirror kernels (ALGO_SIMPLE / ALGO_BLOCK / ALGO_BLOCK_FAST).
 cudaError_t dd_gemm_launch(const GemmArgs& g);
 cudaError_t qd_gemm_launch(const GemmArgs& g);
+// The same products with the reference's Dekker TwoProd (one tile shape for
+// every algorithm: per element the operation sequence is the reference's, so
+// the tiling never changes a bit).  No streamed operands.
+cudaError_t dd_dekker_launch(const GemmArgs& g);
+cudaError_t qd_dekker_launch(const GemmArgs& g);
+
+// Scan the operands of one product (A: m x l, B: l x n views) into the six
+// domain words (domain.cuh) of a per-stream buffer; *words receives the
+// device pointer, valid in stream order until the next scan on `stream`.
+cudaError_t domain_scan(int comps, const double* A, int64_t lda, int m, int l, const double* B,
+                        int64_t ldb, int n, const int** words, cudaStream_t stream);
+// The same over every problem of a batched launch (one set of words).
+cudaError_t domain_scan_batched(int comps, const GemmProblem* probs, int batch, int m, int l,
+                                int n, const int** words, cudaStream_t stream);
+// A mirror product with the reference's semantics on every input: scan,
+// then the DFMA launch gated on the domain and the Dekker launch gated on
+// its complement (g.gate's margins are kept; its words are replaced).
+// ALGO_BLOCK_FAST (not a mirror) and streamed launches run ungated.
+// When `words_out` is non-null the scan's words pointer is stored there.
+cudaError_t gemm_checked(int comps, GemmArgs g, const int** words_out = nullptr);
+// The two gated launches of gemm_checked for operands already scanned.
+cudaError_t gemm_gated(int comps, GemmArgs g, const int* words);
 
 // CTA tile and residency of the kernel a launch would use.
 struct Geometry {

@@ -307,7 +307,9 @@ int rt_gemm_host(int comps, int algo, int tile, int64_t cutoff, int64_t m, int64
         GemmArgs ga{algo, tile, (int)rows, (int)n, (int)(k1 - k0), s.A + k0 * comps, l,
                     s.B + k0 * n * comps, n, s.C, n, p > 0 ? 1 : 0, last ? s.flag : nullptr,
                     d.comp};
-        RT_CU(comps == 2 ? dd_gemm_launch(ga) : qd_gemm_launch(ga));
+        // per panel: domain scan of its operands, then the gated DFMA /
+        // Dekker launches (domain.cuh)
+        RT_CU(gemm_checked(comps, ga));
       }
     }
     for (int g = 0; g < G; ++g) {

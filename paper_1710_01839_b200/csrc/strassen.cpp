@@ -50,6 +50,19 @@ class Driver {
   Driver(int comps, int64_t cutoff, int tile, cudaStream_t s, int64_t* stats)
       : comps_(comps), cutoff_(cutoff), tile_(tile), s_(s), stats_(stats) {}
 
+  // The EFT-domain words of the top-level operands and the recursion depth
+  // (the leaf launches' gate margins).
+  cudaError_t scan_top(const View& A, const View& B, int64_t m, int64_t l, int64_t n) {
+    depth_ = 0;
+    for (int64_t a = m, b = l, c = n; std::min(a, std::min(b, c)) > cutoff_; ++depth_) {
+      a = (a + (a & 1)) / 2;
+      b = (b + (b & 1)) / 2;
+      c = (c + (c & 1)) / 2;
+    }
+    if (l == 0) return cudaSuccess;
+    return domain_scan(comps_, A.p, A.ld, (int)m, (int)l, B.p, B.ld, (int)n, &words_, s_);
+  }
+
   // scratch allocations of the current scope, freed stream-ordered
   cudaError_t alloc(int64_t rows, int64_t cols, bool zero, View* v) {
     size_t bytes = static_cast<size_t>(rows * cols * comps_) * sizeof(double);
@@ -114,7 +127,12 @@ class Driver {
                  0, nullptr, s_};
       g.batch = static_cast<int>(std::min<size_t>(kMaxBatch, probs.size() - q));
       g.probs = static_cast<const GemmProblem*>(d) + q;
-      e = comps_ == 2 ? dd_gemm_launch(g) : qd_gemm_launch(g);
+      // leaf operands are sums of scanned top-level quadrants: the
+      // domain gate with the Strassen margins (domain.cuh)
+      g.gate.words = words_;
+      g.gate.margin_lo = depth_ > 0 ? 52 : 0;
+      g.gate.margin_hi = depth_ > 0 ? depth_ + 1 : 0;
+      e = gemm_checked(comps_, g);
     }
     return e;
   }
@@ -313,6 +331,8 @@ class Driver {
   cudaStream_t s_;
   int64_t* stats_;
   std::vector<void*> scope_;
+  const int* words_ = nullptr;
+  int depth_ = 0;
 };
 
 }  // namespace
@@ -337,6 +357,8 @@ cudaError_t strassen_run(int comps, int64_t cutoff, int tile, int64_t m, int64_t
   }
   Driver d(comps, cutoff, tile, stream, stats);
   View a{const_cast<double*>(A), lda, m, l}, b{const_cast<double*>(B), ldb, l, n}, c{C, ldc, m, n};
+  cudaError_t se = d.scan_top(a, b, m, l, n);
+  if (se != cudaSuccess) return se;
   return d.solve(a, b, c, m, l, n, budget);
 }
 

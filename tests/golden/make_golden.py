@@ -145,5 +145,129 @@ def main():
     save("dd_int_2x2", a=ia.data, b=ib.data, c=matmul_simple(ia, ib).data)
 
 
+def edge_cases():
+    """EFT-domain edge cases (eft.py:19-24, _kernels.pyx:19-29): operands
+    where the reference's split TwoProd overflows (|x| >= ~2^996: NaN) or
+    its error leaves the representable range (products near 2^-969,
+    subnormals), signed zeros in every limb, inf and NaN.  Recorded: the
+    raw kernel output of the reference's ext backend (simple rows and block
+    cells, which never raise) and whether the public matmul_simple raises
+    RangeError (multiply.py:124-127)."""
+    mpmm = load_reference()
+    from mpmm import backend
+    from mpmm.errors import RangeError
+    from mpmm.matrix import DenseMatrix
+    from mpmm.multiply import matmul_simple, matmul_strassen
+    from mpmm.scalar import PrecisionSpec
+
+    sys.path.insert(0, REPO)
+    from paper_1710_01839_b200 import inputs
+
+    kern = backend.kernels()
+    assert kern.NAME == "ext"
+    DD, QD = PrecisionSpec.dd(), PrecisionSpec.qd()
+
+    def M(arr, prec):
+        return DenseMatrix(arr.shape[0], arr.shape[1], prec, np.ascontiguousarray(arr))
+
+    def record(name, a, b, prec, n_min=4):
+        comps = a.shape[2]
+        pre = "dd" if comps == 2 else "qd"
+        m, n = a.shape[0], b.shape[1]
+        cs = np.zeros((m, n, comps))
+        getattr(kern, f"{pre}_simple_rows")(a, b, cs, 0, m)
+        cb = np.zeros((m, n, comps))
+        cells = (-(-m // n_min)) * (-(-n // n_min))
+        getattr(kern, f"{pre}_block_cells")(a, b, cb, n_min, 0, cells)
+        assert np.array_equal(cs, cb, equal_nan=True)
+        try:
+            matmul_simple(M(a, prec), M(b, prec))
+            raises = 0
+        except RangeError:
+            raises = 1
+        np.savez(os.path.join(HERE, name + ".npz"), a=a, b=b, c=cs,
+                 raises=np.array(raises), n_min=np.array(n_min))
+        print("wrote", name, "raises" if raises else "ok",
+              "nan" if np.isnan(cs).any() else "")
+
+    m, l, n = 6, 7, 5
+    base_a, base_b = inputs.gemm_inputs("dd", m, l, n, seed=40)
+
+    def dd_scaled(ea, eb, rows=(0, 2), cols=(1, 3)):
+        a, b = base_a.copy(), base_b.copy()
+        for i in rows:
+            a[i] = np.ldexp(a[i], ea)
+        for j in cols:
+            b[:, j] = np.ldexp(b[:, j], eb)
+        return a, b
+
+    # split overflow side: 2^995 (inside the reference's range), 2^996 and
+    # 2^996.9 (the boundary), 2^1000 (overflowed split -> NaN)
+    for tag, ea, eb in (("big995", 995, -990), ("big996", 996, -996), ("big997", 997, -997),
+                        ("big1000", 1000, -1000)):
+        a, b = dd_scaled(ea, eb)
+        record(f"edge_dd_{tag}", a, b, DD)
+    a, b = dd_scaled(996, -996)
+    a[0, 0] = [1.99 * 2.0 ** 996, 2.0 ** 943]
+    record("edge_dd_big996_9", a, b, DD)
+    # error underflow side: products near 2^-969, subnormal operands
+    for tag, ea, eb in (("tiny969", -500, -470), ("tiny1000", -520, -480),
+                        ("tiny1040", -540, -500)):
+        a, b = dd_scaled(ea, eb)
+        record(f"edge_dd_{tag}", a, b, DD)
+    a, b = base_a.copy(), base_b.copy()
+    a[1, :, 0] = np.ldexp(np.abs(a[1, :, 0]) + 0.5, -1060)   # subnormal high words
+    a[1, :, 1] = 0.0
+    b[:, 2] = np.ldexp(b[:, 2], -3)
+    record("edge_dd_subnormal", a, b, DD)
+    # signed zeros, inf, NaN
+    a, b = base_a.copy(), base_b.copy()
+    a[0] = 0.0
+    a[1] = -0.0
+    a[2, :, 1] = -0.0
+    b[:, 0] = -0.0
+    b[3, :, 1] = 0.0
+    b[4] = [-0.0, 0.0]
+    record("edge_dd_zeros", a, b, DD)
+    a, b = base_a.copy(), base_b.copy()
+    a[2, 3] = [np.inf, 0.0]
+    b[1, 4] = [np.nan, 0.0]
+    record("edge_dd_inf_nan", a, b, DD)
+    # a product that overflows, finite operands (2^600 * 2^500)
+    a, b = dd_scaled(600, 500)
+    record("edge_dd_overflow", a, b, DD)
+
+    # QD: signed-zero limbs in every position, big and tiny limbs
+    qa, qb = inputs.gemm_inputs("qd", 5, 6, 4, seed=41)
+    a, b = qa.copy(), qb.copy()
+    a[0, :, 3] = 0.0
+    a[1, :, 2:] = -0.0
+    a[2, 0] = [0.0, -0.0, 0.0, -0.0]
+    b[:, 1, 1:] = 0.0
+    b[2] = -0.0
+    b[3, :, 3] = -0.0
+    record("edge_qd_zeros", a, b, QD, n_min=2)
+    a, b = qa.copy(), qb.copy()
+    a[0] = np.ldexp(a[0], 997)
+    b[:, 0] = np.ldexp(b[:, 0], -997)
+    record("edge_qd_big997", a, b, QD, n_min=2)
+    a, b = qa.copy(), qb.copy()
+    a[1] = np.ldexp(a[1], -300)
+    b[:, 2] = np.ldexp(b[:, 2], -500)
+    record("edge_qd_tiny", a, b, QD, n_min=2)
+
+    # Strassen on large operands: the leaf operands are quadrant sums
+    sa, sb = inputs.gemm_inputs("dd", 16, 16, 16, seed=42)
+    sa = np.ldexp(sa, 993)
+    sb = np.ldexp(sb, -993)
+    cs = matmul_strassen(M(sa, DD), M(sb, DD), 4, 2)
+    np.savez(os.path.join(HERE, "edge_dd_strassen_big.npz"), a=sa, b=sb, c=cs.data)
+    print("wrote edge_dd_strassen_big")
+
+
 if __name__ == "__main__":
-    main()
+    if "--edge" in sys.argv:
+        edge_cases()
+    else:
+        main()
+        edge_cases()

@@ -77,18 +77,20 @@ def test_bench_two_ranks_json(gpu):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={_port()}",
            os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
-           "--nmin", "32", "--size", "256", "--dist-backend", "gloo", "--same-device",
-           "--no-cpu-baseline"]
+           "--nmin", "32", "--size", "256", "--panel", "64", "--dist-backend", "gloo",
+           "--same-device", "--no-cpu-baseline", "--no-extras"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
-    assert d["gpu_launches"] == 3 and d["scaling"] == "weak"
+    # strong scaling: 3 steps x 4 k-panels x (domain scan, DFMA GEMM, gated Dekker GEMM)
+    assert d["gpu_launches"] == 3 * 4 * 3 and d["scaling"] == "strong"
+    assert d["config"]["m"] == 256 and d["roofline"]["frac"] > 0
     # the reference arm under torchrun: rank 0 prints, the other exits 0
     cmd2 = cmd[:cmd.index("--gpus")] + ["--impl", "reference", "--gpus", "2", "--steps", "1",
-                                        "--warmup", "0", "--size", "128", "--cpu-seconds", "1"]
+                                        "--warmup", "0", "--size", "128", "--cpu-budget", "5"]
     r2 = subprocess.run(cmd2, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r2.returncode == 0, r2.stderr[-3000:]
     lines = [ln for ln in r2.stdout.splitlines() if ln.startswith("{")]

@@ -116,3 +116,45 @@ def test_oracle_matches_compiled_reference(tok, shape, n_min):
     out = np.zeros_like(a)
     getattr(ref, f"{tok}_ewise_sub")(a, a[::-1].copy(), out, 0, m)
     assert np.array_equal(out, oracle.ewise_new(a, a[::-1].copy(), True))
+
+
+EDGE = ["edge_dd_big995", "edge_dd_big996", "edge_dd_big997", "edge_dd_big1000",
+        "edge_dd_big996_9", "edge_dd_tiny969", "edge_dd_tiny1000", "edge_dd_tiny1040",
+        "edge_dd_subnormal", "edge_dd_zeros", "edge_dd_inf_nan", "edge_dd_overflow",
+        "edge_qd_zeros", "edge_qd_big997", "edge_qd_tiny"]
+
+
+def same_bits(x, y):
+    """Bitwise equal, except that any NaN matches any NaN (payloads are
+    platform-dependent: x86 and the GPU produce different default NaNs)."""
+    nx, ny = np.isnan(x), np.isnan(y)
+    if not np.array_equal(nx, ny):
+        return False
+    return np.array_equal(np.where(nx, 0, x.view(np.int64)), np.where(ny, 0, y.view(np.int64)))
+
+
+@pytest.mark.parametrize("name", EDGE)
+def test_edge_goldens(name):
+    """EFT-domain edges (eft.py:19-24): the oracle's Dekker TwoProd gives the
+    reference's results, NaN where the reference's split overflows."""
+    g = golden(name)
+    n_min = int(g["n_min"])
+    assert same_bits(oracle.matmul_simple(g["a"], g["b"]), g["c"])
+    assert same_bits(oracle.matmul_block(g["a"], g["b"], n_min), g["c"])
+    assert bool(g["raises"]) == (not np.isfinite(g["c"]).all())
+
+
+def test_edge_strassen_golden():
+    g = golden("edge_dd_strassen_big")
+    assert same_bits(oracle.strassen(g["a"], g["b"], 4, 2), g["c"])
+
+
+def test_edge_goldens_leave_the_dfma_domain():
+    """The edge set is not vacuous: several cases are outside the domain
+    where a DFMA TwoProd equals Dekker's (the GPU must take its Dekker path
+    there) -- checked with the host restatement of the domain test."""
+    from paper_1710_01839_b200 import domain
+    outside = [n for n in EDGE if domain.unsafe(golden(n)["a"], golden(n)["b"])]
+    assert {"edge_dd_big1000", "edge_dd_inf_nan", "edge_dd_subnormal",
+            "edge_dd_tiny1040", "edge_qd_big997"} <= set(outside)
+    assert "edge_dd_zeros" not in outside and "edge_qd_zeros" not in outside
