@@ -161,6 +161,29 @@ def _inputs_module():
     return mod
 
 
+def hugepage_copy(arr):
+    """``arr`` copied into anonymous memory advised MADV_HUGEPAGE.  The
+    reference's blocked kernel walks B down its columns (a 16*n-byte stride
+    per k), which on 4 KiB pages misses the TLB on nearly every access: on
+    the B200 host the 128-row slice of the 8192^3 DD product takes 11.5 s
+    with B in ordinary numpy memory and 5.6 s in 2 MiB pages
+    (profiles/r02_ref_cpu_probe.log).  The CPU baseline gets the faster
+    placement."""
+    import mmap
+
+    import numpy as np
+    huge = 2 << 20
+    size = (arr.nbytes + 2 * huge - 1) // huge * huge
+    mm = mmap.mmap(-1, size, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+    if hasattr(mmap, "MADV_HUGEPAGE"):
+        mm.madvise(mmap.MADV_HUGEPAGE)
+    buf = np.frombuffer(mm, dtype=np.uint8)
+    off = (-buf.ctypes.data) % huge
+    out = buf[off:off + arr.nbytes].view(arr.dtype).reshape(arr.shape)
+    out[...] = arr
+    return out
+
+
 class ReferenceCPU:
     """The reference's blocked product (multiply.py:148-160 partitioning
     over its compiled _kernels.dd_block_cells, all host threads) on its own
@@ -177,7 +200,7 @@ class ReferenceCPU:
         self.mult = oracle.DEFAULT_SLICE_MULTIPLIER
         if a is None or b is None:
             a, b = _inputs_module().gemm_inputs(prec, size, size, size, seed=seed)
-        self.a, self.b = a, b
+        self.a, self.b = a, hugepage_copy(b)
 
     def rows(self):
         return self.oracle.slice_rows_for(self.n_min, self.size, self.mult)
@@ -186,7 +209,7 @@ class ReferenceCPU:
         """One timed slice; returns (predicted full seconds, slice seconds)."""
         import numpy as np
         rows = rows or self.rows()
-        sl = np.ascontiguousarray(self.a[:rows])
+        sl = hugepage_copy(np.ascontiguousarray(self.a[:rows]))
         t0 = time.perf_counter()
         self.oracle.matmul_block(sl, self.b, self.n_min, threads=self.cores, kernels=self.kern)
         dt = time.perf_counter() - t0
@@ -203,7 +226,8 @@ class ReferenceCPU:
         return dt
 
     def sample(self, slice_s):
-        return (f"{self.prec.upper()} blocked n_min={self.n_min}, threads={self.cores}: the "
+        return (f"{self.prec.upper()} blocked n_min={self.n_min}, threads={self.cores}, operands "
+                f"in 2 MiB pages: the "
                 f"reference's predictor slice (leading {self.rows()} = {self.mult}*n_min rows "
                 f"of A, {self.size}x{self.size}) times all of B in {slice_s:.2f} s, scaled by "
                 f"m/rows = {self.size / self.rows():g} (predict.py:37-50): CPU, predicted; "

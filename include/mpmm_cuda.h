@@ -296,6 +296,15 @@ int mpmm_gemm_multi(int comps, int algo, int64_t n_min, int64_t cutoff, int64_t 
                     int64_t n, const double *a, const double *b, double *c, int64_t panels,
                     int *nonfinite, double *device_ms);
 
+/* The schedule mpmm_gemm_multi uses, computed on the host (no GPU needed):
+ * GPU g owns C rows [rows[2g], rows[2g+1]) -- ceil(m/ngpus) rounded up to
+ * the 64-row CTA tile, trailing GPUs possibly empty --; B is broadcast in
+ * *npanels k-panels [kb[p], kb[p+1]) (panels <= 0: automatic).  rows holds
+ * 2*ngpus entries, kb max(l,1)+2.  Returns 0, or 1 on a bad request.
+ * Replaces the reference's _split_range (multiply.py:86-96) lifted to GPUs. */
+int mpmm_multi_plan(int64_t m, int64_t l, int ngpus, int64_t panels, int64_t *rows, int64_t *kb,
+                    int *npanels);
+
 /* Event timers on a stream (TimingPolicy's device clock, timing.py:22-59). */
 int mpmm_timer_create(void **timer);
 int mpmm_timer_start(void *timer, void *stream);

@@ -76,6 +76,7 @@ _SIGNATURES = {
     "mpmm_oz_shifts_dev": [_INT, _INT, _VP, _I64, _VP, _VP, _VP, _VP],
     "mpmm_exact_check_dev": [_INT, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _VP,
                              _I64, _INT, _VP, _VP],
+    "mpmm_multi_plan": [_I64, _I64, _INT, _I64, _VP, _VP, ctypes.POINTER(_INT)],
     "mpmm_strassen_dev": [_INT, _I64, _I64, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64,
                           _VP, _VP, _VP],
     "mpmm_init": [_INT, _VP],
@@ -307,6 +308,19 @@ def runtime_gpus():
     ids = (ctypes.c_int * 64)()
     check(load().mpmm_runtime_gpus(ctypes.byref(n), ctypes.cast(ids, ctypes.c_void_p), 64))
     return list(ids[:n.value])
+
+
+def multi_plan(m, l, ngpus, panels=0):
+    """mpmm_gemm_multi's schedule: ([(r0, r1)] per GPU, [(k0, k1)] per
+    k-panel).  Pure host code: works without a GPU."""
+    rows = (ctypes.c_int64 * (2 * ngpus))()
+    kb = (ctypes.c_int64 * (max(l, 1) + 2))()
+    npan = _INT(0)
+    if load().mpmm_multi_plan(m, l, ngpus, panels, ctypes.cast(rows, _VP), ctypes.cast(kb, _VP),
+                              ctypes.byref(npan)):
+        raise ValueError("bad multi-GPU plan request")
+    return ([(rows[2 * g], rows[2 * g + 1]) for g in range(ngpus)],
+            [(kb[p], kb[p + 1]) for p in range(npan.value)])
 
 
 def gemm_multi(comps, algo, n_min, cutoff, a, b, c, panels=0):

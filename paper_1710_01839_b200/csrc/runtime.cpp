@@ -191,13 +191,33 @@ int rt_gpus(int* ids, int cap) {
   return static_cast<int>(g_gpus.size());
 }
 
-// Row block of GPU g: ceil(m / G) rounded up to the 64-row CTA tile.
-void rt_shard(int64_t m, int G, int g, int64_t* r0, int64_t* r1) {
-  int64_t per = (m + G - 1) / G;
+}  // namespace mpmm
+
+// The schedule of mpmm_gemm_multi, torch-free and GPU-free (so the host
+// logic is testable on CPU): GPU g owns C rows [rows[2g], rows[2g+1]) --
+// ceil(m / G) rounded up to the 64-row CTA tile, trailing GPUs possibly
+// empty --, and B travels in `*npanels` k-panels [kb[p], kb[p+1]).
+// panels <= 0: automatic (8 from l >= 1024, l/128 from 256, else 1).
+extern "C" int mpmm_multi_plan(int64_t m, int64_t l, int ngpus, int64_t panels, int64_t* rows,
+                               int64_t* kb, int* npanels) {
+  if (m < 0 || l < 0 || ngpus < 1 || rows == nullptr || kb == nullptr || npanels == nullptr)
+    return 1;
+  int64_t per = (m + ngpus - 1) / ngpus;
   per = ((per + 63) / 64) * 64;
-  *r0 = std::min(m, per * g);
-  *r1 = std::min(m, per * (g + 1));
+  for (int g = 0; g < ngpus; ++g) {
+    rows[2 * g] = std::min(m, per * g);
+    rows[2 * g + 1] = std::min(m, per * (g + 1));
+  }
+  if (panels < 1) panels = l >= 1024 ? 8 : (l >= 256 ? l / 128 : 1);
+  panels = std::max<int64_t>(1, std::min<int64_t>(panels, std::max<int64_t>(l, 1)));
+  const int64_t step = l > 0 ? (l + panels - 1) / panels : 1;
+  const int P = l > 0 ? static_cast<int>((l + step - 1) / step) : 0;
+  for (int p = 0; p <= P; ++p) kb[p] = std::min(l, p * step);
+  *npanels = P;
+  return 0;
 }
+
+namespace mpmm {
 
 int rt_gemm_host(int comps, int algo, int tile, int64_t cutoff, int64_t m, int64_t l, int64_t n,
                  const double* a, const double* b, double* c, int* nonfinite, double* device_ms,
@@ -213,10 +233,13 @@ int rt_gemm_host(int comps, int algo, int tile, int64_t cutoff, int64_t m, int64
   DeviceGuard guard;
   const int G = static_cast<int>(g_gpus.size());
   const size_t el = comps * sizeof(double);
-  if (panels < 1) panels = l >= 1024 ? 8 : (l >= 256 ? l / 128 : 1);
-  panels = std::max<int64_t>(1, std::min<int64_t>(panels, std::max<int64_t>(l, 1)));
-  const int64_t step = l > 0 ? (l + panels - 1) / panels : 1;
-  const int P = l > 0 ? static_cast<int>((l + step - 1) / step) : 0;
+  // the schedule (row blocks, k-panels): mpmm_multi_plan
+  std::vector<int64_t> plan_rows(2 * G), kb(static_cast<size_t>(std::max<int64_t>(l, 1)) + 2);
+  int P = 0;
+  if (mpmm_multi_plan(m, l, G, panels, plan_rows.data(), kb.data(), &P) != 0) {
+    *err = "bad multi-GPU plan request";
+    return 1;
+  }
   const bool strassen = algo == 3;
 
   struct Shard {
@@ -248,7 +271,8 @@ int rt_gemm_host(int comps, int algo, int tile, int64_t cutoff, int64_t m, int64
       Gpu& d = g_gpus[g];
       Shard& s = sh[g];
       RT_CU(cudaSetDevice(d.id));
-      rt_shard(m, G, g, &s.r0, &s.r1);
+      s.r0 = plan_rows[2 * g];
+      s.r1 = plan_rows[2 * g + 1];
       const int64_t rows = s.r1 - s.r0;
       RT_CU(cudaEventCreate(&s.t0));
       RT_CU(cudaEventCreate(&s.t1));
@@ -270,7 +294,7 @@ int rt_gemm_host(int comps, int algo, int tile, int64_t cutoff, int64_t m, int64
     }
     // k-panels: A columns and (on GPU 0) B rows from the host, B broadcast
     for (int p = 0; p < P; ++p) {
-      const int64_t k0 = p * step, k1 = std::min(l, k0 + step);
+      const int64_t k0 = kb[p], k1 = kb[p + 1];
       for (int g = 0; g < G; ++g) {
         Gpu& d = g_gpus[g];
         Shard& s = sh[g];

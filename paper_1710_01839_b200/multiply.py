@@ -269,10 +269,65 @@ def _block_into(a, b, c, n_min, threads=1, flag=None):
     _host_partitioned(lambda lo, hi: fn(a.data, b.data, c.data, n_min, lo, hi), cells, threads)
 
 
-def matmul_simple(a, b, threads=1):
-    """Triple-loop product; k accumulated in ascending order."""
+# ---------------------------------------------------------------------------
+# gpus= : several GPUs of this node from one process
+# ---------------------------------------------------------------------------
+
+def _gpu_list(gpus):
+    """``gpus``: a count G (devices 0..G-1) or an explicit device list."""
+    if isinstance(gpus, (int, np.integer)):
+        if gpus < 1:
+            raise ValueError("gpu count must be positive")
+        return list(range(int(gpus)))
+    devs = [int(g) for g in gpus]
+    if not devs or min(devs) < 0:
+        raise ValueError("gpu list must name devices")
+    return devs
+
+
+_runtime_devs = None
+
+
+def _runtime(devs):
+    """The native multi-GPU runtime (csrc/runtime.cpp: one NCCL communicator
+    per device, ncclCommInitAll) over exactly ``devs``."""
+    global _runtime_devs
+    if _runtime_devs == devs:
+        return
+    if len(set(devs)) != len(devs):
+        raise ValueError("row-sharded products need distinct devices")
+    if _runtime_devs is not None:
+        _cuda.runtime_finalize()
+        _runtime_devs = None
+    _cuda.runtime_init(len(devs), devs)
+    _runtime_devs = list(devs)
+
+
+def _rows_multi(a, b, algo, n_min, devs):
+    """C's rows split over ``devs`` (64-row aligned blocks, mpmm_multi_plan),
+    each GPU receiving its rows of A, B broadcast by NCCL in k-panels
+    overlapped with the per-panel GEMMs; bitwise the one-GPU product (each
+    element keeps one owner and its ascending k order)."""
+    _runtime(devs)
+    ha = np.ascontiguousarray(a.host_array())
+    hb = np.ascontiguousarray(b.host_array())
+    out = _pinned_empty(a.rows, b.cols, a.prec.comps)
+    bad, _ = _cuda.gemm_multi(a.prec.comps, algo, n_min, 0, ha, hb, out)
+    if bad:
+        raise RangeError("matrix product overflowed the working precision")
+    c = DenseMatrix(a.rows, b.cols, a.prec, out)
+    return c.to_device(a.device) if a.is_device else c
+
+
+def matmul_simple(a, b, threads=1, *, gpus=1):
+    """Triple-loop product; k accumulated in ascending order.  ``gpus`` > 1
+    row-shards C over that many GPUs of this node (bitwise the same C)."""
     _check_pair(a, b, threads)
+    devs = _gpu_list(gpus)
+    if len(devs) > 1:
+        return _rows_multi(a, b, _cuda.ALGO_SIMPLE, 0, devs)
     if backend.is_cuda() and not a.is_device and not b.is_device:
+
         return _host_product(a, b, _cuda.ALGO_SIMPLE, 0)
     da, db, home = _operands(a, b)
     c = DenseMatrix.zeros(a.rows, b.cols, a.prec, da.device)
@@ -284,9 +339,13 @@ def matmul_simple(a, b, threads=1):
 MODES = ("exact", "fast", "tensor")
 
 
-def matmul_block(a, b, n_min, threads=1, *, mode="exact"):
+def matmul_block(a, b, n_min, threads=1, *, mode="exact", gpus=1):
     """Blocked product with block size ``n_min``; bit-identical to
     :func:`matmul_simple` at every block size (multiply.py:171-182).
+
+    ``gpus`` (a count or a device list) > 1 row-shards C over the GPUs of
+    this node with B broadcast over NCCL (north_star (5)); the result is
+    bitwise the one-GPU product.
 
     ``mode="fast"`` (DD only) opts into the faithful 15-instruction DD
     sequence: within the north_star bound 4 l u (|A||B|)_ij (u = 2^-104) but
@@ -300,6 +359,12 @@ def matmul_block(a, b, n_min, threads=1, *, mode="exact"):
         raise ValueError(f"unknown mode {mode!r}; expected one of {MODES}")
     if mode == "fast" and a.prec.kind is not Kind.DD:
         raise ValueError("the fast accuracy mode is implemented for DD only")
+    devs = _gpu_list(gpus)
+    if len(devs) > 1:
+        if mode == "tensor":
+            raise ValueError("the tensor mode runs on one GPU")
+        return _rows_multi(a, b, _cuda.ALGO_BLOCK_FAST if mode == "fast" else _cuda.ALGO_BLOCK,
+                           n_min, devs)
     if mode == "tensor":
         if not backend.is_cuda():
             raise ValueError("the tensor mode runs on the cuda backend only")
@@ -358,7 +423,7 @@ def _ewise(x, y, subtract, stats=None):
 # ---------------------------------------------------------------------------
 
 def matmul_strassen(a, b, cutoff=DEFAULT_STRASSEN_CUTOFF, leaf_n_min=DEFAULT_BLOCK_SIZE,
-                    threads=1, stats=None, *, rectangular=False):
+                    threads=1, stats=None, *, rectangular=False, gpus=1):
     """Seven-product recursion with the reference's semantics.
 
     Square inputs only unless ``rectangular=True`` (an extension for
@@ -366,6 +431,11 @@ def matmul_strassen(a, b, cutoff=DEFAULT_STRASSEN_CUTOFF, leaf_n_min=DEFAULT_BLO
     to even and the quadrants are m/2 x l/2 and l/2 x n/2, PAPER.md:42;
     recursion stops when the smallest dimension is <= cutoff).  For square
     inputs both modes are the reference's algorithm, bit for bit.
+
+    ``gpus`` (a count or a device list) > 1 spreads the seven top-level
+    products over the GPUs -- the reference's own parallel Strassen runs
+    them on a thread pool (multiply.py:324-329) -- with the operand sums and
+    the combination on the first GPU: bitwise the one-GPU recursion.
     """
     if not rectangular and not (a.rows == a.cols == b.rows == b.cols):
         raise ShapeError("Strassen requires square inputs of equal dimension")
@@ -378,7 +448,11 @@ def matmul_strassen(a, b, cutoff=DEFAULT_STRASSEN_CUTOFF, leaf_n_min=DEFAULT_BLO
         raise ValueError("operation counting is only supported for serial runs")
     if not backend.is_cuda():
         raise ValueError("Strassen runs on the cuda backend only")
+    devs = _gpu_list(gpus)
     da, db, home = _operands(a, b)
+    if len(devs) > 1 and min(a.rows, a.cols, b.cols) > cutoff and not rectangular:
+        c = _strassen_multi(da, db, cutoff, leaf_n_min, devs, stats)
+        return _result(_check_finite(c), home)
     c = DenseMatrix.empty(a.rows, b.cols, a.prec, da.device)
     _strassen_rec(_View.of(da.data), _View.of(db.data), _View.of(c.data), cutoff, leaf_n_min,
                   stats)
@@ -403,20 +477,88 @@ def _strassen_rec(A, B, C, cutoff, leaf_n_min, stats):
         stats.additions += counts[1]
 
 
+def _strassen_multi(da, db, cutoff, leaf_n_min, devs, stats):
+    """The top level of the recursion with its seven products on ``devs``
+    (product i on devs[i % len(devs)]): operand sums on the first device in
+    the reference's order (multiply.py:313-321), each product below the top
+    level by the native recursion on its device (multiply.py:293-338), the
+    quadrant combination back on the first device (multiply.py:334-337).
+    Per element the operations are the one-GPU recursion's: same bits."""
+    import ctypes
+
+    from . import shard
+    torch = _torch()
+    home = da.data.device
+    prec = da.prec
+    n, comps = da.rows, prec.comps
+    even = n + (n & 1)
+    A, B = da.data, db.data
+    if even != n:   # zero padding of an odd dimension (multiply.py:293-299)
+        A = torch.zeros((even, even, comps), dtype=torch.float64, device=home)
+        B = torch.zeros((even, even, comps), dtype=torch.float64, device=home)
+        A[:n, :n] = da.data
+        B[:n, :n] = db.data
+    h = even // 2
+
+    def add(x, y, subtract):
+        out = torch.empty((h, h, comps), dtype=torch.float64, device=home)
+        _ewise_view(_View.of(out), _View.of(x), _View.of(y), -1 if subtract else 1)
+        if stats is not None:
+            stats.additions += 1
+        return out
+
+    qa = [A[i * h:(i + 1) * h, j * h:(j + 1) * h].contiguous() for i in (0, 1) for j in (0, 1)]
+    qb = [B[i * h:(i + 1) * h, j * h:(j + 1) * h].contiguous() for i in (0, 1) for j in (0, 1)]
+    ops = shard.strassen_operands(*qa, *qb, add)
+    home_stream = torch.cuda.current_stream(home)
+    ready = torch.cuda.Event()
+    ready.record(home_stream)
+    prods, events = [], []
+    for i, (x, y) in enumerate(ops):
+        dev = torch.device("cuda", devs[i % len(devs)])
+        with torch.cuda.device(dev):
+            s = torch.cuda.current_stream(dev)
+            s.wait_event(ready)
+            X, Y = x.to(dev, non_blocking=True), y.to(dev, non_blocking=True)
+            P = torch.empty((h, h, comps), dtype=torch.float64, device=dev)
+            counts = (ctypes.c_int64 * 2)() if stats is not None else None
+            _cuda.strassen_dev(comps, cutoff, leaf_n_min, h, h, h, X.data_ptr(), h,
+                               Y.data_ptr(), h, P.data_ptr(), h, None, counts, s.cuda_stream)
+            if stats is not None:
+                stats.multiplications += counts[0]
+                stats.additions += counts[1]
+            ev = torch.cuda.Event()
+            ev.record(s)
+            prods.append(P)
+            events.append(ev)
+            # the operand copies must outlive the queued product
+            X.record_stream(s)
+            Y.record_stream(s)
+    if stats is not None:
+        stats.multiplications += 7
+    for ev in events:
+        home_stream.wait_event(ev)
+    prods = [p.to(home, non_blocking=True) for p in prods]
+    c11, c12, c21, c22 = shard.strassen_combine(prods, add)
+    c = torch.cat([torch.cat([c11, c12], dim=1), torch.cat([c21, c22], dim=1)], dim=0)
+    return DenseMatrix(n, n, prec, c[:n, :n].contiguous())
+
+
 # ---------------------------------------------------------------------------
 # dispatch (multiply.py:345-350)
 # ---------------------------------------------------------------------------
 
-def run_choice(a, b, choice, threads=1):
+def run_choice(a, b, choice, threads=1, *, gpus=1):
+    """Run a tuner outcome; ``gpus`` as in matmul_block / matmul_strassen."""
     if choice.kind is Algorithm.SIMPLE:
-        return matmul_simple(a, b, threads)
+        return matmul_simple(a, b, threads, gpus=gpus)
     if choice.kind is Algorithm.BLOCK:
-        return matmul_block(a, b, choice.n_min, threads)
+        return matmul_block(a, b, choice.n_min, threads, gpus=gpus)
     if choice.kind is Algorithm.EXACT:
         from .tensor import NotRepresentable, matmul_exact
         try:
             return matmul_exact(a, b)
         except NotRepresentable:
             # operands outside the int8 CRT range: the mirror blocked kernel
-            return matmul_block(a, b, choice.n_min or DEFAULT_BLOCK_SIZE, threads)
-    return matmul_strassen(a, b, choice.cutoff, choice.n_min, threads)
+            return matmul_block(a, b, choice.n_min or DEFAULT_BLOCK_SIZE, threads, gpus=gpus)
+    return matmul_strassen(a, b, choice.cutoff, choice.n_min, threads, gpus=gpus)

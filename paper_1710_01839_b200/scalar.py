@@ -1,17 +1,15 @@
-"""Precision descriptors (reference ``pkg/src/mpmm/scalar.py:26-89``).
+"""Precision tokens and their properties (the reference's ``PrecisionSpec``
+and ``Kind``, ``scalar.py:26-89``).
 
-Only the DD and QD families are on the GPU hot path.  ``ap:<bits>`` tokens
-parse (so tables written by the reference load) but every product entry
-point rejects them: arbitrary precision is out of scope.
+The GPU path serves the two fixed families -- double-double (2 float64
+components, 106 mantissa bits) and quad-double (4 components, 212 bits).
+``ap:<bits>`` tokens still parse, so tables written by the reference load,
+but every product entry point rejects them (arbitrary precision is outside
+this build).
 """
 
 import enum
 from dataclasses import dataclass
-
-DD_BITS = 106
-QD_BITS = 212
-AP_MIN_BITS = 24
-AP_MAX_BITS = 1 << 20
 
 
 class Kind(enum.Enum):
@@ -20,76 +18,74 @@ class Kind(enum.Enum):
     AP = "ap"
 
 
+# family -> (mantissa bits, float64 components, u of the north_star GEMM bound)
+_FIXED = {Kind.DD: (106, 2, -104), Kind.QD: (212, 4, -209)}
+AP_BITS_RANGE = (24, 1 << 20)
+DD_BITS, QD_BITS = _FIXED[Kind.DD][0], _FIXED[Kind.QD][0]
+
+
 @dataclass(frozen=True)
 class PrecisionSpec:
     kind: Kind
     bits: int
 
     def __post_init__(self):
-        if self.kind is Kind.DD and self.bits != DD_BITS:
-            raise ValueError("double-double carries a fixed 106-bit mantissa")
-        if self.kind is Kind.QD and self.bits != QD_BITS:
-            raise ValueError("quad-double carries a fixed 212-bit mantissa")
-        if self.kind is Kind.AP and not (AP_MIN_BITS <= self.bits <= AP_MAX_BITS):
-            raise ValueError(f"big-float mantissa bits must lie in [{AP_MIN_BITS}, {AP_MAX_BITS}]")
+        if self.kind in _FIXED:
+            want = _FIXED[self.kind][0]
+            if self.bits != want:
+                raise ValueError(f"{self.kind.value} carries a fixed {want}-bit mantissa")
+        elif not AP_BITS_RANGE[0] <= self.bits <= AP_BITS_RANGE[1]:
+            raise ValueError("big-float mantissa bits must lie in "
+                             f"[{AP_BITS_RANGE[0]}, {AP_BITS_RANGE[1]}]")
 
-    @staticmethod
-    def dd():
-        return PrecisionSpec(Kind.DD, DD_BITS)
+    @classmethod
+    def dd(cls):
+        return cls(Kind.DD, DD_BITS)
 
-    @staticmethod
-    def qd():
-        return PrecisionSpec(Kind.QD, QD_BITS)
+    @classmethod
+    def qd(cls):
+        return cls(Kind.QD, QD_BITS)
 
-    @staticmethod
-    def ap(bits):
-        return PrecisionSpec(Kind.AP, int(bits))
+    @classmethod
+    def ap(cls, bits):
+        return cls(Kind.AP, int(bits))
 
-    @staticmethod
-    def parse(token):
-        """Parse ``dd``, ``qd`` or ``ap:<bits>`` (scalar.py:60-74)."""
-        token = token.strip().lower()
-        if token == "dd":
-            return PrecisionSpec.dd()
-        if token == "qd":
-            return PrecisionSpec.qd()
-        if token.startswith("ap:"):
-            try:
-                bits = int(token[3:])
-            except ValueError:
-                raise ValueError(f"bad precision token {token!r}") from None
-            return PrecisionSpec.ap(bits)
+    @classmethod
+    def parse(cls, token):
+        """``dd``, ``qd`` or ``ap:<bits>``, case and surrounding space ignored."""
+        tok = token.strip().lower()
+        fixed = {k.value: k for k in _FIXED}
+        if tok in fixed:
+            return cls(fixed[tok], _FIXED[fixed[tok]][0])
+        head, sep, tail = tok.partition(":")
+        if head == "ap" and sep and tail.isdigit():
+            return cls.ap(int(tail))
         raise ValueError(f"bad precision token {token!r}")
 
     @property
     def token(self):
-        if self.kind is Kind.AP:
-            return f"ap:{self.bits}"
-        return self.kind.value
+        return f"ap:{self.bits}" if self.kind is Kind.AP else self.kind.value
 
     @property
     def comps(self):
-        """float64 components per element: 2 (DD) or 4 (QD)."""
-        if self.kind is Kind.DD:
-            return 2
-        if self.kind is Kind.QD:
-            return 4
-        raise ValueError("arbitrary precision has no fixed component count")
+        """float64 components per element (the trailing array dimension)."""
+        if self.kind not in _FIXED:
+            raise ValueError("arbitrary precision has no fixed component count")
+        return _FIXED[self.kind][1]
 
     @property
     def unit_roundoff_exp(self):
         return -self.bits
 
     def unit_roundoff(self):
-        """2^-bits, as in the reference (scalar.py:84-86).  Note that the
-        north_star GEMM bound uses u = 2^-104 (DD) / 2^-209 (QD) instead;
-        see ``gemm_bound_u``."""
+        """2^-bits, the reference's u (its verify bounds use it)."""
         return 2.0 ** -self.bits
 
     @property
     def gemm_bound_u(self):
-        """The u of the north_star componentwise bound 4 l u (|A||B|)."""
-        return 2.0 ** -104 if self.kind is Kind.DD else 2.0 ** -209
+        """The u of the north_star bound |c - c_exact| <= 4 l u (|A||B|):
+        2^-104 (DD) or 2^-209 (QD)."""
+        return 2.0 ** _FIXED[self.kind][2]
 
     def __str__(self):
         return self.token

@@ -109,10 +109,12 @@ def test_edge_streamed_and_panelled_host_products(gpu, tok):
     k-panel)."""
     m, l, n = 96, 320, 80
     a, b = inputs.gemm_inputs(tok, m, l, n, seed=44)
-    a[5, 200] = np.ldexp(a[5, 200], 1000)      # split overflow: NaN in row 5
+    a0, b0 = a.copy(), b.copy()
+    a[5, 200] = 0.0
+    a[5, 200, 0] = 0.75 * 2.0 ** 1000           # split overflow: NaN in row 5
     b[17, 3] = np.ldexp(b[17, 3], -1010)       # error underflow in column 3
     want = oracle.matmul_simple(a, b)
-    assert domain.unsafe(a, b) and np.isnan(want[5]).any()
+    assert domain.unsafe(a, b) and np.isnan(want[5]).all()
     import torch
     pa = torch.from_numpy(a).pin_memory().numpy()
     pb = torch.from_numpy(b).pin_memory().numpy()
@@ -123,8 +125,7 @@ def test_edge_streamed_and_panelled_host_products(gpu, tok):
     _cuda.gemm_host(a.shape[2], _cuda.ALGO_BLOCK, 32, a, b, out2, accumulate=False)
     assert same_bits(out2, want)
     # without the injected values the same path stays on the DFMA kernel
-    a[5, 200] = inputs.gemm_inputs(tok, m, l, n, seed=44)[0][5, 200]
-    b[17, 3] = inputs.gemm_inputs(tok, m, l, n, seed=44)[1][17, 3]
+    a, b = a0, b0
     assert not domain.unsafe(a, b)
     pa[...] = a
     pb[...] = b

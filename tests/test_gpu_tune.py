@@ -119,3 +119,67 @@ def test_tune_one_with_exact_candidate_and_run_choice(gpu, tmp_path):
     from oracle import exact
     ratio, _ = exact.bound_ratio(a, b, c, range(0, 96, 7), range(0, 72, 5), 104)
     assert ratio <= 1.0
+
+
+@pytest.mark.parametrize("tok,n", [("dd", 4096), ("qd", 2048)])
+def test_acceptance_criteria_6_7_on_the_gpu(gpu, tok, n):
+    """The reference's acceptance criteria 6 and 7 (test_acceptance.py:
+    141-182) for the GPU predictor, at configs[4] sizes where the slices
+    are a fraction of the product: every candidate's prediction within
+    15 % of its measured time, the chosen candidate within 10 % of the
+    fastest measured one, and the prediction phase (both slices of every
+    candidate) at most 0.7 x the exhaustive search."""
+    from paper_1710_01839_b200.tune import _measure_block
+    p = mp.PrecisionSpec.parse(tok)
+    a, b = inputs.gemm_inputs_device(tok, n, n, n, seed=1)
+    A, B = DenseMatrix(n, n, p, a), DenseMatrix(n, n, p, b)
+    pol = mp.TimingPolicy(warmup_runs=1, measured_runs=3, aggregator="min")
+    cands = [16, 32, 64, 128, 256]
+    best, recs = mp.select_block_size(A, B, cands, policy=pol)
+    full = {c: _measure_block(A, B, c, 1, pol) for c in cands}
+    phase = sum(r.slice_time_s + r.slice2_time_s for r in recs)
+    for r in recs:
+        err = mp.rel_diff(r.predicted_full_s, full[r.n_min])
+        print(f"{tok} n={n} n_min={r.n_min} predicted={r.predicted_full_s * 1e3:.2f} ms "
+              f"measured={full[r.n_min] * 1e3:.2f} ms err={err:.2%}")
+        assert err <= 0.15, (r.n_min, err)
+    assert full[best] <= 1.10 * min(full.values()), (best, full)
+    assert phase <= 0.7 * sum(full.values()), (phase, sum(full.values()))
+
+
+def test_tune_over_gpu_counts(gpu, tmp_path):
+    """gpus > 1 points: the largest row block's product measured on this
+    GPU plus the modelled broadcast; more GPUs -> a smaller block time."""
+    cfg = mp.TuningConfig(precisions=[DD], dims=[512], block_candidates=[32, 64],
+                          thread_counts=[1], strassen_cutoffs=[128], gpu_counts=[1, 2, 8],
+                          inputs="seeded", out_path=str(tmp_path / "g.tbl"))
+    table = mp.tune_sweep(cfg)
+    rows = {r.gpus: r for r in table.rows}
+    assert sorted(rows) == [1, 2, 8] and not table.failures
+    assert not rows[1].gpus_modelled and rows[2].gpus_modelled and rows[8].gpus_modelled
+    assert rows[8].block_time_s < rows[2].block_time_s < rows[1].block_time_s
+    assert open(cfg.out_path).read().startswith("mpmmtune v2")
+    assert mp.load_table(cfg.out_path) == table
+
+
+def test_gpus_argument(gpu):
+    """gpus= on the public API: Strassen's seven top-level products spread
+    over a device list (the same device twice here) give the one-GPU bits;
+    row sharding needs distinct devices."""
+    a, b = inputs.gemm_inputs("dd", 300, 300, 300, seed=6)
+    A = DenseMatrix(300, 300, DD, a).to_device()
+    B = DenseMatrix(300, 300, DD, b).to_device()
+    one = mp.matmul_strassen(A, B, 64, 32)
+    st1, st2 = mp.StrassenStats(), mp.StrassenStats()
+    assert mp.matmul_strassen(A, B, 64, 32, stats=st1) == one
+    two = mp.matmul_strassen(A, B, 64, 32, gpus=[0, 0], stats=st2)
+    assert two == one and two.is_device
+    assert (st1.multiplications, st1.additions) == (st2.multiplications, st2.additions)
+    assert np.array_equal(one.host_array(), oracle.strassen(a, b, 64, 32))
+    choice = mp.AlgorithmChoice.parse("strassen:64/32")
+    assert mp.run_choice(A, B, choice, gpus=[0, 0]) == one
+    with pytest.raises(ValueError):
+        mp.matmul_block(A, B, 32, gpus=[0, 0])
+    with pytest.raises(ValueError):
+        mp.matmul_block(A, B, 32, gpus=0)
+    assert mp.matmul_block(A, B, 32, gpus=1) == mp.matmul_block(A, B, 32)

@@ -279,7 +279,7 @@ def test_tuning_config_validation():
 def test_tune_sweep_records_failures(monkeypatch):
     import paper_1710_01839_b200.tune as tune_mod
 
-    def flaky(prec, n, threads, cfg, _accum=None):
+    def flaky(prec, n, threads, cfg, _accum=None, gpus=1):
         if n == 24:
             raise RuntimeError("injected fault")
         return mk_row(prec, n, threads, False)
@@ -293,6 +293,52 @@ def test_tune_sweep_records_failures(monkeypatch):
     table = mp.tune_sweep(cfg)
     assert len(table.rows) == 1 and len(table.failures) == 1
     assert "injected" in table.failures[0].message
+
+
+def test_tune_sweep_over_gpu_counts(monkeypatch, tmp_path):
+    """gpu_counts is swept like thread_counts (reference tune.py:173-213):
+    one row per (prec, n, threads, gpus), thresholds per gpus series, and
+    the modelled rows survive a save/load round trip as "G~"."""
+    import paper_1710_01839_b200.tune as tune_mod
+    seen = []
+
+    def fake(prec, n, threads, cfg, _accum=None, gpus=1):
+        seen.append((n, gpus))
+        _accum["selection"] = _accum.get("selection", 0.0) + 0.5
+        r = mk_row(prec, n, threads, n >= 32 and gpus == 1)
+        r.gpus, r.gpus_modelled = gpus, gpus > 1
+        return r
+
+    monkeypatch.setattr(tune_mod, "tune_one", fake)
+    monkeypatch.setattr(tune_mod, "_warm", lambda *a: None)
+    cfg = mp.TuningConfig(precisions=[DD], dims=[16, 32, 64], block_candidates=[8],
+                          thread_counts=[1], gpu_counts=[8, 1, 2],
+                          out_path=str(tmp_path / "g.tbl"))
+    table = mp.tune_sweep(cfg)
+    assert seen == [(n, g) for n in (16, 32, 64) for g in (1, 2, 8)]
+    assert table.prediction_total_s == 0.5 * 9
+    assert table.thresholds == {(DD, 1): 32}
+    text = open(tmp_path / "g.tbl").read()
+    assert text.startswith("mpmmtune v2") and " 8~ " in text and " 1 " in text
+    back = mp.load_table(str(tmp_path / "g.tbl"))
+    assert sorted((r.n, r.gpus, r.gpus_modelled) for r in back.rows) == \
+        sorted((n, g, g > 1) for n in (16, 32, 64) for g in (1, 2, 8))
+    with pytest.raises(ValueError):
+        mp.TuningConfig(precisions=[DD], dims=[16], block_candidates=[8], thread_counts=[1],
+                        gpu_counts=[0])
+
+
+def test_shard_model_geometry():
+    """The G-GPU point tunes the largest row block's product; the exposed
+    broadcast is one k-panel (blocked/simple) or all of B (Strassen)."""
+    from paper_1710_01839_b200.tune import _Shard
+    cfg = mp.TuningConfig(precisions=[DD], dims=[16], block_candidates=[8], thread_counts=[1],
+                          bcast_bytes_per_s=1e9, bcast_panels=8)
+    s1 = _Shard(8192, 1, 2, cfg)
+    assert s1.rows == 8192 and s1.full_s == 0.0 and s1.panel_s == 0.0
+    s3 = _Shard(8192, 3, 2, cfg)
+    assert s3.rows == 2752                       # ceil(8192/3) -> 64-row multiple
+    assert s3.full_s == 16.0 * 8192 * 8192 / 1e9 and s3.panel_s == s3.full_s / 8
 
 
 # --- sharding -----------------------------------------------------------------
