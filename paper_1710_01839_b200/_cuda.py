@@ -310,6 +310,11 @@ def runtime_gpus():
     return list(ids[:n.value])
 
 
+def exact_release():
+    """mpmm_exact_release: drop the exact mode's cached plans and buffers."""
+    check(load().mpmm_exact_release())
+
+
 def multi_plan(m, l, ngpus, panels=0):
     """mpmm_gemm_multi's schedule: ([(r0, r1)] per GPU, [(k0, k1)] per
     k-panel).  Pure host code: works without a GPU."""

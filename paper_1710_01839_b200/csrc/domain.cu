@@ -235,11 +235,12 @@ cudaError_t gemm_checked(int comps, GemmArgs g, const int** words_out) {
     g.gate.words = nullptr;
     return comps == 2 ? dd_gemm_launch(g) : qd_gemm_launch(g);
   }
-  if (g.probs != nullptr && g.gate.words != nullptr) {
+  if ((g.probs != nullptr || g.sprobs != nullptr) && g.gate.words != nullptr) {
     // batched problems the caller has scanned (e.g. Strassen leaves, whose
     // operands derive from one scanned pair; margins set by the caller)
     return gemm_gated(comps, g, g.gate.words);
   }
+  if (g.sprobs != nullptr) return cudaErrorInvalidValue;   // the caller scans
   const int* words = nullptr;
   cudaError_t e = g.probs != nullptr
       ? domain_scan_batched(comps, g.probs, g.batch, g.m, g.l, g.n, &words, g.stream)

@@ -222,11 +222,22 @@ struct Entry {
   const void* last[3] = {nullptr, nullptr, nullptr};
   cudaGraphExec_t graph = nullptr;         // replay for ptrs == graph_ptrs
   const void* graph_ptrs[3] = {nullptr, nullptr, nullptr};
+  // held for a whole exact_gemm call: host threads sharing a stream (the
+  // legacy default stream) and shape must not interleave on one entry
+  std::mutex mu;
+  int users = 0;              // calls holding a pointer to it (guarded by g_mu)
+  uint64_t last_use = 0;      // g_clock at the last call (guarded by g_mu)
 };
 
-using Key = std::tuple<int, uintptr_t, int, int64_t, int64_t, int64_t>;
+// (device, stream, comps, m, l, n, lda, ldb, ldc): the strides are part of
+// the key, so a captured graph is never replayed with other strides
+using Key = std::tuple<int, uintptr_t, int, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t>;
 std::mutex g_mu;
 std::map<Key, std::unique_ptr<Entry>> g_entries;
+uint64_t g_clock = 0;
+// entries kept at once (each may hold up to kKeepBytes of workspace and a
+// graph); beyond it the least recently used idle entry is dropped
+constexpr size_t kMaxEntries = 6;
 
 size_t workspace_bytes(const Plan& pl, int comps, int64_t m, int64_t l, int64_t n) {
   const Pads P = pads_for(m, l, n);
@@ -332,6 +343,42 @@ cudaError_t enqueue_product(const Plan& pl, int comps, int64_t m, int64_t l, int
   return oz_combine_launch(comps, jobs, pl.njobs, (int)m, (int)n, C, ws.aux, s, P.tc, pl.win);
 }
 
+// Free an entry's graph, workspace, pinned buffers and capture stream.
+void drop_entry(Entry& en, cudaStream_t s) {
+  if (en.graph) cudaGraphExecDestroy(en.graph);
+  en.graph = nullptr;
+  free_workspace(en.ws, s);
+  if (en.aux_host) cudaFreeHost(en.aux_host);
+  if (en.el_host) cudaFreeHost(en.el_host);
+  if (en.side) cudaStreamDestroy(en.side);
+  en.aux_host = en.el_host = nullptr;
+  en.side = nullptr;
+}
+
+// With g_mu held: drop least-recently-used idle entries beyond kMaxEntries.
+void evict_locked() {
+  while (g_entries.size() > kMaxEntries) {
+    auto victim = g_entries.end();
+    for (auto it = g_entries.begin(); it != g_entries.end(); ++it)
+      if (it->second->users == 0 &&
+          (victim == g_entries.end() || it->second->last_use < victim->second->last_use))
+        victim = it;
+    if (victim == g_entries.end()) return;   // every entry is in use
+    drop_entry(*victim->second, reinterpret_cast<cudaStream_t>(std::get<1>(victim->first)));
+    g_entries.erase(victim);
+  }
+}
+
+// A call's claim on its entry: users++ under g_mu on entry, users-- on exit.
+struct EntryUse {
+  Entry* en;
+  explicit EntryUse(Entry* e) : en(e) {}
+  ~EntryUse() {
+    std::lock_guard<std::mutex> lock(g_mu);
+    --en->users;
+  }
+};
+
 }  // namespace
 
 // 0 ok; 1 bad argument; 2 CUDA error; 4 not representable; 5 non-finite
@@ -369,7 +416,7 @@ int exact_gemm(int comps, int64_t m, int64_t l, int64_t n, const double* A, int6
     return 1;
   }
   // table uploads (synchronous) must not happen inside a capture: warm them
-  const Key key{dev, reinterpret_cast<uintptr_t>(s), comps, m, l, n};
+  const Key key{dev, reinterpret_cast<uintptr_t>(s), comps, m, l, n, lda, ldb, ldc};
   std::unique_lock<std::mutex> lock(g_mu);
   auto& slot = g_entries[key];
   if (!slot) {
@@ -380,12 +427,19 @@ int exact_gemm(int comps, int64_t m, int64_t l, int64_t n, const double* A, int6
         (e = cudaMallocHost(reinterpret_cast<void**>(&ne->el_host), elb)) != cudaSuccess ||
         (e = cudaStreamCreateWithFlags(&ne->side, cudaStreamNonBlocking)) != cudaSuccess) {
       *err = cudaGetErrorString(e);
+      drop_entry(*ne, s);
+      g_entries.erase(key);
       return 2;
     }
     slot = std::move(ne);
   }
   Entry& en = *slot;
+  ++en.users;
+  en.last_use = ++g_clock;
+  evict_locked();
   lock.unlock();
+  EntryUse use(&en);
+  std::lock_guard<std::mutex> entry_lock(en.mu);
   auto cuda_err = [&](cudaError_t ce) {
     if (err->empty()) *err = cudaGetErrorString(ce);
     return 2;
@@ -565,17 +619,17 @@ int exact_gemm(int comps, int64_t m, int64_t l, int64_t n, const double* A, int6
 }
 
 // Drop every cached plan, workspace and graph (device memory back to the pool).
+// Entries in use by another thread are left alone.
 void exact_release() {
   std::lock_guard<std::mutex> lock(g_mu);
-  for (auto& kv : g_entries) {
-    Entry& en = *kv.second;
-    if (en.graph) cudaGraphExecDestroy(en.graph);
-    free_workspace(en.ws, reinterpret_cast<cudaStream_t>(std::get<1>(kv.first)));
-    if (en.aux_host) cudaFreeHost(en.aux_host);
-    if (en.el_host) cudaFreeHost(en.el_host);
-    if (en.side) cudaStreamDestroy(en.side);
+  for (auto it = g_entries.begin(); it != g_entries.end();) {
+    if (it->second->users != 0) {
+      ++it;
+      continue;
+    }
+    drop_entry(*it->second, reinterpret_cast<cudaStream_t>(std::get<1>(it->first)));
+    it = g_entries.erase(it);
   }
-  g_entries.clear();
 }
 
 }  // namespace mpmm

@@ -253,6 +253,214 @@ __device__ __forceinline__ void gemm_tile(const Prob& pr, int m, int n, int l, i
     }
 }
 
+// ---------------------------------------------------------------------------
+// Strassen leaves with their operand sums folded into the tile loads
+// (multiply.py:313-321): the left operand is X + sa*Y (sa = +-1; 0: X alone)
+// and the right one Z + sb*W, each sum the reference's ewise add/sub
+// (_kernels.pyx:189-230 DD, :407-452 QD) evaluated per staged element --
+// the same bits as the materialised sum, without writing and re-reading it.
+// Every thread stages whole elements (all V vectors) of X and Y by
+// cp.async, waits for its own copies and forms the sums in place before the
+// tile barrier, so the fold adds no barrier.
+// ---------------------------------------------------------------------------
+
+struct SumProb {
+  const double2* A;
+  const double2* A2;
+  const double2* B;
+  const double2* B2;
+  double2* C;
+  int64_t lda, ldb, ldc;
+  int sa, sb;
+};
+
+__device__ __forceinline__ SumProb get_sum_prob(const SumProblem& g) {
+  return SumProb{reinterpret_cast<const double2*>(g.A), reinterpret_cast<const double2*>(g.A2),
+                 reinterpret_cast<const double2*>(g.B), reinterpret_cast<const double2*>(g.B2),
+                 reinterpret_cast<double2*>(g.C), g.lda, g.ldb, g.ldc, g.sa, g.sb};
+}
+
+// x <- x + s*y on one staged element (s = +1 / -1): the reference ewise op
+template <int V>
+__device__ __forceinline__ void fold_sum(double2* x, const double2* y, int s) {
+  if constexpr (V == 1) {
+    const double yh = s < 0 ? -y[0].x : y[0].x, yl = s < 0 ? -y[0].y : y[0].y;
+    double h, lo;
+    dd_add(x[0].x, x[0].y, yh, yl, h, lo);
+    x[0] = make_double2(h, lo);
+  } else {
+    const double a[4] = {x[0].x, x[0].y, x[1].x, x[1].y};
+    double b[4] = {y[0].x, y[0].y, y[1].x, y[1].y};
+    if (s < 0)
+      for (int q = 0; q < 4; ++q) b[q] = -b[q];
+    double r[4];
+    qd_add(a, b, r);
+    x[0] = make_double2(r[0], r[1]);
+    x[1] = make_double2(r[2], r[3]);
+  }
+}
+
+template <class Ops, int BM, int BN, int BK>
+struct SumSmem {
+  using T = TileSmem<Ops, BM, BN, BK>;
+  // As, Bs double-buffered, then the Y / W staging of both stages
+  static constexpr int TOTAL = 2 * T::TOTAL;
+};
+
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int NT>
+__device__ __forceinline__ void gemm_tile_sum(const SumProb& pr, int m, int n, int l, int m0,
+                                              int n0, double2* smem, bool& bad) {
+  constexpr int V = Ops::V;
+  constexpr int NTX = BN / TN, NTY = BM / TM;
+  static_assert(NTX * NTY == NT, "thread tile does not cover the CTA tile");
+  using S = TileSmem<Ops, BM, BN, BK>;
+  double2* const Y0 = smem + S::TOTAL;   // staging of the second summands
+  auto As = [&](double2* base, int st, int r, int k) -> double2* {
+    return base + st * S::A_STAGE + (r * (BK + 1) + k) * V;
+  };
+  auto Bs = [&](double2* base, int st, int k, int c) -> double2* {
+    return base + 2 * S::A_STAGE + st * S::B_STAGE + (k * BN + c) * V;
+  };
+  const int tid = threadIdx.x;
+  const int tx = tid % NTX, ty = tid / NTX;
+
+  double acc[TM][TN][Ops::NACC];
+#pragma unroll
+  for (int r = 0; r < TM; ++r)
+#pragma unroll
+    for (int c = 0; c < TN; ++c)
+#pragma unroll
+      for (int q = 0; q < Ops::NACC; ++q) acc[r][c][q] = 0.0;
+
+  const int ktiles = (l + BK - 1) / BK;
+  auto load = [&](int kt, int st) {
+    const int k0 = kt * BK;
+    for (int el = tid; el < BM * BK; el += NT) {
+      const int row = el / BK, col = el % BK;
+      const int gi = m0 + row, gk = k0 + col;
+      const bool ok = gi < m && gk < l;
+      const int64_t off = ((int64_t)gi * pr.lda + gk) * V;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        cp_async16(As(smem, st, row, col) + v, ok ? pr.A + off + v : pr.A, ok);
+        if (pr.sa) cp_async16(As(Y0, st, row, col) + v, ok ? pr.A2 + off + v : pr.A2, ok);
+      }
+    }
+    for (int el = tid; el < BK * BN; el += NT) {
+      const int row = el / BN, col = el % BN;
+      const int gk = k0 + row, gj = n0 + col;
+      const bool ok = gk < l && gj < n;
+      const int64_t off = ((int64_t)gk * pr.ldb + gj) * V;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        cp_async16(Bs(smem, st, row, col) + v, ok ? pr.B + off + v : pr.B, ok);
+        if (pr.sb) cp_async16(Bs(Y0, st, row, col) + v, ok ? pr.B2 + off + v : pr.B2, ok);
+      }
+    }
+  };
+  // the sums of this thread's own staged elements (visible to it after
+  // its cp.async group completed; the tile barrier publishes them)
+  auto fold = [&](int st) {
+    if (pr.sa)
+      for (int el = tid; el < BM * BK; el += NT) {
+        const int row = el / BK, col = el % BK;
+        fold_sum<V>(As(smem, st, row, col), As(Y0, st, row, col), pr.sa);
+      }
+    if (pr.sb)
+      for (int el = tid; el < BK * BN; el += NT) {
+        const int row = el / BN, col = el % BN;
+        fold_sum<V>(Bs(smem, st, row, col), Bs(Y0, st, row, col), pr.sb);
+      }
+  };
+
+  if (ktiles > 0) {
+    load(0, 0);
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int st = kt & 1;
+    if (kt + 1 < ktiles) {
+      load(kt + 1, st ^ 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    fold(st);
+    __syncthreads();
+    const int kcount = min(BK, l - kt * BK);
+    auto step = [&](int kk) {
+      double2 a[TM][V], b[TN][V];
+#pragma unroll
+      for (int r = 0; r < TM; ++r)
+#pragma unroll
+        for (int v = 0; v < V; ++v) a[r][v] = As(smem, st, ty + r * NTY, kk)[v];
+#pragma unroll
+      for (int c = 0; c < TN; ++c)
+#pragma unroll
+        for (int v = 0; v < V; ++v) b[c][v] = Bs(smem, st, kk, tx + c * NTX)[v];
+#pragma unroll
+      for (int r = 0; r < TM; ++r)
+#pragma unroll
+        for (int c = 0; c < TN; ++c) Ops::madd(acc[r][c], a[r], b[c]);
+    };
+    if (kcount == BK) {
+#pragma unroll 2
+      for (int kk = 0; kk < BK; ++kk) step(kk);
+    } else {
+      for (int kk = 0; kk < kcount; ++kk) step(kk);
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int r = 0; r < TM; ++r)
+#pragma unroll
+    for (int c = 0; c < TN; ++c) {
+      int i = m0 + ty + r * NTY, j = n0 + tx + c * NTX;
+      if (i < m && j < n) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          pr.C[((int64_t)i * pr.ldc + j) * V + v] =
+              make_double2(acc[r][c][2 * v], acc[r][c][2 * v + 1]);
+          bad |= !finite2(acc[r][c][2 * v], acc[r][c][2 * v + 1]);
+        }
+      }
+    }
+}
+
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
+gemm_tiled_sum(const SumProblem* __restrict__ probs, int m, int n, int l,
+               int* __restrict__ nonfinite, const DomainGate gate) {
+  constexpr int NT = (BM / TM) * (BN / TN);
+  extern __shared__ __align__(16) double2 dsmem[];
+  if (gate_skip(gate)) return;
+  const int tiles_n = (n + BN - 1) / BN, tiles_m = (m + BM - 1) / BM;
+  const int per = tiles_m * tiles_n;
+  const int p = blockIdx.x / per, t = blockIdx.x % per;
+  const SumProb pr = get_sum_prob(probs[p]);
+  bool bad = false;
+  gemm_tile_sum<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, (t / tiles_n) * BM, (t % tiles_n) * BN,
+                                            dsmem, bad);
+  if (nonfinite != nullptr && bad) atomicOr(nonfinite, 1);
+}
+
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB>
+cudaError_t launch_tiled_sum(const GemmArgs& g) {
+  auto kern = gemm_tiled_sum<Ops, BM, BN, BK, TM, TN, MINB>;
+  constexpr size_t bytes = SumSmem<Ops, BM, BN, BK>::TOTAL * sizeof(double2);
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (attr != cudaSuccess) return attr;
+  int64_t tiles = (int64_t)((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN) * g.batch;
+  if (tiles == 0) return cudaSuccess;
+  if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
+  kern<<<(unsigned)tiles, (BM / TM) * (BN / TN), bytes, g.stream>>>(g.sprobs, g.m, g.n, g.l,
+                                                                    g.nonfinite, g.gate);
+  return cudaGetLastError();
+}
+
 // Plain tiled kernel: one CTA per (problem, tile).  STREAM: the operands
 // arrive while it runs (wait_k_panel); a separate instantiation, so the
 // resident-operand kernel keeps its code unchanged.

@@ -56,6 +56,7 @@ static cudaError_t dd32_geometry(Geometry* geo) { return dd_geometry<Ops, MPMM_D
 
 cudaError_t dd_gemm_launch(const GemmArgs& g) {
   if (g.m <= 0 || g.n <= 0 || g.batch <= 0) return cudaSuccess;
+  if (g.sprobs != nullptr) return launch_tiled_sum<DDOps, 32, 32, 16, 2, 2, 2>(g);
   if (g.algo == ALGO_SIMPLE) return launch_simple<DDOps>(g);
   if (g.algo == ALGO_BLOCK_FAST) return dd_blocked<DDFastOps>(g);
   return dd_blocked<DDOps>(g);
@@ -64,6 +65,7 @@ cudaError_t dd_gemm_launch(const GemmArgs& g) {
 cudaError_t dd_dekker_launch(const GemmArgs& g) {
   if (g.m <= 0 || g.n <= 0 || g.batch <= 0) return cudaSuccess;
   if (g.kready != nullptr) return cudaErrorNotSupported;
+  if (g.sprobs != nullptr) return launch_tiled_sum<DDDekkerOps, 32, 32, 16, 2, 2, 2>(g);
   return launch_tiled<DDDekkerOps, 32, 32, 16, 2, 2, 2>(g);
 }
 

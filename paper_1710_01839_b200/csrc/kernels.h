@@ -26,6 +26,19 @@ struct GemmProblem {
   int64_t lda, ldb, ldc;
 };
 
+// One Strassen leaf with its operand sums folded into the tile loads
+// (gemm.cuh gemm_tiled_sum): (A + sa*A2) * (B + sb*B2), sa/sb in {0, +1, -1}
+// (0: the operand alone); A2 shares A's leading dimension, B2 B's.
+struct SumProblem {
+  const double* A;
+  const double* A2;
+  const double* B;
+  const double* B2;
+  double* C;
+  int64_t lda, ldb, ldc;
+  int32_t sa, sb;
+};
+
 struct GemmArgs {
   int algo;          // ALGO_SIMPLE or ALGO_BLOCK
   int tile;          // Tile (ALGO_BLOCK)
@@ -49,6 +62,9 @@ struct GemmArgs {
   // EFT-domain gate (domain.cuh): with gate.words set, the launch runs only
   // on the side of the domain test gate.want_unsafe selects.
   DomainGate gate{};
+  // Strassen leaves with folded operand sums: `batch` SumProblems in device
+  // memory (ALGO_BLOCK only; one tile configuration per precision).
+  const SumProblem* sprobs = nullptr;
 };
 
 // The DFMA mirror kernels (ALGO_SIMPLE / ALGO_BLOCK / ALGO_BLOCK_FAST).

@@ -40,6 +40,10 @@ struct View {
 
 struct Node {
   View A, B, C;     // operands and the (possibly padded) product target
+  // a leaf whose operand sums are folded into its tile loads:
+  // left = A + sa*A2, right = B + sb*B2 (sa, sb in {0, +1, -1})
+  View A2{}, B2{};
+  int sa = 0, sb = 0;
   View Cout;        // where the product finally goes (== C unless padded)
   bool crop = false;
   View P[7];
@@ -118,6 +122,30 @@ class Driver {
     return e;
   }
 
+  // Leaves with folded operand sums: one launch per <= 65535 problems.
+  cudaError_t leaves_fused(const std::vector<Node>& nodes, int64_t m, int64_t l, int64_t n) {
+    if (nodes.empty() || m == 0 || n == 0) return cudaSuccess;
+    std::vector<SumProblem> probs;
+    probs.reserve(nodes.size());
+    for (const Node& nd : nodes)
+      probs.push_back(SumProblem{nd.A.p, nd.sa ? nd.A2.p : nullptr, nd.B.p,
+                                 nd.sb ? nd.B2.p : nullptr, nd.C.p, nd.A.ld, nd.B.ld, nd.C.ld,
+                                 nd.sa, nd.sb});
+    void* d = nullptr;
+    cudaError_t e = upload(probs.data(), probs.size() * sizeof(SumProblem), &d);
+    for (size_t q = 0; e == cudaSuccess && q < probs.size(); q += kMaxBatch) {
+      GemmArgs g{ALGO_BLOCK, tile_, (int)m, (int)n, (int)l, nullptr, 0, nullptr, 0, nullptr, 0,
+                 0, nullptr, s_};
+      g.batch = static_cast<int>(std::min<size_t>(kMaxBatch, probs.size() - q));
+      g.sprobs = static_cast<const SumProblem*>(d) + q;
+      g.gate.words = words_;
+      g.gate.margin_lo = depth_ > 0 ? 52 : 0;
+      g.gate.margin_hi = depth_ > 0 ? depth_ + 1 : 0;
+      e = gemm_checked(comps_, g);
+    }
+    return e;
+  }
+
   cudaError_t leaves(const std::vector<GemmProblem>& probs, int64_t m, int64_t l, int64_t n) {
     if (probs.empty() || m == 0 || n == 0) return cudaSuccess;
     void* d = nullptr;
@@ -166,8 +194,10 @@ class Driver {
 
   // One level of the recursion for `nodes` (all m x l x n): padding, the
   // operand sums, and the children (returned).  multiply.py:300-332.
+  // fuse: the children are leaves whose operand sums the leaf launch folds
+  // into its tile loads (no sums materialised at this level).
   cudaError_t expand(std::vector<Node>& nodes, int64_t m, int64_t l, int64_t n,
-                     std::vector<Node>* children) {
+                     std::vector<Node>* children, bool fuse = false) {
     TraceRange trace_("strassen: operand sums (one level)");
     const int64_t me = m + (m & 1), le = l + (l & 1), ne = n + (n & 1);
     const int64_t hm = me / 2, hl = le / 2, hn = ne / 2;
@@ -182,13 +212,40 @@ class Driver {
         if ((e = alloc(me, ne, false, &nd.C)) != cudaSuccess) return e;
         nd.crop = true;
       }
-      if ((e = alloc(5 * hm, hl, false, &ta)) != cudaSuccess) return e;
-      if ((e = alloc(5 * hl, hn, false, &tb)) != cudaSuccess) return e;
       if ((e = alloc(7 * hm, hn, false, &pt)) != cudaSuccess) return e;
       const View a11 = sub(Ap, 0, 0, hm, hl), a12 = sub(Ap, 0, hl, hm, hl);
       const View a21 = sub(Ap, hm, 0, hm, hl), a22 = sub(Ap, hm, hl, hm, hl);
       const View b11 = sub(Bp, 0, 0, hl, hn), b12 = sub(Bp, 0, hn, hl, hn);
       const View b21 = sub(Bp, hl, 0, hl, hn), b22 = sub(Bp, hl, hn, hl, hn);
+      for (int q = 0; q < 7; ++q) nd.P[q] = sub(pt, q * hm, 0, hm, hn);
+      if (fuse) {
+        // the seven products' operands as (first, second, sign) triples, in
+        // the reference's order and signs (multiply.py:313-321)
+        const View* xa[7] = {&a11, &a21, &a11, &a22, &a11, &a21, &a12};
+        const View* ya[7] = {&a22, &a22, nullptr, nullptr, &a12, &a11, &a22};
+        const int sga[7] = {1, 1, 0, 0, 1, -1, -1};
+        const View* xb[7] = {&b11, &b11, &b12, &b21, &b22, &b11, &b21};
+        const View* yb[7] = {&b22, nullptr, &b22, &b11, nullptr, &b12, &b22};
+        const int sgb[7] = {1, 0, -1, -1, 0, 1, 1};
+        for (int q = 0; q < 7; ++q) {
+          Node c;
+          c.A = *xa[q];
+          c.B = *xb[q];
+          c.sa = sga[q];
+          c.sb = sgb[q];
+          if (ya[q]) c.A2 = *ya[q];
+          if (yb[q]) c.B2 = *yb[q];
+          c.C = nd.P[q];
+          children->push_back(c);
+        }
+        if (stats_) {
+          stats_[0] += 7;
+          stats_[1] += 18;
+        }
+        continue;
+      }
+      if ((e = alloc(5 * hm, hl, false, &ta)) != cudaSuccess) return e;
+      if ((e = alloc(5 * hl, hn, false, &tb)) != cudaSuccess) return e;
       View SA[5], SB[5];
       for (int q = 0; q < 5; ++q) {
         SA[q] = sub(ta, q * hm, 0, hm, hl);
@@ -205,7 +262,6 @@ class Driver {
       sb.push_back(ew(SB[2], b21, b11, -1));
       sb.push_back(ew(SB[3], b11, b12, 1));
       sb.push_back(ew(SB[4], b21, b22, 1));
-      for (int q = 0; q < 7; ++q) nd.P[q] = sub(pt, q * hm, 0, hm, hn);
       const View xs[7] = {SA[0], SA[1], a11, a22, SA[2], SA[3], SA[4]};
       const View ys[7] = {SB[0], b11, SB[1], SB[2], b22, SB[3], SB[4]};
       for (int q = 0; q < 7; ++q) {
@@ -269,9 +325,13 @@ class Driver {
     nodes[0].B = B;
     nodes[0].C = C;
     cudaError_t e = cudaSuccess;
+    bool fused = false;
     while (std::min(m, std::min(l, n)) > cutoff_) {
       std::vector<Node> children;
-      if ((e = expand(nodes, m, l, n, &children)) != cudaSuccess) return e;
+      const int64_t hm = (m + (m & 1)) / 2, hl = (l + (l & 1)) / 2, hn = (n + (n & 1)) / 2;
+      // the last expansion folds its operand sums into the leaf launch
+      fused = fuse_ && std::min(hm, std::min(hl, hn)) <= cutoff_;
+      if ((e = expand(nodes, m, l, n, &children, fused)) != cudaSuccess) return e;
       levels.push_back(std::move(nodes));
       lm.push_back(m);
       ln.push_back(n);
@@ -280,11 +340,15 @@ class Driver {
       l = (l + (l & 1)) / 2;
       n = (n + (n & 1)) / 2;
     }
-    std::vector<GemmProblem> probs;
-    probs.reserve(nodes.size());
-    for (const Node& nd : nodes) probs.push_back(GemmProblem{nd.A.p, nd.B.p, nd.C.p, nd.A.ld,
-                                                             nd.B.ld, nd.C.ld});
-    if ((e = leaves(probs, m, l, n)) != cudaSuccess) return e;
+    if (fused) {
+      if ((e = leaves_fused(nodes, m, l, n)) != cudaSuccess) return e;
+    } else {
+      std::vector<GemmProblem> probs;
+      probs.reserve(nodes.size());
+      for (const Node& nd : nodes)
+        probs.push_back(GemmProblem{nd.A.p, nd.B.p, nd.C.p, nd.A.ld, nd.B.ld, nd.C.ld});
+      if ((e = leaves(probs, m, l, n)) != cudaSuccess) return e;
+    }
     for (size_t d = levels.size(); d-- > 0;)
       if ((e = combine(levels[d], lm[d], ln[d])) != cudaSuccess) return e;
     return cudaSuccess;
@@ -333,6 +397,10 @@ class Driver {
   std::vector<void*> scope_;
   const int* words_ = nullptr;
   int depth_ = 0;
+
+ public:
+  // fold the last level's operand sums into the leaf launch
+  bool fuse_ = true;
 };
 
 }  // namespace
@@ -356,6 +424,7 @@ cudaError_t strassen_run(int comps, int64_t cutoff, int tile, int64_t m, int64_t
     budget = static_cast<int64_t>(free_b / 8 * 6 / 10);
   }
   Driver d(comps, cutoff, tile, stream, stats);
+  if (const char* env = std::getenv("MPMM_STRASSEN_FUSE")) d.fuse_ = env[0] != '0';
   View a{const_cast<double*>(A), lda, m, l}, b{const_cast<double*>(B), ldb, l, n}, c{C, ldc, m, n};
   cudaError_t se = d.scan_top(a, b, m, l, n);
   if (se != cudaSuccess) return se;

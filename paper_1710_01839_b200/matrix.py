@@ -291,3 +291,46 @@ def _raise_norm(rc):
 
 __all__ = ["DenseMatrix", "BlockPartition", "make_partition", "leading_rows",
            "generate_test_pair", "frobenius_norm", "frobenius_rel_diff", "PrecisionSpec"]
+
+
+# ---------------------------------------------------------------------------
+# text dumps (the reference's write_matrix / read_matrix format)
+# ---------------------------------------------------------------------------
+
+def write_matrix(mat, fp):
+    """One header line ``rows cols precision``, then a line per row: the
+    elements separated by spaces, each element's components as hex floats
+    joined by commas -- exact, and readable by the reference's
+    read_matrix.  Device matrices are copied to the host first."""
+    data = mat.host_array()
+    fp.write(f"{mat.rows} {mat.cols} {mat.prec.token}\n")
+    for row in data:
+        fp.write(" ".join(",".join(float(c).hex() for c in el) for el in row) + "\n")
+
+
+def read_matrix(fp):
+    """Inverse of write_matrix (DD and QD dumps); a malformed dump raises
+    TableFormatError."""
+    from .errors import TableFormatError
+    head = fp.readline().split()
+    try:
+        rows, cols, prec = int(head[0]), int(head[1]), PrecisionSpec.parse(head[2])
+        comps = prec.comps
+    except (IndexError, ValueError) as ex:
+        raise TableFormatError(f"bad matrix dump header: {ex}") from None
+    if len(head) != 3:
+        raise TableFormatError("bad matrix dump header")
+    data = np.zeros((rows, cols, comps))
+    for i in range(rows):
+        elems = fp.readline().split()
+        if len(elems) != cols:
+            raise TableFormatError(f"row {i} has {len(elems)} elements, expected {cols}")
+        for j, el in enumerate(elems):
+            parts = el.split(",")
+            if len(parts) != comps:
+                raise TableFormatError(f"element {i},{j} has {len(parts)} components")
+            try:
+                data[i, j] = [float.fromhex(p) for p in parts]
+            except ValueError:
+                raise TableFormatError(f"element {i},{j}: bad hex float") from None
+    return DenseMatrix(rows, cols, prec, data)

@@ -32,6 +32,8 @@ is raised when even single components do not fit (e.g. a row spanning
 2^300 of dynamic range).
 """
 
+import collections
+import threading
 from functools import lru_cache
 
 import numpy as np
@@ -177,20 +179,36 @@ def matmul_exact_tensors(A, B):
     return C.clone()
 
 
-_OUT = {}   # (device, stream, shape) -> the driver's output buffer (stable address)
+# (device, stream, shape) -> the driver's output buffer (a stable address),
+# least recently used first; at most _OUT_KEEP shapes are kept
+_OUT = collections.OrderedDict()
+_OUT_KEEP = 4
+_OUT_LOCK = threading.Lock()
 
 
 def _out_buffer(m, n, comps, dev, stream):
     """A stable result address per shape and stream, so repeated products
     of the same operands can replay the driver's captured graph; callers
-    get a copy."""
+    get a copy.  Bounded: the least recently used shape is dropped."""
     import torch
-    key = (dev.index, stream, m, n, comps)
-    buf = _OUT.get(key)
-    if buf is None:
-        buf = torch.empty((m, n, comps), dtype=torch.float64, device=dev)
+    key = (dev.index, stream, m, n, comps, threading.get_ident())
+    with _OUT_LOCK:
+        buf = _OUT.pop(key, None)
+        if buf is None:
+            buf = torch.empty((m, n, comps), dtype=torch.float64, device=dev)
         _OUT[key] = buf
+        while len(_OUT) > _OUT_KEEP:
+            _OUT.popitem(last=False)
     return buf
+
+
+def release():
+    """Free the exact mode's cached state: result buffers here, plans,
+    workspaces, graphs and pinned buffers in the native driver
+    (mpmm_exact_release; entries in use by another thread are kept)."""
+    with _OUT_LOCK:
+        _OUT.clear()
+    _cuda.exact_release()
 
 
 def matmul_exact(a, b):

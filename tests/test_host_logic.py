@@ -407,3 +407,22 @@ def test_native_tensor_planner():
     ea3 = ea.copy()
     ea3[6] = -400
     assert _cuda.oz_plan(2, 3, 3, 64, ea3, eb) is None
+
+
+def test_matrix_dump_round_trip_and_reference_format():
+    """write_matrix / read_matrix (reference matrix.py:318-354): exact hex
+    components, one row per line; malformed dumps raise TableFormatError."""
+    import io
+    from paper_1710_01839_b200 import inputs
+    for tok in ("dd", "qd"):
+        a, _ = inputs.gemm_inputs(tok, 3, 4, 2, seed=9)
+        m = mp.DenseMatrix(3, 4, mp.PrecisionSpec.parse(tok), a)
+        buf = io.StringIO()
+        mp.write_matrix(m, buf)
+        text = buf.getvalue()
+        assert text.splitlines()[0] == f"3 4 {tok}"
+        assert text.splitlines()[1].split()[0] == ",".join(x.hex() for x in a[0, 0])
+        assert mp.read_matrix(io.StringIO(text)) == m
+    for bad in ("3 4\n", "1 2 dd\n0x1p+0,0x0p+0\n", "1 1 dd\n0x1p+0\n", "x y dd\n"):
+        with pytest.raises(TableFormatError):
+            mp.read_matrix(io.StringIO(bad))
