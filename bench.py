@@ -527,9 +527,29 @@ def run_extras(args, torch, _cuda, mp, inputs, DenseMatrix, A, B, dev, stream, b
     prec = mp.PrecisionSpec.parse(args.prec)
     comps = prec.comps
 
+    # (0) BASELINE configs[1]: DD 1024^3 blocked, seed 0, L2 flushed -- first,
+    # before the long products below warm the GPU into its power cap
+    if args.prec == "dd":
+        s = 1024
+        a1, b1 = inputs.gemm_inputs_device("dd", s, s, s, seed=0, device=dev)
+        c1 = torch.empty((s, s, 2), dtype=torch.float64, device=dev)
+        flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+        res = {}
+        for nm in (32, 64):
+            def g1():
+                _cuda.gemm_dev(2, _cuda.ALGO_BLOCK, nm, s, s, s, a1.data_ptr(), s,
+                               b1.data_ptr(), s, c1.data_ptr(), s, False, None,
+                               stream.cuda_stream)
+            timed(torch, g1, 3, flush)
+            res[nm] = statistics.mean(timed(torch, g1, 20, flush))
+        nm = min(res, key=res.get)
+        out["cfg1"] = {"what": "BASELINE configs[1]: DD blocked m=l=n=1024, seed 0, L2 flushed",
+                       "size": s, "n_min": nm, "value": 2.0 * s ** 3 / res[nm],
+                       "unit": "2mnl/s", "ms": res[nm] * 1e3, "kernel_s": res[nm]}
+        del a1, b1, c1, flush
     # (1) the tuner's step 2/3 at this size: blocked vs Strassen(cutoff)
     Ad, Bd = DenseMatrix(n, n, prec, A), DenseMatrix(n, n, prec, B)
-    cand = [c for c in (n // 32, n // 16, n // 8, n // 4, n // 2) if c >= 256]
+    cand = [c for c in (n // 64, n // 32, n // 16, n // 8, n // 4, n // 2) if c >= 128]
     strassen = []
     for cut in cand:
         mp.matmul_strassen(Ad, Bd, cut, args.nmin)
@@ -585,25 +605,6 @@ def run_extras(args, torch, _cuda, mp, inputs, DenseMatrix, A, B, dev, stream, b
     except Exception as ex:  # noqa: BLE001 - reported; the headline is unaffected
         out["tensor_mode"] = {"unavailable": f"{type(ex).__name__}: {ex}"}
 
-    # (4) BASELINE configs[1]: DD 1024^3 blocked, seed 0, L2 flushed
-    if args.prec == "dd":
-        s = 1024
-        a1, b1 = inputs.gemm_inputs_device("dd", s, s, s, seed=0, device=dev)
-        c1 = torch.empty((s, s, 2), dtype=torch.float64, device=dev)
-        flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
-        res = {}
-        for nm in (32, 64):
-            def g1():
-                _cuda.gemm_dev(2, _cuda.ALGO_BLOCK, nm, s, s, s, a1.data_ptr(), s,
-                               b1.data_ptr(), s, c1.data_ptr(), s, False, None,
-                               stream.cuda_stream)
-            timed(torch, g1, 3, flush)
-            res[nm] = statistics.mean(timed(torch, g1, 20, flush))
-        nm = min(res, key=res.get)
-        out["cfg1"] = {"what": "BASELINE configs[1]: DD blocked m=l=n=1024, seed 0, L2 flushed",
-                       "size": s, "n_min": nm, "value": 2.0 * s ** 3 / res[nm],
-                       "unit": "2mnl/s", "ms": res[nm] * 1e3, "kernel_s": res[nm]}
-        del a1, b1, c1, flush
     torch.cuda.empty_cache()
     return out
 

@@ -483,6 +483,62 @@ gemm_tiled(const GemmProblem* __restrict__ probs, Prob single, int m, int n, int
   if (nonfinite != nullptr && bad) atomicOr(nonfinite, 1);
 }
 
+// The Dekker (rare-path) launches of the domain gate as persistent CTAs
+// striding over the tiles: in the usual in-domain case every CTA exits at
+// the gate, so the launch costs one small grid instead of a CTA per tile.
+// SUM: Strassen leaves with folded operand sums (SumProblem table).
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB, bool SUM>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
+gemm_persist(const GemmProblem* __restrict__ probs, const SumProblem* __restrict__ sprobs,
+             Prob single, int P, int m, int n, int l, int accumulate, int* __restrict__ nonfinite,
+             const DomainGate gate) {
+  constexpr int NT = (BM / TM) * (BN / TN);
+  extern __shared__ __align__(16) double2 dsmem[];
+  if (gate_skip(gate)) return;
+  const int tiles_n = (n + BN - 1) / BN, tiles_m = (m + BM - 1) / BM;
+  const int per = tiles_m * tiles_n;
+  const int64_t total = (int64_t)P * per;
+  bool bad = false;
+  for (int64_t u = blockIdx.x; u < total; u += gridDim.x) {
+    const int p = (int)(u / per), t = (int)(u % per);
+    const int m0 = (t / tiles_n) * BM, n0 = (t % tiles_n) * BN;
+    if constexpr (SUM) {
+      gemm_tile_sum<Ops, BM, BN, BK, TM, TN, NT>(get_sum_prob(sprobs[p]), m, n, l, m0, n0,
+                                                dsmem, bad);
+    } else {
+      gemm_tile<Ops, BM, BN, BK, TM, TN, NT>(get_prob(probs, single, p), m, n, l, accumulate,
+                                             m0, n0, dsmem, bad);
+    }
+  }
+  if (nonfinite != nullptr && bad) atomicOr(nonfinite, 1);
+}
+
+inline Prob single_prob(const GemmArgs& g);
+
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB>
+cudaError_t launch_persist(const GemmArgs& g) {
+  const bool sum = g.sprobs != nullptr;
+  auto kern = sum ? gemm_persist<Ops, BM, BN, BK, TM, TN, MINB, true>
+                  : gemm_persist<Ops, BM, BN, BK, TM, TN, MINB, false>;
+  const size_t bytes = (sum ? SumSmem<Ops, BM, BN, BK>::TOTAL
+                            : TileSmem<Ops, BM, BN, BK>::TOTAL) * sizeof(double2);
+  constexpr int NT = (BM / TM) * (BN / TN);
+  int dev = 0, sms = 0, occ = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, bytes);
+  if (e != cudaSuccess) return e;
+  const int64_t tiles = (int64_t)((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN) * g.batch;
+  if (tiles == 0) return cudaSuccess;
+  const int64_t slots = (int64_t)sms * (occ > 0 ? occ : 1);
+  const unsigned grid = (unsigned)(tiles < slots ? tiles : slots);
+  kern<<<grid, NT, bytes, g.stream>>>(g.probs, g.sprobs, single_prob(g), g.batch, g.m, g.n, g.l,
+                                      g.accumulate, g.nonfinite, g.gate);
+  return cudaGetLastError();
+}
+
 // Persistent largest-first kernel: big BM x BN tiles in whole waves, then
 // the leftover big tiles as quarter tiles (BM/2 x BN/2, TM/2 x TN/2 per
 // thread, same thread count).

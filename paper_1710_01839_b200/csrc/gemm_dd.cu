@@ -65,8 +65,7 @@ cudaError_t dd_gemm_launch(const GemmArgs& g) {
 cudaError_t dd_dekker_launch(const GemmArgs& g) {
   if (g.m <= 0 || g.n <= 0 || g.batch <= 0) return cudaSuccess;
   if (g.kready != nullptr) return cudaErrorNotSupported;
-  if (g.sprobs != nullptr) return launch_tiled_sum<DDDekkerOps, 32, 32, 16, 2, 2, 2>(g);
-  return launch_tiled<DDDekkerOps, 32, 32, 16, 2, 2, 2>(g);
+  return launch_persist<DDDekkerOps, 32, 32, 16, 2, 2, 2>(g);
 }
 
 cudaError_t dd_gemm_geometry(int algo, int tile, Geometry* geo) {

@@ -35,8 +35,7 @@ cudaError_t qd_gemm_launch(const GemmArgs& g) {
 cudaError_t qd_dekker_launch(const GemmArgs& g) {
   if (g.m <= 0 || g.n <= 0 || g.batch <= 0) return cudaSuccess;
   if (g.kready != nullptr) return cudaErrorNotSupported;
-  if (g.sprobs != nullptr) return launch_tiled_sum<QDDekkerOps, 16, 16, 8, 1, 1, 2>(g);
-  return launch_tiled<QDDekkerOps, 16, 16, 8, 1, 1, 2>(g);
+  return launch_persist<QDDekkerOps, 16, 16, 8, 1, 1, 2>(g);
 }
 
 cudaError_t qd_gemm_geometry(int algo, int tile, Geometry* geo) {

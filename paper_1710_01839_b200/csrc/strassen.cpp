@@ -330,7 +330,9 @@ class Driver {
       std::vector<Node> children;
       const int64_t hm = (m + (m & 1)) / 2, hl = (l + (l & 1)) / 2, hn = (n + (n & 1)) / 2;
       // the last expansion folds its operand sums into the leaf launch
-      fused = fuse_ && std::min(hm, std::min(hl, hn)) <= cutoff_;
+      // when the leaves are small enough for that to pay
+      fused = std::min(hm, std::min(hl, hn)) <= cutoff_ &&
+              (fuse_ == 1 || (fuse_ < 0 && std::max(hm, std::max(hl, hn)) <= kFuseLeafMax));
       if ((e = expand(nodes, m, l, n, &children, fused)) != cudaSuccess) return e;
       levels.push_back(std::move(nodes));
       lm.push_back(m);
@@ -399,8 +401,14 @@ class Driver {
   int depth_ = 0;
 
  public:
-  // fold the last level's operand sums into the leaf launch
-  bool fuse_ = true;
+  // fold the last level's operand sums into the leaf launch: 1 always,
+  // 0 never, -1 (default) for leaves up to kFuseLeafMax.  Measured on the
+  // B200 (tools/exp/strassen_fuse_probe.py): 1.6 % faster with 128^3 leaves,
+  // 2-3.5 % slower from 256^3 up (the fold re-sums every operand tile once
+  // per CTA column -- +2.5 % FP64 work -- against 48 B per summed element
+  // of HBM traffic saved)
+  int fuse_ = -1;
+  static constexpr int64_t kFuseLeafMax = 128;
 };
 
 }  // namespace
@@ -424,7 +432,7 @@ cudaError_t strassen_run(int comps, int64_t cutoff, int tile, int64_t m, int64_t
     budget = static_cast<int64_t>(free_b / 8 * 6 / 10);
   }
   Driver d(comps, cutoff, tile, stream, stats);
-  if (const char* env = std::getenv("MPMM_STRASSEN_FUSE")) d.fuse_ = env[0] != '0';
+  if (const char* env = std::getenv("MPMM_STRASSEN_FUSE")) d.fuse_ = env[0] == '0' ? 0 : 1;
   View a{const_cast<double*>(A), lda, m, l}, b{const_cast<double*>(B), ldb, l, n}, c{C, ldc, m, n};
   cudaError_t se = d.scan_top(a, b, m, l, n);
   if (se != cudaSuccess) return se;
