@@ -77,6 +77,24 @@ struct QDDekkerOps {
   }
 };
 
+// Tile t of a tiles_m x tiles_n grid in grouped order: kGroupM tile rows
+// at a time, column-major inside the group.  The ~296 CTAs resident at once
+// then share ~16 A row panels and ~19 B column panels instead of 1-2 A
+// panels and every B panel of a row-major sweep, so B is re-read from HBM
+// once per 16 tile rows rather than once per tile row (8192^3 DD: 279 GB
+// of DRAM reads per launch row-major, profiles/r02f_dd8192_raw.csv).  The
+// order never changes a bit: each output tile is computed independently.
+constexpr int kGroupM = 16;
+
+__device__ __forceinline__ void grouped_tile(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
+  const int span = kGroupM * tiles_n;
+  const int first = (t / span) * kGroupM;
+  const int rows = min(kGroupM, tiles_m - first);
+  const int r = t % span;
+  tm = first + r % rows;
+  tn = r / rows;
+}
+
 // Problem descriptor (pointers as double2 views, leading dims in elements).
 struct Prob {
   const double2* A;
@@ -441,8 +459,9 @@ gemm_tiled_sum(const SumProblem* __restrict__ probs, int m, int n, int l,
   const int p = blockIdx.x / per, t = blockIdx.x % per;
   const SumProb pr = get_sum_prob(probs[p]);
   bool bad = false;
-  gemm_tile_sum<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, (t / tiles_n) * BM, (t % tiles_n) * BN,
-                                            dsmem, bad);
+  int tm, tn;
+  grouped_tile(t, tiles_m, tiles_n, tm, tn);
+  gemm_tile_sum<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, tm * BM, tn * BN, dsmem, bad);
   if (nonfinite != nullptr && bad) atomicOr(nonfinite, 1);
 }
 
@@ -477,8 +496,9 @@ gemm_tiled(const GemmProblem* __restrict__ probs, Prob single, int m, int n, int
   const int p = blockIdx.x / per, t = blockIdx.x % per;
   const Prob pr = get_prob(probs, single, p);
   bool bad = false;
-  gemm_tile<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, (t / tiles_n) * BM,
-                                         (t % tiles_n) * BN, smem, bad,
+  int tm, tn;
+  grouped_tile(t, tiles_m, tiles_n, tm, tn);
+  gemm_tile<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, tm * BM, tn * BN, smem, bad,
                                          STREAM ? kr : KReady{nullptr, 0});
   if (nonfinite != nullptr && bad) atomicOr(nonfinite, 1);
 }
@@ -567,7 +587,9 @@ gemm_lpt(const GemmProblem* __restrict__ probs, Prob single, int P, int m, int n
     }
     const int p = t / per, tt = t % per;
     const Prob pr = get_prob(probs, single, p);
-    int m0 = (tt / tiles_n) * BM, n0 = (tt % tiles_n) * BN;
+    int tm, tn;
+    grouped_tile(tt, tiles_m, tiles_n, tm, tn);
+    int m0 = tm * BM, n0 = tn * BN;
     if (q < 0) {
       gemm_tile<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, m0, n0, smem, bad);
     } else {

@@ -40,13 +40,13 @@ def _oracle_local_gemm(a_local, b_panel, c_local, k0, k1, accumulate):
         oracle.block_cells(a, b, c, 8, 0, cells)
 
 
-def _worker(rank, world, port, tok, m, l, n, panel, out_path):
+def _worker(rank, world, port, tok, m, l, n, panel, out_path, align=4):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         a, b = inputs.gemm_inputs(tok, m, l, n, seed=5)
-        lo, hi = shard.row_shards(m, world, align=4)[rank]
+        lo, hi = shard.row_shards(m, world, align=align)[rank]
         a_local = torch.from_numpy(np.ascontiguousarray(a[lo:hi]))
         b_buf = torch.from_numpy(b.copy()) if rank == 0 else torch.zeros(b.shape, dtype=torch.float64)
         c_local = shard.broadcast_matmul(a_local, b_buf, panel_rows=panel, src=0,
@@ -66,6 +66,20 @@ def test_two_rank_broadcast_matmul_is_bitwise_invariant(tmp_path, tok, m, l, n, 
     parts = [np.load(f"{out}.{r}.npy") for r in range(world)]
     c = np.concatenate(parts, axis=0)
     a, b = inputs.gemm_inputs(tok, m, l, n, seed=5)
+    assert np.array_equal(c, oracle.matmul_simple(a, b))
+
+
+def test_four_ranks_uneven_64_row_shards(tmp_path):
+    """World size 4 with the production 64-row alignment and m not a
+    multiple of it (m = 200: shards of 64, 64, 64 and 8 rows), B in five
+    uneven k-panels: the stitched C is bitwise the single product."""
+    world, m, l, n = 4, 200, 150, 40
+    assert [hi - lo for lo, hi in shard.row_shards(m, world, align=64)] == [64, 64, 64, 8]
+    out = str(tmp_path / "c4")
+    tmp.spawn(_worker, args=(world, _free_port(), "dd", m, l, n, 32, out, 64), nprocs=world,
+              join=True)
+    c = np.concatenate([np.load(f"{out}.{r}.npy") for r in range(world)], axis=0)
+    a, b = inputs.gemm_inputs("dd", m, l, n, seed=5)
     assert np.array_equal(c, oracle.matmul_simple(a, b))
 
 
