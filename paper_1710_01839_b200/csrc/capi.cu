@@ -251,7 +251,28 @@ int host_rows_gemm_streamed(int comps, int tile, int64_t rows, int64_t l, int64_
   double* dCh = static_cast<double*>(pinned_alias(c_rows));
   if (dCh == nullptr) return -1;
   const size_t el = comps * sizeof(double);
-  const int npan = static_cast<int>((l + kStreamPanel - 1) / kStreamPanel);
+  // Two streaming orders.  k-panels (64 columns of A and rows of B): every
+  // tile consumes panel after panel, so only the first panel is exposed --
+  // as long as all panels land within one wave of tiles.  For large
+  // operands (>= 128 MiB) they do not (DD 8192^3: 2 GiB of H2D take ~40 ms,
+  // one wave computes in ~7 ms), so A goes by row panels and B by column
+  // panels in the order the grouped tile raster consumes them: the first
+  // wave needs ~16 A and ~19 B panels (~140 MB) and later waves find theirs
+  // already landed.
+  int64_t tile_mb = 128;   // MPMM_STREAM_TILE_MB: the switch-over (tests, measurements)
+  if (const char* env = std::getenv("MPMM_STREAM_TILE_MB")) tile_mb = std::atoll(env);
+  const bool tile_mode = tile_mb >= 0 &&
+                         static_cast<int64_t>((rows * l + l * n) * el) >= (tile_mb << 20);
+  constexpr int64_t kRowsPerA = 64, kColsPerB = 128;
+  Geometry geo{};
+  if (tile_mode) {
+    cudaError_t ge = comps == 2 ? dd_gemm_geometry(ALGO_BLOCK, tile, &geo)
+                                : qd_gemm_geometry(ALGO_BLOCK, tile, &geo);
+    if (ge != cudaSuccess) return cuda_fail(ge, "streamed product: tile geometry");
+  }
+  const int na = tile_mode ? static_cast<int>((rows + kRowsPerA - 1) / kRowsPerA) : 0;
+  const int nb = tile_mode ? static_cast<int>((n + kColsPerB - 1) / kColsPerB) : 0;
+  const int npan = tile_mode ? na + nb : static_cast<int>((l + kStreamPanel - 1) / kStreamPanel);
   DevBuf dA, dB, dflags;
   CU(dA.alloc(rows * l * comps, hs->comp));
   CU(dB.alloc(l * n * comps, hs->comp));
@@ -265,28 +286,62 @@ int host_rows_gemm_streamed(int comps, int tile, int64_t rows, int64_t l, int64_
   CU(cudaEventRecord(ready.e, hs->comp));
   CU(cudaStreamWaitEvent(hs->copy, ready.e, 0));
   // The GEMM is enqueued FIRST: its CTAs start as soon as the flags are
-  // zeroed and wait for each panel, so the ~50 copy/flag API calls below
-  // no longer delay the launch.
+  // zeroed and wait for each panel, so the copy/flag API calls below no
+  // longer delay the launch.
   GemmArgs g{ALGO_BLOCK, tile, (int)rows, (int)n, (int)l, dA.p, l, dB.p, n, dCh, n, 0, dint,
              hs->comp};
   g.kready = dint + 1;
-  g.kpanel = static_cast<int>(kStreamPanel);
+  if (tile_mode) {
+    g.kpanel = 0;
+    g.ktile_rows = static_cast<int>(kRowsPerA);
+    g.ktile_cols = static_cast<int>(kColsPerB);
+    g.ka_panels = na;
+  } else {
+    g.kpanel = static_cast<int>(kStreamPanel);
+  }
   CU(gemm(comps, g));
-  for (int p = 0; p < npan; ++p) {
-    const int64_t k0 = p * kStreamPanel, k1 = std::min<int64_t>(l, k0 + kStreamPanel);
-    cudaError_t e = cudaMemcpy2DAsync(dA.p + k0 * comps, l * el, a_rows + k0 * comps, l * el,
-                                      (k1 - k0) * el, rows, cudaMemcpyHostToDevice, hs->copy);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(dB.p + k0 * n * comps, b + k0 * n * comps, (k1 - k0) * n * el,
-                          cudaMemcpyHostToDevice, hs->copy);
+  // the copies, each followed by its flag, in consumption order
+  struct Copy { bool is_a; int64_t lo, hi; int flag; };
+  std::vector<Copy> order;
+  if (tile_mode) {
+    const int first_group = static_cast<int>(
+        std::min<int64_t>(na, (int64_t{kTileGroupM} * geo.bm + kRowsPerA - 1) / kRowsPerA));
+    auto a_panel = [&](int q) {
+      order.push_back({true, q * kRowsPerA, std::min<int64_t>(rows, (q + 1) * kRowsPerA), q});
+    };
+    for (int q = 0; q < first_group; ++q) a_panel(q);
+    for (int q = 0; q < nb; ++q)
+      order.push_back({false, q * kColsPerB, std::min<int64_t>(n, (q + 1) * kColsPerB), na + q});
+    for (int q = first_group; q < na; ++q) a_panel(q);
+  } else {
+    for (int p = 0; p < npan; ++p)
+      order.push_back({true, p * kStreamPanel, std::min<int64_t>(l, (p + 1) * kStreamPanel), p});
+  }
+  for (size_t i = 0; i < order.size(); ++i) {
+    const Copy& c = order[i];
+    cudaError_t e;
+    if (!tile_mode) {              // k-panel: columns of A, rows of B
+      e = cudaMemcpy2DAsync(dA.p + c.lo * comps, l * el, a_rows + c.lo * comps, l * el,
+                            (c.hi - c.lo) * el, rows, cudaMemcpyHostToDevice, hs->copy);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(dB.p + c.lo * n * comps, b + c.lo * n * comps,
+                            (c.hi - c.lo) * n * el, cudaMemcpyHostToDevice, hs->copy);
+    } else if (c.is_a) {           // rows of A
+      e = cudaMemcpyAsync(dA.p + c.lo * l * comps, a_rows + c.lo * l * comps,
+                          (c.hi - c.lo) * l * el, cudaMemcpyHostToDevice, hs->copy);
+    } else {                       // columns of B
+      e = cudaMemcpy2DAsync(dB.p + c.lo * comps, n * el, b + c.lo * comps, n * el,
+                            (c.hi - c.lo) * el, l, cudaMemcpyHostToDevice, hs->copy);
+    }
     if (e != cudaSuccess) {
       // release the launched GEMM (it must not wait out its bound), then report
-      for (int q = p; q < npan; ++q)
-        cudaMemcpyAsync(dint + 1 + q, one, sizeof(int), cudaMemcpyHostToDevice, hs->copy);
+      for (size_t j = i; j < order.size(); ++j)
+        cudaMemcpyAsync(dint + 1 + order[j].flag, one, sizeof(int), cudaMemcpyHostToDevice,
+                        hs->copy);
       cudaStreamSynchronize(hs->comp);
       return cuda_fail(e, "streamed product: operand panel copy");
     }
-    CU(cudaMemcpyAsync(dint + 1 + p, one, sizeof(int), cudaMemcpyHostToDevice, hs->copy));
+    CU(cudaMemcpyAsync(dint + 1 + c.flag, one, sizeof(int), cudaMemcpyHostToDevice, hs->copy));
   }
   // The streamed launch runs the DFMA kernel before the operands have
   // landed, so their domain check (domain.cuh) follows the copies on the

@@ -84,7 +84,7 @@ struct QDDekkerOps {
 // once per 16 tile rows rather than once per tile row (8192^3 DD: 279 GB
 // of DRAM reads per launch row-major, profiles/r02f_dd8192_raw.csv).  The
 // order never changes a bit: each output tile is computed independently.
-constexpr int kGroupM = 16;
+constexpr int kGroupM = kTileGroupM;
 
 __device__ __forceinline__ void grouped_tile(int t, int tiles_m, int tiles_n, int& tm, int& tn) {
   const int span = kGroupM * tiles_n;
@@ -123,13 +123,45 @@ struct TileSmem {
 // written by the copy stream (a 4-byte copy-engine H2D) after the panel's
 // H2D, so a CTA spinning here never waits on another kernel; the operand
 // tiles are then read through L2 (cp.async.cg), where the DMA writes land.
+//
+// Tile mode (panel_k == 0, tile_rows > 0): large products stream A by row
+// panels and B by column panels in the order the grouped tile raster
+// consumes them; flags[q] for A row panel q (tile_rows rows), then
+// flags[a_panels + q] for B column panel q (tile_cols columns).  A CTA waits
+// once, before its tile, for the panels its rows and columns lie in.
 struct KReady {
   const int* flags;
   int panel_k;
+  int tile_rows = 0, tile_cols = 0, a_panels = 0;
 };
 
+// bounded wait for flags[q] (see wait_k_panel); called by one thread
+__device__ __forceinline__ void spin_flag(const KReady& kr, int q) {
+  const volatile int* f = kr.flags + q;
+  const volatile int* st = kr.flags - 1;
+  const long long t0 = clock64();
+  while (*f == 0 && (*st & 4) == 0) {
+    __nanosleep(200);
+    if (clock64() - t0 > (1ll << 32)) {   // ~2.2 s at 1.965 GHz
+      atomicOr(const_cast<int*>(kr.flags) - 1, 4);
+      break;
+    }
+  }
+}
+
+__device__ __forceinline__ void wait_tile_panels(const KReady& kr, int m0, int n0, int m, int n,
+                                                 int bm, int bn) {
+  if (kr.flags == nullptr || kr.panel_k != 0) return;
+  if (threadIdx.x == 0) {
+    spin_flag(kr, (min(m0 + bm, m) - 1) / kr.tile_rows);
+    spin_flag(kr, kr.a_panels + (min(n0 + bn, n) - 1) / kr.tile_cols);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ void wait_k_panel(const KReady& kr, int k0, int& seen) {
-  if (kr.flags == nullptr) return;
+  if (kr.flags == nullptr || kr.panel_k == 0) return;
   const int q = k0 / kr.panel_k;
   if (q <= seen) return;
   if (threadIdx.x == 0) {
@@ -214,6 +246,7 @@ __device__ __forceinline__ void gemm_tile(const Prob& pr, int m, int n, int l, i
   };
 
   int seen = -1;   // highest k-panel known to have landed (streamed operands)
+  wait_tile_panels(kr, m0, n0, m, n, BM, BN);
   if (ktiles > 0) {
     wait_k_panel(kr, 0, seen);
     load(0, 0);
@@ -659,7 +692,7 @@ cudaError_t launch_tiled(const GemmArgs& g) {
   if (tiles == 0) return cudaSuccess;
   if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
   const unsigned grid = (unsigned)tiles, nt = (BM / TM) * (BN / TN);
-  const KReady kr{g.kready, g.kpanel};
+  const KReady kr{g.kready, g.kpanel, g.ktile_rows, g.ktile_cols, g.ka_panels};
   if (g.kready != nullptr)
     gemm_tiled<Ops, BM, BN, BK, TM, TN, MINB, true><<<grid, nt, 0, g.stream>>>(
         g.probs, single_prob(g), g.m, g.n, g.l, g.accumulate, g.nonfinite, kr, g.gate);

@@ -59,6 +59,9 @@ struct GemmArgs {
   // are kpanel columns of k.  Null: the operands are already resident.
   const int* kready = nullptr;
   int kpanel = 0;
+  // kpanel == 0 with kready set: tile mode -- kready[0 .. ka_panels) flag A
+  // row panels of ktile_rows rows, then B column panels of ktile_cols columns
+  int ktile_rows = 0, ktile_cols = 0, ka_panels = 0;
   // EFT-domain gate (domain.cuh): with gate.words set, the launch runs only
   // on the side of the domain test gate.want_unsafe selects.
   DomainGate gate{};
@@ -68,6 +71,10 @@ struct GemmArgs {
 };
 
 // The DFMA mirror kernels (ALGO_SIMPLE / ALGO_BLOCK / ALGO_BLOCK_FAST).
+// Tile rows per group of the grouped tile raster (gemm.cuh grouped_tile);
+// the streamed host product copies operands in that order.
+constexpr int kTileGroupM = 16;
+
 cudaError_t dd_gemm_launch(const GemmArgs& g);
 cudaError_t qd_gemm_launch(const GemmArgs& g);
 // The same products with the reference's Dekker TwoProd (one tile shape for

@@ -111,3 +111,26 @@ def test_streamed_host_products_from_concurrent_threads(gpu):
 
     with ThreadPoolExecutor(4) as ex:
         assert all(ex.map(work, range(8)))
+
+
+@pytest.mark.parametrize("tok,m,l,n,nmin", [("dd", 700, 300, 650, 32), ("dd", 1030, 257, 333, 16),
+                                            ("qd", 200, 150, 300, 64), ("dd", 64, 200, 900, 128)])
+def test_tile_streamed_host_product(gpu, monkeypatch, tok, m, l, n, nmin):
+    """Large host products stream A by row panels and B by column panels in
+    the grouped tile raster's order (one wait per tile); forced here at small
+    sizes (MPMM_STREAM_TILE_MB=0) with ragged panel counts: the reference's
+    bits, also with operands outside the DFMA domain (NaN row, Dekker path)."""
+    monkeypatch.setenv("MPMM_STREAM_TILE_MB", "0")
+    prec = mp.PrecisionSpec.parse(tok)
+    a, b = inputs.gemm_inputs(tok, m, l, n, seed=13)
+    want = oracle.matmul_simple(a, b)
+    out = _pinned(np.zeros((m, n, prec.comps)))
+    assert _cuda.gemm_host(prec.comps, _cuda.ALGO_BLOCK, nmin, _pinned(a), _pinned(b), out)
+    assert np.array_equal(out, want)
+    a[m // 2, l // 3] = 0.0
+    a[m // 2, l // 3, 0] = 0.75 * 2.0 ** 1000        # the reference's split overflows
+    want = oracle.matmul_simple(a, b)
+    out = _pinned(np.zeros((m, n, prec.comps)))
+    assert not _cuda.gemm_host(prec.comps, _cuda.ALGO_BLOCK, nmin, _pinned(a), _pinned(b), out)
+    from test_oracle_golden import same_bits
+    assert same_bits(out, want) and np.isnan(out[m // 2]).all()
