@@ -120,3 +120,23 @@ def test_predict_layout(gpu, capsys):
     assert main(["predict", "--prec", "dd", "--dim", "256", "--nmin", "16,32,64"]) == EX_OK
     out = capsys.readouterr().out
     assert "best n_min=" in out and out.count("\n") >= 5
+
+
+@pytest.mark.gpu
+def test_tune_gpu_sweep_seeded_inputs(gpu, tmp_path, capsys):
+    """tune --gpus 1,2,8 --inputs seeded: rows per GPU count (G > 1 from the
+    shard product plus the broadcast model, 'G~' in the v2 table), the
+    gpus_source CSV column, a winners grid per GPU count."""
+    out = tmp_path / "g.tbl"
+    rc = main(["tune", "--prec", "dd", "--dims", "256", "--nmin", "16,32", "--threads", "1",
+               "--gpus", "1,2,8", "--cutoffs", "64", "--inputs", "seeded", "--seed", "1",
+               "--out", str(out)])
+    assert rc == EX_OK
+    text = open(out).read()
+    assert text.startswith("mpmmtune v2") and " 2~ " in text and " 8~ " in text
+    rows = [ln for ln in open(str(out) + ".csv") if not ln.startswith("#")]
+    assert rows[0].startswith("prec,bits,n,threads,gpus,gpus_source,")
+    assert len(rows) == 4 and "shard+bcast model" in rows[3]
+    assert main(["report", "--in", str(out), "--format", "winners"]) == EX_OK
+    grid = capsys.readouterr().out
+    assert "gpus=2" in grid and "gpus=8" in grid and "?" not in grid
