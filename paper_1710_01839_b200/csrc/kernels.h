@@ -73,7 +73,10 @@ struct GemmArgs {
 // The DFMA mirror kernels (ALGO_SIMPLE / ALGO_BLOCK / ALGO_BLOCK_FAST).
 // Tile rows per group of the grouped tile raster (gemm.cuh grouped_tile);
 // the streamed host product copies operands in that order.
-constexpr int kTileGroupM = 16;
+#ifndef MPMM_GROUP_M
+#define MPMM_GROUP_M 16   // experiments: -DMPMM_GROUP_M=n (tools/exp/build_variant.py)
+#endif
+constexpr int kTileGroupM = MPMM_GROUP_M;
 
 cudaError_t dd_gemm_launch(const GemmArgs& g);
 cudaError_t qd_gemm_launch(const GemmArgs& g);
