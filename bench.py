@@ -561,7 +561,7 @@ def run_extras(args, torch, _cuda, mp, inputs, DenseMatrix, A, B, dev, stream, b
         del a1, b1, c1, flush
     # (1) the tuner's step 2/3 at this size: blocked vs Strassen(cutoff)
     Ad, Bd = DenseMatrix(n, n, prec, A), DenseMatrix(n, n, prec, B)
-    cand = [c for c in (n // 64, n // 32, n // 16, n // 8, n // 4, n // 2) if c >= 128]
+    cand = [c for c in (n // 128, n // 64, n // 32, n // 16, n // 8, n // 4, n // 2) if c >= 64]
     strassen = []
     for cut in cand:
         mp.matmul_strassen(Ad, Bd, cut, args.nmin)

@@ -31,6 +31,19 @@
 #define MPMM_DD32 32, 64, 8, 2, 4, 2
 #endif
 
+// TILE_LPT's configuration (experiments: -DMPMM_LPT_VAR=i)
+#if !defined(MPMM_LPT_VAR) || MPMM_LPT_VAR == 0
+#define MPMM_LPT_CFG 64, 64, 8, 4, 4, 1
+#elif MPMM_LPT_VAR == 1
+#define MPMM_LPT_CFG 64, 64, 8, 4, 4, 2
+#elif MPMM_LPT_VAR == 2
+#define MPMM_LPT_CFG 64, 64, 16, 4, 4, 2
+#elif MPMM_LPT_VAR == 3
+#define MPMM_LPT_CFG 64, 32, 8, 4, 2, 2
+#elif MPMM_LPT_VAR == 4
+#define MPMM_LPT_CFG 32, 64, 8, 2, 4, 2
+#endif
+
 namespace mpmm {
 
 template <class Ops>
@@ -40,7 +53,7 @@ static cudaError_t dd_blocked(const GemmArgs& g) {
     case TILE_32: return launch_tiled<Ops, MPMM_DD32>(g);
     case TILE_64: return launch_tiled<Ops, 64, 64, 8, 4, 4, 1>(g);
     case TILE_32x64: return launch_tiled<Ops, 32, 64, 8, 2, 2, 1>(g);
-    case TILE_LPT: return launch_lpt<Ops, 64, 64, 8, 4, 4, 1>(g);
+    case TILE_LPT: return launch_lpt<Ops, MPMM_LPT_CFG>(g);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -79,7 +92,7 @@ cudaError_t dd_gemm_geometry(int algo, int tile, Geometry* geo) {
       case TILE_32x64: geo->bm = 32, geo->bn = 64;
         return occupancy_of(gemm_tiled<DDFastOps, 32, 64, 8, 2, 2, 1>, 512, geo);
       case TILE_LPT: geo->bm = 64, geo->bn = 64;
-        return occupancy_of(gemm_lpt<DDFastOps, 64, 64, 8, 4, 4, 1>, 256, geo);
+        return occupancy_of(gemm_lpt<DDFastOps, MPMM_LPT_CFG>, 256, geo);
       default: return cudaErrorInvalidValue;
     }
   }
@@ -96,7 +109,7 @@ cudaError_t dd_gemm_geometry(int algo, int tile, Geometry* geo) {
     case TILE_32x64: geo->bm = 32, geo->bn = 64;
       return occupancy_of(gemm_tiled<DDOps, 32, 64, 8, 2, 2, 1>, 512, geo);
     case TILE_LPT: geo->bm = 64, geo->bn = 64;
-      return occupancy_of(gemm_lpt<DDOps, 64, 64, 8, 4, 4, 1>, 256, geo);
+      return occupancy_of(gemm_lpt<DDOps, MPMM_LPT_CFG>, 256, geo);
     default: return cudaErrorInvalidValue;
   }
 }
