@@ -459,7 +459,44 @@ def run_ours(args, rank, world, local_rank):
     h2d = elem * (n * n + n * n)           # all of A (over the ranks) + B once
     d2h = elem * n * n + 4 * world         # C + the finite flags
 
+    # N > 1: the fused alternative to the broadcast -- every rank's GEMM
+    # reads B straight from rank 0's HBM over peer memory (CUDA IPC,
+    # shard.PeerOperand), no collective; reported beside the NCCL line
+    peer = None
+    if world > 1 and not args.no_extras:
+        # every failure is made collective (the status all-reduce), so no
+        # rank is left waiting in a barrier the others skipped
+        pb, err = None, ""
+        try:
+            pb = shard.PeerOperand(B if rank == 0 else None, src=0)
+            for _ in range(2):
+                shard.peer_matmul(A, pb, n_min=args.nmin)
+            torch.cuda.synchronize()
+        except Exception as ex:  # noqa: BLE001 - reported below
+            err = f"{type(ex).__name__}: {ex}"
+        okt = torch.tensor([0 if err else 1], dtype=torch.int32, device=dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        if okt.item():
+            dist.barrier()
+            ps = sum(timed(torch, lambda: shard.peer_matmul(A, pb, n_min=args.nmin),
+                           args.steps))
+            dist.barrier()
+            tp = torch.tensor([ps], dtype=torch.float64, device=dev)
+            dist.all_reduce(tp, op=dist.ReduceOp.MAX)
+            peer = {"what": "B read over peer memory (CUDA IPC mapping of rank 0's buffer) by "
+                            "every rank's GEMM launch: no broadcast, same bits",
+                    "value": 2.0 * madds * args.steps / tp.item(), "unit": "2mnl/s",
+                    "ms_per_step": tp.item() / args.steps * 1e3}
+        else:
+            peer = {"unavailable": err or "another rank failed to map B"}
+        if pb is not None:
+            pb.close()
+        else:
+            dist.barrier()    # pairs with close()'s barrier on the ranks that mapped B
+
     extras = {}
+    if peer is not None:
+        extras["peer_mode"] = peer
     if rank == 0 and world == 1 and not args.no_extras:
         sub_sampler = ClockSampler(local_rank).start()
         extras = run_extras(args, torch, _cuda, mp, inputs, DenseMatrix, A, B, dev, stream,

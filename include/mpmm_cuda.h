@@ -305,6 +305,24 @@ int mpmm_gemm_multi(int comps, int algo, int64_t n_min, int64_t cutoff, int64_t 
 int mpmm_multi_plan(int64_t m, int64_t l, int ngpus, int64_t panels, int64_t *rows, int64_t *kb,
                     int *npanels);
 
+/* ---------------------------------------------------------------------------
+ * B shared over peer memory (one process per GPU): the alternative to the
+ * NCCL broadcast.  The source rank allocates B's buffer with mpmm_ipc_alloc
+ * (cudaMalloc + a CUDA IPC handle of mpmm_ipc_handle_size() bytes), the
+ * other ranks map it with mpmm_ipc_open and pass the mapped pointer as B to
+ * mpmm_gemm_dev: the GEMM reads B's tiles from the source GPU over NVLink
+ * as it consumes them (no collective, same bits).  mpmm_ipc_close unmaps,
+ * mpmm_ipc_free frees (source rank, after every mapping is closed).
+ * Errors: MPMM_ERR_ARG / MPMM_ERR_CUDA, text in mpmm_peer_last_error().
+ * ------------------------------------------------------------------------- */
+int mpmm_ipc_handle_size(void);
+/* init: optional source (device or host) copied into the new buffer */
+int mpmm_ipc_alloc(int64_t bytes, const void *init, void **ptr, void *handle);
+int mpmm_ipc_free(void *ptr);
+int mpmm_ipc_open(const void *handle, void **ptr);
+int mpmm_ipc_close(void *ptr);
+const char *mpmm_peer_last_error(void);
+
 /* Event timers on a stream (TimingPolicy's device clock, timing.py:22-59). */
 int mpmm_timer_create(void **timer);
 int mpmm_timer_start(void *timer, void *stream);

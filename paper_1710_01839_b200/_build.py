@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmpmm_cuda.so")
 SOURCES = ["gemm_dd.cu", "gemm_qd.cu", "domain.cu", "ewise.cu", "verify.cu", "rng.cu", "ozaki.cu", "tc_i8.cu", "int8gemm.cpp",
-           "strassen.cpp", "runtime.cpp", "oz_plan.cpp", "exact.cpp", "capi.cu", "host_norms.cpp"]
+           "strassen.cpp", "runtime.cpp", "peer.cpp", "oz_plan.cpp", "exact.cpp", "capi.cu", "host_norms.cpp"]
 HEADERS = ["ddqd.cuh", "common.cuh", "kernels.h", "gemm.cuh", "domain.cuh", "trace.h"]
 
 # -fmad=false: no implicit contraction (the reference is built with

@@ -76,6 +76,12 @@ _SIGNATURES = {
     "mpmm_oz_shifts_dev": [_INT, _INT, _VP, _I64, _VP, _VP, _VP, _VP],
     "mpmm_exact_check_dev": [_INT, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _VP,
                              _I64, _INT, _VP, _VP],
+    "mpmm_ipc_handle_size": [],
+    "mpmm_ipc_alloc": [_I64, _VP, ctypes.POINTER(_VP), _VP],
+    "mpmm_ipc_free": [_VP],
+    "mpmm_ipc_open": [_VP, ctypes.POINTER(_VP)],
+    "mpmm_ipc_close": [_VP],
+    "mpmm_peer_last_error": [],
     "mpmm_multi_plan": [_I64, _I64, _INT, _I64, _VP, _VP, ctypes.POINTER(_INT)],
     "mpmm_strassen_dev": [_INT, _I64, _I64, _I64, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _I64,
                           _VP, _VP, _VP],
@@ -118,7 +124,8 @@ def load():
     for name, argtypes in _SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = argtypes
-        fn.restype = ctypes.c_char_p if name == "mpmm_last_error" else ctypes.c_int
+        fn.restype = (ctypes.c_char_p if name in ("mpmm_last_error", "mpmm_peer_last_error")
+                      else ctypes.c_int)
     _lib = lib
     return lib
 
@@ -313,6 +320,36 @@ def runtime_gpus():
 def exact_release():
     """mpmm_exact_release: drop the exact mode's cached plans and buffers."""
     check(load().mpmm_exact_release())
+
+
+def _peer_check(rc):
+    if rc:
+        raise DeviceError(load().mpmm_peer_last_error().decode() or f"peer error {rc}")
+
+
+def ipc_alloc(nbytes, init=None):
+    """(device pointer, IPC handle bytes) of a fresh cudaMalloc'ed buffer,
+    filled from the pointer ``init`` when given."""
+    size = load().mpmm_ipc_handle_size()
+    handle = ctypes.create_string_buffer(size)
+    ptr = ctypes.c_void_p()
+    _peer_check(load().mpmm_ipc_alloc(nbytes, init, ctypes.byref(ptr), handle))
+    return ptr.value, handle.raw
+
+
+def ipc_open(handle):
+    buf = ctypes.create_string_buffer(handle, len(handle))
+    ptr = ctypes.c_void_p()
+    _peer_check(load().mpmm_ipc_open(buf, ctypes.byref(ptr)))
+    return ptr.value
+
+
+def ipc_close(ptr):
+    _peer_check(load().mpmm_ipc_close(ptr))
+
+
+def ipc_free(ptr):
+    _peer_check(load().mpmm_ipc_free(ptr))
 
 
 def multi_plan(m, l, ngpus, panels=0):

@@ -22,6 +22,7 @@ can be exercised on CPU ranks over ``gloo`` (tests/test_shard_gloo.py).
 import math
 
 from . import _cuda
+from .errors import DeviceError
 
 
 def row_shards(m, world, align=1):
@@ -109,6 +110,70 @@ def broadcast_matmul(a_local, b, *, n_min=64, simple=False, group=None, src=0,
         compute.wait_event(landed[p])
         local_gemm(a_local, b[k0:k1], c_local, k0, k1, p > 0)
     b.record_stream(comm)
+    return c_local
+
+
+class PeerOperand:
+    """B shared over peer memory instead of broadcast (the fused
+    alternative to the NCCL broadcast; ``csrc/peer.cpp``).
+
+    Collective: every rank of ``group`` constructs it.  The source rank
+    copies its B into a buffer it exports by CUDA IPC; the handle travels
+    once through ``torch.distributed``; every other rank maps the buffer.
+    ``ptr`` is then B's address as this rank sees it: passed as B to the
+    GEMM, the kernel reads B's tiles from the source GPU's HBM over
+    NVLink/NVSwitch while it computes -- no broadcast, no k-panel schedule,
+    the same kernels and therefore the same bits.  ``close()`` (collective)
+    unmaps and, on the source rank after a barrier, frees."""
+
+    def __init__(self, b, *, group=None, src=0):
+        import torch.distributed as dist
+        self.group, self.src = group, src
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.shape = tuple(b.shape) if b is not None else None
+        self.ptr = None
+        obj = [None]
+        if self.rank == src:
+            import torch
+            torch.cuda.synchronize(b.device)      # B complete before the copy
+            try:
+                self.ptr, handle = _cuda.ipc_alloc(b.numel() * 8, b.data_ptr())
+                obj = [(handle, self.shape)]
+            except Exception as ex:  # noqa: BLE001 - every rank raises below
+                obj = [("error", str(ex))]
+        if dist.is_initialized():
+            dist.broadcast_object_list(obj, src=_group_rank_to_global(group, src), group=group)
+        if obj[0][0] == "error":
+            raise DeviceError(f"peer operand: the source rank failed: {obj[0][1]}")
+        handle, self.shape = obj[0]
+        if self.rank != src:
+            self.ptr = _cuda.ipc_open(handle)
+
+    def close(self):
+        """Collective: unmap, barrier, free on the source rank (every rank
+        must call it, also one whose mapping failed)."""
+        import torch.distributed as dist
+        if self.ptr is not None and self.rank != self.src:
+            _cuda.ipc_close(self.ptr)
+        if dist.is_initialized():
+            dist.barrier(group=self.group)
+        if self.ptr is not None and self.rank == self.src:
+            _cuda.ipc_free(self.ptr)
+        self.ptr = None
+
+
+def peer_matmul(a_local, peer_b, *, n_min=64, simple=False, nonfinite=None):
+    """C_local = A_local * B with B read over peer memory (PeerOperand):
+    one GEMM launch on this rank, its B tiles pulled from the source GPU."""
+    import torch
+    comps = a_local.shape[2]
+    l, n = peer_b.shape[0], peer_b.shape[1]
+    rows = a_local.shape[0]
+    c_local = torch.empty((rows, n, comps), dtype=torch.float64, device=a_local.device)
+    if rows:
+        _cuda.gemm_dev(comps, _cuda.ALGO_SIMPLE if simple else _cuda.ALGO_BLOCK, n_min, rows, l,
+                       n, a_local.data_ptr(), l, peer_b.ptr, n, c_local.data_ptr(), n, False,
+                       nonfinite, torch.cuda.current_stream().cuda_stream)
     return c_local
 
 

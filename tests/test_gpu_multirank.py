@@ -78,7 +78,7 @@ def test_bench_two_ranks_json(gpu):
            "--master-addr=127.0.0.1", f"--master-port={_port()}",
            os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "3", "--warmup", "3",
            "--nmin", "32", "--size", "256", "--panel", "64", "--dist-backend", "gloo",
-           "--same-device", "--no-cpu-baseline", "--no-extras"]
+           "--same-device", "--no-cpu-baseline"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
@@ -88,6 +88,9 @@ def test_bench_two_ranks_json(gpu):
     # strong scaling: 3 steps x 4 k-panels x (domain scan, DFMA GEMM, gated Dekker GEMM)
     assert d["gpu_launches"] == 3 * 4 * 3 and d["scaling"] == "strong"
     assert d["config"]["m"] == 256 and d["roofline"]["frac"] > 0
+    # the peer-memory alternative to the broadcast (CUDA IPC between the
+    # two ranks' processes, same GPU here)
+    assert d["peer_mode"].get("value", 0) > 0, d["peer_mode"]
     # the reference arm under torchrun: rank 0 prints, the other exits 0
     cmd2 = cmd[:cmd.index("--gpus")] + ["--impl", "reference", "--gpus", "2", "--steps", "1",
                                         "--warmup", "0", "--size", "128", "--cpu-budget", "5"]
@@ -139,3 +142,47 @@ def test_two_ranks_strassen_products_equal_single_gpu_strassen(gpu, tmp_path, to
                               DenseMatrix(n, n, prec, b).to_device(), 64, 32).host_array()
     for rank in range(2):
         assert np.array_equal(np.load(f"{out}.{rank}.npy"), want)
+
+
+PEER_WORKER = r'''
+import os, sys
+sys.path.insert(0, os.environ["REPO"])
+import numpy as np, torch, torch.distributed as dist
+from paper_1710_01839_b200 import inputs, shard
+dist.init_process_group("gloo")
+r, w = dist.get_rank(), dist.get_world_size()
+torch.cuda.set_device(0)
+tok = os.environ["TOK"]
+m, l, n = 200, 150, 120
+a, b = inputs.gemm_inputs(tok, m, l, n, seed=9)
+lo, hi = shard.row_shards(m, w, align=64)[r]
+A = torch.from_numpy(np.ascontiguousarray(a[lo:hi])).cuda()
+B = torch.from_numpy(b).cuda() if r == 0 else None
+pb = shard.PeerOperand(B, src=0)
+assert (r == 0) == (B is not None) and pb.shape == b.shape
+C = shard.peer_matmul(A, pb, n_min=32)
+torch.cuda.synchronize()
+np.save(os.environ["OUT"] + f".{r}.npy", C.cpu().numpy())
+pb.close()
+dist.destroy_process_group()
+'''
+
+
+@pytest.mark.parametrize("tok", ["dd", "qd"])
+def test_two_ranks_peer_memory_operand(gpu, tmp_path, tok):
+    """B shared by CUDA IPC instead of broadcast: rank 1 maps rank 0's B
+    (another process's allocation on the same GPU here; a peer GPU over
+    NVLink on a multi-GPU box) and its GEMM reads B's tiles through the
+    mapping. The stitched C is bitwise the one-process product."""
+    import oracle
+    from paper_1710_01839_b200 import inputs
+    script = tmp_path / "p.py"
+    script.write_text(PEER_WORKER)
+    env = dict(os.environ, REPO=ROOT, TOK=tok, OUT=str(tmp_path / "c"))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", str(script)]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    c = np.concatenate([np.load(str(tmp_path / f"c.{k}.npy")) for k in range(2)], axis=0)
+    a, b = inputs.gemm_inputs(tok, 200, 150, 120, seed=9)
+    assert np.array_equal(c, oracle.matmul_simple(a, b))
