@@ -127,8 +127,12 @@ class DenseMatrix:
     # -- element access ------------------------------------------------------
 
     def get(self, i, j):
-        """Components of element (i, j) as a tuple of floats."""
-        return tuple(float(c) for c in self.host_array()[i, j])
+        """Element (i, j) as a Scalar (reference matrix.py:79-83); its
+        ``payload`` is the tuple of float components."""
+        from .scalar import Scalar
+        if self.is_device:
+            return Scalar(self.prec, self.data[i, j].cpu().tolist())
+        return Scalar(self.prec, self.data[i, j].tolist())
 
     def to_float_array(self):
         """Lossy double view (reference matrix.py:85-89)."""

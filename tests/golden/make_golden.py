@@ -265,9 +265,44 @@ def edge_cases():
     print("wrote edge_dd_strassen_big")
 
 
+def scalar_cases():
+    """The reference's host scalar algebra (scalar.py:95-251 over ddqd.py):
+    add/sub/mul/div/sqrt on seeded DD and QD pairs, and the literal
+    constructors, recorded for tests/test_host_logic.py."""
+    load_reference()
+    from mpmm.scalar import PrecisionSpec, Scalar, scalar_sqrt
+
+    sys.path.insert(0, REPO)
+    from paper_1710_01839_b200 import inputs
+
+    out = {}
+    for tok in ("dd", "qd"):
+        prec = PrecisionSpec.parse(tok)
+        a, b = inputs.gemm_inputs(tok, 1, 40, 1, seed=70)
+        xs = [Scalar(prec, tuple(float(c) for c in a[0, k])) for k in range(40)]
+        ys = [Scalar(prec, tuple(float(c) for c in b[k, 0])) for k in range(40)]
+        out[f"{tok}_x"] = np.array([x.payload for x in xs])
+        out[f"{tok}_y"] = np.array([y.payload for y in ys])
+        for name, fn in (("add", lambda x, y: x + y), ("sub", lambda x, y: x - y),
+                         ("mul", lambda x, y: x * y), ("div", lambda x, y: x / y)):
+            out[f"{tok}_{name}"] = np.array([fn(x, y).payload for x, y in zip(xs, ys)])
+        out[f"{tok}_sqrt"] = np.array([scalar_sqrt(x if x.payload[0] >= 0 else -x).payload
+                                       for x in xs])
+        out[f"{tok}_lits"] = np.array([Scalar.from_str("0.1", prec).payload,
+                                       Scalar.from_str("-3.14159265358979323846264338327950288",
+                                                       prec).payload,
+                                       Scalar.from_int(2 ** 60 + 1, prec).payload,
+                                       Scalar.from_int(-(3 ** 70), prec).payload])
+    np.savez(os.path.join(HERE, "scalar_ops.npz"), **out)
+    print("wrote scalar_ops", sorted(out))
+
+
 if __name__ == "__main__":
     if "--edge" in sys.argv:
         edge_cases()
+    elif "--scalar" in sys.argv:
+        scalar_cases()
     else:
         main()
         edge_cases()
+        scalar_cases()
