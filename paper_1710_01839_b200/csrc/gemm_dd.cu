@@ -9,7 +9,9 @@
 //   TILE_16    16x16 CTA tile, 1x1 per thread, 256 threads, 4 CTAs/SM
 //   TILE_32    32x32, 2x2, 256 threads, 2 CTAs/SM, k-tiles of 16
 //   TILE_LPT   persistent 64x64 (4x4) tiles in whole waves + 32x32 quarters
-//   TILE_32x64 32x64, 2x2, 512 threads
+//   TILE_32x64 32x64, 2x4, 256 threads, 2 CTAs/SM (0.6-0.8 % faster than
+//              TILE_32 in steady state -- fewer LDS per multiply-add --
+//              but a coarser wave quantum: profiles/r02_tile_variants2.log)
 //   TILE_64    64x64, 4x4, 256 threads, plain grid
 #include "gemm.cuh"
 
@@ -52,7 +54,7 @@ static cudaError_t dd_blocked(const GemmArgs& g) {
     case TILE_16: return launch_tiled<Ops, 16, 16, 16, 1, 1, 4>(g);
     case TILE_32: return launch_tiled<Ops, MPMM_DD32>(g);
     case TILE_64: return launch_tiled<Ops, 64, 64, 8, 4, 4, 1>(g);
-    case TILE_32x64: return launch_tiled<Ops, 32, 64, 8, 2, 2, 1>(g);
+    case TILE_32x64: return launch_tiled<Ops, 32, 64, 8, 2, 4, 2>(g);
     case TILE_LPT: return launch_lpt<Ops, MPMM_LPT_CFG>(g);
     default: return cudaErrorInvalidValue;
   }
@@ -90,7 +92,7 @@ cudaError_t dd_gemm_geometry(int algo, int tile, Geometry* geo) {
       case TILE_64: geo->bm = 64, geo->bn = 64;
         return occupancy_of(gemm_tiled<DDFastOps, 64, 64, 8, 4, 4, 1>, 256, geo);
       case TILE_32x64: geo->bm = 32, geo->bn = 64;
-        return occupancy_of(gemm_tiled<DDFastOps, 32, 64, 8, 2, 2, 1>, 512, geo);
+        return occupancy_of(gemm_tiled<DDFastOps, 32, 64, 8, 2, 4, 2>, 256, geo);
       case TILE_LPT: geo->bm = 64, geo->bn = 64;
         return occupancy_of(gemm_lpt<DDFastOps, MPMM_LPT_CFG>, 256, geo);
       default: return cudaErrorInvalidValue;
@@ -107,7 +109,7 @@ cudaError_t dd_gemm_geometry(int algo, int tile, Geometry* geo) {
     case TILE_64: geo->bm = 64, geo->bn = 64;
       return occupancy_of(gemm_tiled<DDOps, 64, 64, 8, 4, 4, 1>, 256, geo);
     case TILE_32x64: geo->bm = 32, geo->bn = 64;
-      return occupancy_of(gemm_tiled<DDOps, 32, 64, 8, 2, 2, 1>, 512, geo);
+      return occupancy_of(gemm_tiled<DDOps, 32, 64, 8, 2, 4, 2>, 256, geo);
     case TILE_LPT: geo->bm = 64, geo->bn = 64;
       return occupancy_of(gemm_lpt<DDOps, MPMM_LPT_CFG>, 256, geo);
     default: return cudaErrorInvalidValue;
