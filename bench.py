@@ -289,13 +289,30 @@ def fp64_peak(torch, _cuda, dev):
     return out
 
 
-def load_ncu_traffic(key):
+def load_ncu_traffic(*keys):
+    """DRAM bytes per launch of the first of ``keys`` present in the
+    committed ncu summary (profiles/ncu_summary.json), else None."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as fp:
-            return json.load(fp).get(key, {}).get("dram_bytes_per_launch")
+            summary = json.load(fp)
     except (OSError, ValueError):
         return None
+    for key in keys:
+        if key in summary:
+            return summary[key].get("dram_bytes_per_launch")
+    return None
+
+
+def kernel_label(_cuda, comps, n_min):
+    """The blocked kernel n_min selects, as its launch geometry."""
+    try:
+        g = _cuda.gemm_geometry(comps, _cuda.ALGO_BLOCK, n_min)
+        ops = "DDOps" if comps == 2 else "QDOps"
+        return (f"gemm_tiled<{ops}> blocked mirror, {g['tile_m']}x{g['tile_n']} CTA tile, "
+                f"{g['threads']} threads, {g['ctas_per_sm']} CTAs/SM (n_min={n_min})")
+    except Exception:  # noqa: BLE001 - a label only
+        return f"blocked mirror, n_min={n_min}"
 
 
 def timed(torch, fn, reps, flush=None, stream=None):
@@ -509,7 +526,10 @@ def run_ours(args, rank, world, local_rank):
     achieved = F * float(rows_max) * n * n / kernel_s / 1e12
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak,
-                "traffic": load_ncu_traffic(f"{args.prec}{n}"),
+                "traffic": load_ncu_traffic(f"{args.prec}{n}_nmin{args.nmin}"),
+                "traffic_source": "profiles/ncu_summary.json "
+                                  f"['{args.prec}{n}_nmin{args.nmin}'] (ncu --set full of "
+                                  "this launch, tools/prof_kernel.py)",
                 "peak_source": "nominal 148 SMs x 64 FP64 lanes x 2 flop x 1.965 GHz: "
                                "MEASURED_PEAKS.json has no FP64 entry and the profiling "
                                "guide states no FP64 fallback; the strictest denominator "
@@ -517,9 +537,7 @@ def run_ours(args, rank, world, local_rank):
                 "burst_dfma_tflops": burst["dfma"], "burst_dadd_tflops": burst["dadd"],
                 "frac_of_burst": achieved / burst["dfma"],
                 "flops_per_madd": F, "kernel_ms": kernel_s * 1e3,
-                "kernel": f"gemm_tiled<{args.prec.upper()}Ops,32,32,16,2,2,2> blocked mirror, "
-                          f"n_min={args.nmin}" if args.prec == "dd" else
-                          f"gemm_tiled<QDOps> blocked mirror, n_min={args.nmin}",
+                "kernel": kernel_label(_cuda, comps, args.nmin),
                 "fp64_issue_frac": (I_DD * 2 * float(rows_max) * n * n / kernel_s / 1e12 / peak)
                 if args.prec == "dd" else None}
     line = {
