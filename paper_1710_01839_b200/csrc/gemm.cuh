@@ -24,6 +24,9 @@
 // every SM ends within about one quarter tile of the others.
 #pragma once
 
+#include <mutex>
+#include <unordered_map>
+
 #include "common.cuh"
 #include "ddqd.cuh"
 #include "kernels.h"
@@ -93,6 +96,30 @@ __device__ __forceinline__ void grouped_tile(int t, int tiles_m, int tiles_n, in
   const int r = t % span;
   tm = first + r % rows;
   tn = r / rows;
+}
+
+// Kernels whose tiles need more than the 48 KB default of dynamic shared
+// memory opt in once per device (the attribute is per device: the native
+// multi-GPU runtime launches the same kernels on several).
+inline cudaError_t allow_smem_impl(const void* kern, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, uint64_t> done;   // kernel -> device bit mask
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  std::lock_guard<std::mutex> lock(mu);
+  uint64_t& mask = done[kern];
+  if (mask & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) mask |= bit;
+  return e;
+}
+
+template <class Kern>
+inline cudaError_t allow_smem(Kern kern, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  return allow_smem_impl(reinterpret_cast<const void*>(kern), bytes);
 }
 
 // Problem descriptor (pointers as double2 views, leading dims in elements).
@@ -305,6 +332,169 @@ __device__ __forceinline__ void gemm_tile(const Prob& pr, int m, int n, int l, i
 }
 
 // ---------------------------------------------------------------------------
+// Interior tiles (the whole BM x BN tile inside C, l a multiple of BK): the
+// same multiply-adds in the same order as gemm_tile, with the instruction
+// overhead around them cut down -- the kernel is bound by the FP64 pipe, and
+// every LDS / address / loop instruction takes issue and register-file
+// cycles from it.  Differences from gemm_tile:
+//   * no bounds predicates; the cp.async sources are per-thread pointers
+//     advanced once per k-tile, the destinations thread base + immediates;
+//   * ONE barrier per k-tile: wait for tile kt (issued a whole k-tile
+//     earlier), barrier, issue tile kt+1 into the buffer everybody finished
+//     reading before that barrier, compute tile kt;
+//   * the k loop steps UNROLL at a time through shared-memory addresses that
+//     are advanced, not recomputed; operand fetches are base + immediate.
+// ---------------------------------------------------------------------------
+
+#ifndef MPMM_INTERIOR
+#define MPMM_INTERIOR 1       // experiments: -DMPMM_INTERIOR=0 (tools/exp/build_variant.py)
+#endif
+#ifndef MPMM_INTERIOR_UNROLL
+#define MPMM_INTERIOR_UNROLL 4
+#endif
+
+__device__ __forceinline__ void cp_async16_at(uint32_t saddr, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem) : "memory");
+}
+
+__device__ __forceinline__ double2 lds_double2(uint32_t saddr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(saddr));
+  return v;
+}
+
+// whether gemm_tile_interior's copy mapping covers this configuration
+template <class Ops, int BM, int BN, int BK, int NT>
+struct InteriorOk {
+  static constexpr int V = Ops::V;
+  static constexpr bool value = MPMM_INTERIOR != 0 && NT % (BK * V) == 0 && NT % (BN * V) == 0 &&
+                                (BM * BK * V) % NT == 0 && (BK * BN * V) % NT == 0 &&
+                                BK % MPMM_INTERIOR_UNROLL == 0;
+};
+
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int NT>
+__device__ __forceinline__ void gemm_tile_interior(const Prob& pr, int l, int accumulate, int m0,
+                                                   int n0, double2* smem, bool& bad) {
+  constexpr int V = Ops::V;
+  constexpr int NTX = BN / TN, NTY = BM / TM;
+  constexpr int UNROLL = MPMM_INTERIOR_UNROLL;
+  static_assert(NTX * NTY == NT, "thread tile does not cover the CTA tile");
+  using S = TileSmem<Ops, BM, BN, BK>;
+  constexpr int AROWS = NT / (BK * V);          // A rows covered by one pass of the CTA's copies
+  constexpr int BROWS = NT / (BN * V);
+  constexpr int ACH = BM / AROWS, BCH = BK / BROWS;   // 16-byte chunks per thread and k-tile
+  constexpr uint32_t A_STAGE_B = S::A_STAGE * 16, B_STAGE_B = S::B_STAGE * 16;
+  const int tid = threadIdx.x;
+  const int tx = tid % NTX, ty = tid / NTX;
+
+  double acc[TM][TN][Ops::NACC];
+#pragma unroll
+  for (int r = 0; r < TM; ++r)
+#pragma unroll
+    for (int c = 0; c < TN; ++c) {
+      const int i = m0 + ty + r * NTY, j = n0 + tx + c * NTX;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        double2 x = accumulate ? __ldcg(pr.C + ((int64_t)i * pr.ldc + j) * V + v)
+                               : make_double2(0.0, 0.0);
+        acc[r][c][2 * v] = x.x;
+        acc[r][c][2 * v + 1] = x.y;
+      }
+    }
+
+  // copies: thread -> (row, 16-byte column) of the A and B k-tiles
+  const int arow = tid / (BK * V), acol = tid % (BK * V);
+  const int brow = tid / (BN * V), bcol = tid % (BN * V);
+  const double2* asrc = pr.A + (int64_t)(m0 + arow) * pr.lda * V + acol;
+  const double2* bsrc = pr.B + ((int64_t)brow * pr.ldb + n0) * V + bcol;
+  const int64_t astep = (int64_t)AROWS * pr.lda * V;
+  const int64_t bstep = (int64_t)BROWS * pr.ldb * V;
+  const int64_t bnext = (int64_t)BK * pr.ldb * V;
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const uint32_t adst = sbase + (arow * (BK + 1) * V + acol) * 16;
+  const uint32_t bdst = sbase + 2 * A_STAGE_B + (brow * BN * V + bcol) * 16;
+  auto load = [&](int st) {
+#pragma unroll
+    for (int i = 0; i < ACH; ++i)
+      cp_async16_at(adst + st * A_STAGE_B + i * (AROWS * (BK + 1) * V * 16), asrc + i * astep);
+#pragma unroll
+    for (int i = 0; i < BCH; ++i)
+      cp_async16_at(bdst + st * B_STAGE_B + i * (BROWS * BN * V * 16), bsrc + i * bstep);
+    asrc += BK * V;
+    bsrc += bnext;
+  };
+  // operand fetches: thread base + immediates
+  const uint32_t ard = sbase + ty * ((BK + 1) * V * 16);
+  const uint32_t brd = sbase + 2 * A_STAGE_B + tx * (V * 16);
+
+  const int ktiles = l / BK;
+  load(0);
+  cp_async_commit();
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int st = kt & 1;
+    cp_async_wait<0>();
+    __syncthreads();
+    if (kt + 1 < ktiles) {
+      load(st ^ 1);
+      cp_async_commit();
+    }
+    uint32_t ap = ard + st * A_STAGE_B, bp = brd + st * B_STAGE_B;
+    const uint32_t aend = ap + BK * V * 16;
+#pragma unroll 1
+    do {
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        double2 a[TM][V], b[TN][V];
+#pragma unroll
+        for (int r = 0; r < TM; ++r)
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            a[r][v] = lds_double2(ap + ((r * NTY * (BK + 1) + u) * V + v) * 16);
+#pragma unroll
+        for (int c = 0; c < TN; ++c)
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            b[c][v] = lds_double2(bp + ((u * BN + c * NTX) * V + v) * 16);
+#pragma unroll
+        for (int r = 0; r < TM; ++r)
+#pragma unroll
+          for (int c = 0; c < TN; ++c) Ops::madd(acc[r][c], a[r], b[c]);
+      }
+      ap += UNROLL * V * 16;
+      bp += UNROLL * BN * V * 16;
+    } while (ap != aend);
+  }
+  __syncthreads();   // the buffers are free for the CTA's next tile
+
+#pragma unroll
+  for (int r = 0; r < TM; ++r)
+#pragma unroll
+    for (int c = 0; c < TN; ++c) {
+      const int i = m0 + ty + r * NTY, j = n0 + tx + c * NTX;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        pr.C[((int64_t)i * pr.ldc + j) * V + v] =
+            make_double2(acc[r][c][2 * v], acc[r][c][2 * v + 1]);
+        bad |= !finite2(acc[r][c][2 * v], acc[r][c][2 * v + 1]);
+      }
+    }
+}
+
+// gemm_tile, through the interior path when the tile qualifies (uniform per
+// CTA, so the barriers inside never diverge)
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int NT>
+__device__ __forceinline__ void gemm_tile_any(const Prob& pr, int m, int n, int l, int accumulate,
+                                              int m0, int n0, double2* smem, bool& bad) {
+  if constexpr (InteriorOk<Ops, BM, BN, BK, NT>::value) {
+    if (m0 + BM <= m && n0 + BN <= n && l >= BK && l % BK == 0) {
+      gemm_tile_interior<Ops, BM, BN, BK, TM, TN, NT>(pr, l, accumulate, m0, n0, smem, bad);
+      return;
+    }
+  }
+  gemm_tile<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, m0, n0, smem, bad);
+}
+
+// ---------------------------------------------------------------------------
 // Strassen leaves with their operand sums folded into the tile loads
 // (multiply.py:313-321): the left operand is X + sa*Y (sa = +-1; 0: X alone)
 // and the right one Z + sb*W, each sum the reference's ewise add/sub
@@ -502,9 +692,7 @@ template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB>
 cudaError_t launch_tiled_sum(const GemmArgs& g) {
   auto kern = gemm_tiled_sum<Ops, BM, BN, BK, TM, TN, MINB>;
   constexpr size_t bytes = SumSmem<Ops, BM, BN, BK>::TOTAL * sizeof(double2);
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (attr != cudaSuccess) return attr;
+  if (cudaError_t attr = allow_smem(kern, bytes); attr != cudaSuccess) return attr;
   int64_t tiles = (int64_t)((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN) * g.batch;
   if (tiles == 0) return cudaSuccess;
   if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
@@ -522,7 +710,7 @@ gemm_tiled(const GemmProblem* __restrict__ probs, Prob single, int m, int n, int
            int accumulate, int* __restrict__ nonfinite, const KReady kr,
            const DomainGate gate) {
   constexpr int NT = (BM / TM) * (BN / TN);
-  __shared__ __align__(16) double2 smem[TileSmem<Ops, BM, BN, BK>::TOTAL];
+  extern __shared__ __align__(16) double2 smem[];   // TileSmem<Ops, BM, BN, BK>::TOTAL
   if (gate_skip(gate)) return;
   const int tiles_n = (n + BN - 1) / BN, tiles_m = (m + BM - 1) / BM;
   const int per = tiles_m * tiles_n;
@@ -531,8 +719,12 @@ gemm_tiled(const GemmProblem* __restrict__ probs, Prob single, int m, int n, int
   bool bad = false;
   int tm, tn;
   grouped_tile(t, tiles_m, tiles_n, tm, tn);
-  gemm_tile<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, tm * BM, tn * BN, smem, bad,
-                                         STREAM ? kr : KReady{nullptr, 0});
+  if constexpr (STREAM)
+    gemm_tile<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, tm * BM, tn * BN, smem, bad,
+                                           kr);
+  else
+    gemm_tile_any<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, tm * BM, tn * BN, smem,
+                                               bad);
   if (nonfinite != nullptr && bad) atomicOr(nonfinite, 1);
 }
 
@@ -579,8 +771,7 @@ cudaError_t launch_persist(const GemmArgs& g) {
   int dev = 0, sms = 0, occ = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) e = allow_smem(kern, bytes);
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, bytes);
   if (e != cudaSuccess) return e;
   const int64_t tiles = (int64_t)((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN) * g.batch;
@@ -601,7 +792,7 @@ gemm_lpt(const GemmProblem* __restrict__ probs, Prob single, int P, int m, int n
          int accumulate, int* __restrict__ nonfinite, const DomainGate gate) {
   constexpr int NT = (BM / TM) * (BN / TN);
   static_assert(TM % 2 == 0 && TN % 2 == 0, "quarter tiles need even thread tiles");
-  __shared__ __align__(16) double2 smem[TileSmem<Ops, BM, BN, BK>::TOTAL];
+  extern __shared__ __align__(16) double2 smem[];   // TileSmem<Ops, BM, BN, BK>::TOTAL
   if (gate_skip(gate)) return;
   const int tiles_n = (n + BN - 1) / BN, tiles_m = (m + BM - 1) / BM;
   const int per = tiles_m * tiles_n;
@@ -624,13 +815,13 @@ gemm_lpt(const GemmProblem* __restrict__ probs, Prob single, int P, int m, int n
     grouped_tile(tt, tiles_m, tiles_n, tm, tn);
     int m0 = tm * BM, n0 = tn * BN;
     if (q < 0) {
-      gemm_tile<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, m0, n0, smem, bad);
+      gemm_tile_any<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, m0, n0, smem, bad);
     } else {
       m0 += (q / 2) * (BM / 2);
       n0 += (q % 2) * (BN / 2);
       if (m0 < m && n0 < n)  // uniform per CTA: no divergent barriers
-        gemm_tile<Ops, BM / 2, BN / 2, BK, TM / 2, TN / 2, NT>(pr, m, n, l, accumulate, m0, n0,
-                                                              smem, bad);
+        gemm_tile_any<Ops, BM / 2, BN / 2, BK, TM / 2, TN / 2, NT>(pr, m, n, l, accumulate, m0,
+                                                                  n0, smem, bad);
     }
   }
   if (nonfinite != nullptr && bad) atomicOr(nonfinite, 1);
@@ -692,13 +883,19 @@ cudaError_t launch_tiled(const GemmArgs& g) {
   if (tiles == 0) return cudaSuccess;
   if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
   const unsigned grid = (unsigned)tiles, nt = (BM / TM) * (BN / TN);
+  constexpr size_t bytes = TileSmem<Ops, BM, BN, BK>::TOTAL * sizeof(double2);
   const KReady kr{g.kready, g.kpanel, g.ktile_rows, g.ktile_cols, g.ka_panels};
-  if (g.kready != nullptr)
-    gemm_tiled<Ops, BM, BN, BK, TM, TN, MINB, true><<<grid, nt, 0, g.stream>>>(
-        g.probs, single_prob(g), g.m, g.n, g.l, g.accumulate, g.nonfinite, kr, g.gate);
-  else
-    gemm_tiled<Ops, BM, BN, BK, TM, TN, MINB, false><<<grid, nt, 0, g.stream>>>(
-        g.probs, single_prob(g), g.m, g.n, g.l, g.accumulate, g.nonfinite, kr, g.gate);
+  if (g.kready != nullptr) {
+    auto kern = gemm_tiled<Ops, BM, BN, BK, TM, TN, MINB, true>;
+    if (cudaError_t e = allow_smem(kern, bytes); e != cudaSuccess) return e;
+    kern<<<grid, nt, bytes, g.stream>>>(g.probs, single_prob(g), g.m, g.n, g.l, g.accumulate,
+                                        g.nonfinite, kr, g.gate);
+  } else {
+    auto kern = gemm_tiled<Ops, BM, BN, BK, TM, TN, MINB, false>;
+    if (cudaError_t e = allow_smem(kern, bytes); e != cudaSuccess) return e;
+    kern<<<grid, nt, bytes, g.stream>>>(g.probs, single_prob(g), g.m, g.n, g.l, g.accumulate,
+                                        g.nonfinite, kr, g.gate);
+  }
   return cudaGetLastError();
 }
 
@@ -706,10 +903,12 @@ template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB>
 cudaError_t launch_lpt(const GemmArgs& g) {
   auto kern = gemm_lpt<Ops, BM, BN, BK, TM, TN, MINB>;
   constexpr int NT = (BM / TM) * (BN / TN);
+  constexpr size_t bytes = TileSmem<Ops, BM, BN, BK>::TOTAL * sizeof(double2);
   int dev = 0, sms = 0, occ = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, 0);
+  if (e == cudaSuccess) e = allow_smem(kern, bytes);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, bytes);
   if (e != cudaSuccess) return e;
   int64_t tiles = (int64_t)((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN) * g.batch;
   if (tiles == 0) return cudaSuccess;
@@ -718,8 +917,8 @@ cudaError_t launch_lpt(const GemmArgs& g) {
   // fewer units than slots: launch one CTA per unit (all quarter tiles)
   int64_t units = tiles < slots ? 4 * tiles : slots;
   int grid = (int)(units < slots ? units : slots);
-  kern<<<grid, NT, 0, g.stream>>>(g.probs, single_prob(g), g.batch, g.m, g.n, g.l,
-                                  g.accumulate, g.nonfinite, g.gate);
+  kern<<<grid, NT, bytes, g.stream>>>(g.probs, single_prob(g), g.batch, g.m, g.n, g.l,
+                                      g.accumulate, g.nonfinite, g.gate);
   return cudaGetLastError();
 }
 
@@ -733,9 +932,26 @@ cudaError_t launch_simple(const GemmArgs& g) {
 }
 
 template <class Kern>
-cudaError_t occupancy_of(Kern kern, int threads, Geometry* geo) {
+cudaError_t occupancy_of(Kern kern, int threads, Geometry* geo, size_t smem_bytes = 0) {
   geo->threads = threads;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&geo->ctas_per_sm, kern, threads, 0);
+  if (cudaError_t e = allow_smem(kern, smem_bytes); e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&geo->ctas_per_sm, kern, threads,
+                                                       smem_bytes);
+}
+
+// CTA tile and residency of a gemm_tiled / gemm_lpt configuration
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB>
+cudaError_t tiled_geometry(Geometry* geo) {
+  geo->bm = BM, geo->bn = BN;
+  return occupancy_of(gemm_tiled<Ops, BM, BN, BK, TM, TN, MINB, false>, (BM / TM) * (BN / TN), geo,
+                      TileSmem<Ops, BM, BN, BK>::TOTAL * sizeof(double2));
+}
+
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB>
+cudaError_t lpt_geometry(Geometry* geo) {
+  geo->bm = BM, geo->bn = BN;
+  return occupancy_of(gemm_lpt<Ops, BM, BN, BK, TM, TN, MINB>, (BM / TM) * (BN / TN), geo,
+                      TileSmem<Ops, BM, BN, BK>::TOTAL * sizeof(double2));
 }
 
 }  // namespace mpmm

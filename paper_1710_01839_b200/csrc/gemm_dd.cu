@@ -15,35 +15,31 @@
 //   TILE_64    64x64, 4x4, 256 threads, plain grid
 #include "gemm.cuh"
 
-// TILE_32's configuration can be overridden at build time (experiments:
-// tools/exp/build_variant.py -DMPMM_DD32_CFG=i).
-#if !defined(MPMM_DD32_CFG) || MPMM_DD32_CFG == 0
-#define MPMM_DD32 32, 32, 16, 2, 2, 2
-#elif MPMM_DD32_CFG == 1
-#define MPMM_DD32 32, 32, 8, 2, 2, 2
-#elif MPMM_DD32_CFG == 2
-#define MPMM_DD32 32, 64, 8, 2, 4, 1
-#elif MPMM_DD32_CFG == 3
-#define MPMM_DD32 64, 32, 8, 4, 2, 1
-#elif MPMM_DD32_CFG == 4
-#define MPMM_DD32 32, 32, 16, 1, 4, 2
-#elif MPMM_DD32_CFG == 5
-#define MPMM_DD32 32, 32, 16, 4, 1, 2
-#elif MPMM_DD32_CFG == 6
-#define MPMM_DD32 32, 64, 8, 2, 4, 2
+// Experiments select another set at build time (tools/exp/build_variant.py
+// -DMPMM_DDCFG=i; nvcc splits -D values at commas, hence the index).
+#if defined(MPMM_DDCFG) && MPMM_DDCFG == 1
+#define MPMM_DD32 32, 32, 32, 2, 2, 2
+#define MPMM_DD32x64 32, 64, 16, 2, 4, 2
+#define MPMM_DD64 64, 64, 16, 4, 4, 1
+#elif defined(MPMM_DDCFG) && MPMM_DDCFG == 2
+#define MPMM_DD32 64, 32, 16, 4, 2, 2
+#define MPMM_DD32x64 32, 64, 32, 2, 4, 2
+#define MPMM_DD64 64, 64, 32, 4, 4, 1
 #endif
-
-// TILE_LPT's configuration (experiments: -DMPMM_LPT_VAR=i)
-#if !defined(MPMM_LPT_VAR) || MPMM_LPT_VAR == 0
-#define MPMM_LPT_CFG 64, 64, 8, 4, 4, 1
-#elif MPMM_LPT_VAR == 1
-#define MPMM_LPT_CFG 64, 64, 8, 4, 4, 2
-#elif MPMM_LPT_VAR == 2
-#define MPMM_LPT_CFG 64, 64, 16, 4, 4, 2
-#elif MPMM_LPT_VAR == 3
-#define MPMM_LPT_CFG 64, 32, 8, 4, 2, 2
-#elif MPMM_LPT_VAR == 4
-#define MPMM_LPT_CFG 32, 64, 8, 2, 4, 2
+#ifndef MPMM_DD16
+#define MPMM_DD16 16, 16, 16, 1, 1, 4
+#endif
+#ifndef MPMM_DD32
+#define MPMM_DD32 32, 32, 16, 2, 2, 2
+#endif
+#ifndef MPMM_DD64
+#define MPMM_DD64 64, 64, 8, 4, 4, 1
+#endif
+#ifndef MPMM_DD32x64
+#define MPMM_DD32x64 32, 64, 8, 2, 4, 2
+#endif
+#ifndef MPMM_DDLPT
+#define MPMM_DDLPT 64, 64, 8, 4, 4, 1
 #endif
 
 namespace mpmm {
@@ -51,23 +47,26 @@ namespace mpmm {
 template <class Ops>
 static cudaError_t dd_blocked(const GemmArgs& g) {
   switch (g.tile) {
-    case TILE_16: return launch_tiled<Ops, 16, 16, 16, 1, 1, 4>(g);
+    case TILE_16: return launch_tiled<Ops, MPMM_DD16>(g);
     case TILE_32: return launch_tiled<Ops, MPMM_DD32>(g);
-    case TILE_64: return launch_tiled<Ops, 64, 64, 8, 4, 4, 1>(g);
-    case TILE_32x64: return launch_tiled<Ops, 32, 64, 8, 2, 4, 2>(g);
-    case TILE_LPT: return launch_lpt<Ops, MPMM_LPT_CFG>(g);
+    case TILE_64: return launch_tiled<Ops, MPMM_DD64>(g);
+    case TILE_32x64: return launch_tiled<Ops, MPMM_DD32x64>(g);
+    case TILE_LPT: return launch_lpt<Ops, MPMM_DDLPT>(g);
     default: return cudaErrorInvalidValue;
   }
 }
 
-template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB>
-static cudaError_t dd_geometry(Geometry* geo) {
-  geo->bm = BM, geo->bn = BN;
-  return occupancy_of(gemm_tiled<Ops, BM, BN, BK, TM, TN, MINB>, (BM / TM) * (BN / TN), geo);
-}
-
 template <class Ops>
-static cudaError_t dd32_geometry(Geometry* geo) { return dd_geometry<Ops, MPMM_DD32>(geo); }
+static cudaError_t dd_blocked_geometry(int tile, Geometry* geo) {
+  switch (tile) {
+    case TILE_16: return tiled_geometry<Ops, MPMM_DD16>(geo);
+    case TILE_32: return tiled_geometry<Ops, MPMM_DD32>(geo);
+    case TILE_64: return tiled_geometry<Ops, MPMM_DD64>(geo);
+    case TILE_32x64: return tiled_geometry<Ops, MPMM_DD32x64>(geo);
+    case TILE_LPT: return lpt_geometry<Ops, MPMM_DDLPT>(geo);
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 cudaError_t dd_gemm_launch(const GemmArgs& g) {
   if (g.m <= 0 || g.n <= 0 || g.batch <= 0) return cudaSuccess;
@@ -84,36 +83,12 @@ cudaError_t dd_dekker_launch(const GemmArgs& g) {
 }
 
 cudaError_t dd_gemm_geometry(int algo, int tile, Geometry* geo) {
-  if (algo == ALGO_BLOCK_FAST) {
-    switch (tile) {
-      case TILE_16: geo->bm = 16, geo->bn = 16;
-        return occupancy_of(gemm_tiled<DDFastOps, 16, 16, 16, 1, 1, 4>, 256, geo);
-      case TILE_32: return dd32_geometry<DDFastOps>(geo);
-      case TILE_64: geo->bm = 64, geo->bn = 64;
-        return occupancy_of(gemm_tiled<DDFastOps, 64, 64, 8, 4, 4, 1>, 256, geo);
-      case TILE_32x64: geo->bm = 32, geo->bn = 64;
-        return occupancy_of(gemm_tiled<DDFastOps, 32, 64, 8, 2, 4, 2>, 256, geo);
-      case TILE_LPT: geo->bm = 64, geo->bn = 64;
-        return occupancy_of(gemm_lpt<DDFastOps, MPMM_LPT_CFG>, 256, geo);
-      default: return cudaErrorInvalidValue;
-    }
-  }
   if (algo == ALGO_SIMPLE) {
     geo->bm = 8, geo->bn = 32;
     return occupancy_of(gemm_simple<DDOps>, 256, geo);
   }
-  switch (tile) {
-    case TILE_16: geo->bm = 16, geo->bn = 16;
-      return occupancy_of(gemm_tiled<DDOps, 16, 16, 16, 1, 1, 4>, 256, geo);
-    case TILE_32: return dd32_geometry<DDOps>(geo);
-    case TILE_64: geo->bm = 64, geo->bn = 64;
-      return occupancy_of(gemm_tiled<DDOps, 64, 64, 8, 4, 4, 1>, 256, geo);
-    case TILE_32x64: geo->bm = 32, geo->bn = 64;
-      return occupancy_of(gemm_tiled<DDOps, 32, 64, 8, 2, 4, 2>, 256, geo);
-    case TILE_LPT: geo->bm = 64, geo->bn = 64;
-      return occupancy_of(gemm_lpt<DDOps, MPMM_LPT_CFG>, 256, geo);
-    default: return cudaErrorInvalidValue;
-  }
+  if (algo == ALGO_BLOCK_FAST) return dd_blocked_geometry<DDFastOps>(tile, geo);
+  return dd_blocked_geometry<DDOps>(tile, geo);
 }
 
 }  // namespace mpmm

@@ -15,6 +15,12 @@
 //   TILE_64    16x16, 1x1, 256 threads, 3 CTAs/SM
 #include "gemm.cuh"
 
+#define MPMM_QD16 16, 16, 8, 1, 1, 2
+#define MPMM_QD32 8, 16, 8, 1, 1, 4
+#define MPMM_QD64 16, 16, 8, 1, 1, 3
+#define MPMM_QD32x64 8, 32, 8, 1, 1, 2
+#define MPMM_QDLPT 16, 16, 16, 1, 1, 2
+
 namespace mpmm {
 
 cudaError_t qd_gemm_launch(const GemmArgs& g) {
@@ -23,11 +29,11 @@ cudaError_t qd_gemm_launch(const GemmArgs& g) {
   if (g.algo == ALGO_SIMPLE) return launch_simple<QDOps>(g);
   if (g.algo != ALGO_BLOCK) return cudaErrorNotSupported;
   switch (g.tile) {
-    case TILE_16: return launch_tiled<QDOps, 16, 16, 8, 1, 1, 2>(g);
-    case TILE_32: return launch_tiled<QDOps, 8, 16, 8, 1, 1, 4>(g);
-    case TILE_64: return launch_tiled<QDOps, 16, 16, 8, 1, 1, 3>(g);
-    case TILE_32x64: return launch_tiled<QDOps, 8, 32, 8, 1, 1, 2>(g);
-    case TILE_LPT: return launch_tiled<QDOps, 16, 16, 16, 1, 1, 2>(g);
+    case TILE_16: return launch_tiled<QDOps, MPMM_QD16>(g);
+    case TILE_32: return launch_tiled<QDOps, MPMM_QD32>(g);
+    case TILE_64: return launch_tiled<QDOps, MPMM_QD64>(g);
+    case TILE_32x64: return launch_tiled<QDOps, MPMM_QD32x64>(g);
+    case TILE_LPT: return launch_tiled<QDOps, MPMM_QDLPT>(g);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -44,16 +50,11 @@ cudaError_t qd_gemm_geometry(int algo, int tile, Geometry* geo) {
     return occupancy_of(gemm_simple<QDOps>, 256, geo);
   }
   switch (tile) {
-    case TILE_16: geo->bm = 16, geo->bn = 16;
-      return occupancy_of(gemm_tiled<QDOps, 16, 16, 8, 1, 1, 2>, 256, geo);
-    case TILE_32: geo->bm = 8, geo->bn = 16;
-      return occupancy_of(gemm_tiled<QDOps, 8, 16, 8, 1, 1, 4>, 128, geo);
-    case TILE_64: geo->bm = 16, geo->bn = 16;
-      return occupancy_of(gemm_tiled<QDOps, 16, 16, 8, 1, 1, 3>, 256, geo);
-    case TILE_32x64: geo->bm = 8, geo->bn = 32;
-      return occupancy_of(gemm_tiled<QDOps, 8, 32, 8, 1, 1, 2>, 256, geo);
-    case TILE_LPT: geo->bm = 16, geo->bn = 16;
-      return occupancy_of(gemm_tiled<QDOps, 16, 16, 16, 1, 1, 2>, 256, geo);
+    case TILE_16: return tiled_geometry<QDOps, MPMM_QD16>(geo);
+    case TILE_32: return tiled_geometry<QDOps, MPMM_QD32>(geo);
+    case TILE_64: return tiled_geometry<QDOps, MPMM_QD64>(geo);
+    case TILE_32x64: return tiled_geometry<QDOps, MPMM_QD32x64>(geo);
+    case TILE_LPT: return tiled_geometry<QDOps, MPMM_QDLPT>(geo);
     default: return cudaErrorInvalidValue;
   }
 }

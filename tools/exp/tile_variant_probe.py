@@ -12,7 +12,7 @@ for n, reps in ((1024, 20), (2048, 5), (8192, 1)):
     a, b = inputs.gemm_inputs_device("dd", n, n, n, seed=1)
     c = torch.empty_like(a)
     s = torch.cuda.current_stream().cuda_stream
-    for nm in (32, 64):
+    for nm in [int(x) for x in os.environ.get('MPMM_PROBE_NMIN', '32,64').split(',')]:
         run = lambda: _cuda.gemm_dev(2, _cuda.ALGO_BLOCK, nm, n, n, n, a.data_ptr(), n,
                                      b.data_ptr(), n, c.data_ptr(), n, False, None, s)
         run(); torch.cuda.synchronize()
