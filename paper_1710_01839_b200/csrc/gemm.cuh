@@ -372,9 +372,10 @@ struct InteriorOk {
                                 BK % MPMM_INTERIOR_UNROLL == 0;
 };
 
-template <class Ops, int BM, int BN, int BK, int TM, int TN, int NT>
-__device__ __forceinline__ void gemm_tile_interior(const Prob& pr, int l, int accumulate, int m0,
-                                                   int n0, double2* smem, bool& bad) {
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int NT, bool STREAM = false>
+__device__ __forceinline__ void gemm_tile_interior(const Prob& pr, int m, int n, int l,
+                                                   int accumulate, int m0, int n0, double2* smem,
+                                                   bool& bad, const KReady kr = KReady{nullptr, 0}) {
   constexpr int V = Ops::V;
   constexpr int NTX = BN / TN, NTY = BM / TM;
   constexpr int UNROLL = MPMM_INTERIOR_UNROLL;
@@ -428,6 +429,11 @@ __device__ __forceinline__ void gemm_tile_interior(const Prob& pr, int l, int ac
   const uint32_t brd = sbase + 2 * A_STAGE_B + tx * (V * 16);
 
   const int ktiles = l / BK;
+  int seen = -1;   // highest k-panel known to have landed (streamed operands)
+  if constexpr (STREAM) {
+    wait_tile_panels(kr, m0, n0, m, n, BM, BN);
+    wait_k_panel(kr, 0, seen);
+  }
   load(0);
   cp_async_commit();
   for (int kt = 0; kt < ktiles; ++kt) {
@@ -435,6 +441,7 @@ __device__ __forceinline__ void gemm_tile_interior(const Prob& pr, int l, int ac
     cp_async_wait<0>();
     __syncthreads();
     if (kt + 1 < ktiles) {
+      if constexpr (STREAM) wait_k_panel(kr, (kt + 1) * BK, seen);
       load(st ^ 1);
       cp_async_commit();
     }
@@ -482,16 +489,18 @@ __device__ __forceinline__ void gemm_tile_interior(const Prob& pr, int l, int ac
 
 // gemm_tile, through the interior path when the tile qualifies (uniform per
 // CTA, so the barriers inside never diverge)
-template <class Ops, int BM, int BN, int BK, int TM, int TN, int NT>
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int NT, bool STREAM = false>
 __device__ __forceinline__ void gemm_tile_any(const Prob& pr, int m, int n, int l, int accumulate,
-                                              int m0, int n0, double2* smem, bool& bad) {
+                                              int m0, int n0, double2* smem, bool& bad,
+                                              const KReady kr = KReady{nullptr, 0}) {
   if constexpr (InteriorOk<Ops, BM, BN, BK, NT>::value) {
     if (m0 + BM <= m && n0 + BN <= n && l >= BK && l % BK == 0) {
-      gemm_tile_interior<Ops, BM, BN, BK, TM, TN, NT>(pr, l, accumulate, m0, n0, smem, bad);
+      gemm_tile_interior<Ops, BM, BN, BK, TM, TN, NT, STREAM>(pr, m, n, l, accumulate, m0, n0,
+                                                              smem, bad, kr);
       return;
     }
   }
-  gemm_tile<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, m0, n0, smem, bad);
+  gemm_tile<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, m0, n0, smem, bad, kr);
 }
 
 // ---------------------------------------------------------------------------
@@ -719,12 +728,8 @@ gemm_tiled(const GemmProblem* __restrict__ probs, Prob single, int m, int n, int
   bool bad = false;
   int tm, tn;
   grouped_tile(t, tiles_m, tiles_n, tm, tn);
-  if constexpr (STREAM)
-    gemm_tile<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, tm * BM, tn * BN, smem, bad,
-                                           kr);
-  else
-    gemm_tile_any<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, tm * BM, tn * BN, smem,
-                                               bad);
+  gemm_tile_any<Ops, BM, BN, BK, TM, TN, NT, STREAM>(pr, m, n, l, accumulate, tm * BM, tn * BN,
+                                                     smem, bad, STREAM ? kr : KReady{nullptr, 0});
   if (nonfinite != nullptr && bad) atomicOr(nonfinite, 1);
 }
 

@@ -19,7 +19,7 @@
 // -DMPMM_DDCFG=i; nvcc splits -D values at commas, hence the index).
 #if defined(MPMM_DDCFG) && MPMM_DDCFG == 1
 #define MPMM_DD32 32, 32, 32, 2, 2, 2
-#define MPMM_DD32x64 32, 64, 16, 2, 4, 2
+#define MPMM_DD32x64 32, 64, 8, 2, 4, 2
 #define MPMM_DD64 64, 64, 16, 4, 4, 1
 #elif defined(MPMM_DDCFG) && MPMM_DDCFG == 2
 #define MPMM_DD32 64, 32, 16, 4, 2, 2
@@ -36,7 +36,7 @@
 #define MPMM_DD64 64, 64, 8, 4, 4, 1
 #endif
 #ifndef MPMM_DD32x64
-#define MPMM_DD32x64 32, 64, 8, 2, 4, 2
+#define MPMM_DD32x64 32, 64, 16, 2, 4, 2
 #endif
 #ifndef MPMM_DDLPT
 #define MPMM_DDLPT 64, 64, 8, 4, 4, 1
