@@ -679,6 +679,160 @@ __device__ __forceinline__ void gemm_tile_sum(const SumProb& pr, int m, int n, i
     }
 }
 
+// gemm_tile_sum for interior tiles: the pipeline of gemm_tile_interior (one
+// barrier per k-tile, advanced addresses, no predicates) with the operand
+// sums formed on each thread's own staged elements before that barrier.
+template <class Ops, int BM, int BN, int BK, int NT>
+struct SumInteriorOk {
+  static constexpr bool value = MPMM_INTERIOR != 0 && NT % BK == 0 && NT % BN == 0 &&
+                                (BM * BK) % NT == 0 && (BK * BN) % NT == 0 &&
+                                BK % MPMM_INTERIOR_UNROLL == 0;
+};
+
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int NT>
+__device__ __forceinline__ void gemm_tile_sum_interior(const SumProb& pr, int l, int m0, int n0,
+                                                       double2* smem, bool& bad) {
+  constexpr int V = Ops::V;
+  constexpr int NTX = BN / TN, NTY = BM / TM;
+  constexpr int UNROLL = MPMM_INTERIOR_UNROLL;
+  using S = TileSmem<Ops, BM, BN, BK>;
+  constexpr int AROWS = NT / BK, BROWS = NT / BN;       // rows per pass of the CTA's copies
+  constexpr int AEL = BM / AROWS, BEL = BK / BROWS;     // elements per thread and k-tile
+  constexpr uint32_t A_STAGE_B = S::A_STAGE * 16, B_STAGE_B = S::B_STAGE * 16;
+  constexpr uint32_t Y_OFF_B = S::TOTAL * 16;           // staging of the second summands
+  const int tid = threadIdx.x;
+  const int tx = tid % NTX, ty = tid / NTX;
+
+  double acc[TM][TN][Ops::NACC];
+#pragma unroll
+  for (int r = 0; r < TM; ++r)
+#pragma unroll
+    for (int c = 0; c < TN; ++c)
+#pragma unroll
+      for (int q = 0; q < Ops::NACC; ++q) acc[r][c][q] = 0.0;
+
+  // copies: thread -> (row, element column) of the A and B k-tiles
+  const int arow = tid / BK, acol = tid % BK;
+  const int brow = tid / BN, bcol = tid % BN;
+  const int64_t aoff = ((int64_t)(m0 + arow) * pr.lda + acol) * V;
+  const int64_t boff = ((int64_t)brow * pr.ldb + n0 + bcol) * V;
+  const double2* asrc = pr.A + aoff;
+  const double2* a2src = pr.A2 + aoff;
+  const double2* bsrc = pr.B + boff;
+  const double2* b2src = pr.B2 + boff;
+  const int64_t astep = (int64_t)AROWS * pr.lda * V;
+  const int64_t bstep = (int64_t)BROWS * pr.ldb * V;
+  const int64_t bnext = (int64_t)BK * pr.ldb * V;
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const int aidx = (arow * (BK + 1) + acol) * V;                   // in double2
+  const int bidx = 2 * S::A_STAGE + (brow * BN + bcol) * V;
+  const bool sa = pr.sa != 0, sb = pr.sb != 0;
+  auto load = [&](int st) {
+#pragma unroll
+    for (int i = 0; i < AEL; ++i)
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const uint32_t d = sbase + (aidx + st * S::A_STAGE + i * AROWS * (BK + 1) * V + v) * 16;
+        cp_async16_at(d, asrc + i * astep + v);
+        if (sa) cp_async16_at(d + Y_OFF_B, a2src + i * astep + v);
+      }
+#pragma unroll
+    for (int i = 0; i < BEL; ++i)
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const uint32_t d = sbase + (bidx + st * S::B_STAGE + i * BROWS * BN * V + v) * 16;
+        cp_async16_at(d, bsrc + i * bstep + v);
+        if (sb) cp_async16_at(d + Y_OFF_B, b2src + i * bstep + v);
+      }
+    asrc += BK * V, a2src += BK * V;
+    bsrc += bnext, b2src += bnext;
+  };
+  // the reference's ewise add/sub on this thread's own staged elements
+  auto fold = [&](int st) {
+    if (sa) {
+#pragma unroll
+      for (int i = 0; i < AEL; ++i) {
+        double2* x = smem + aidx + st * S::A_STAGE + i * AROWS * (BK + 1) * V;
+        fold_sum<V>(x, x + S::TOTAL, pr.sa);
+      }
+    }
+    if (sb) {
+#pragma unroll
+      for (int i = 0; i < BEL; ++i) {
+        double2* x = smem + bidx + st * S::B_STAGE + i * BROWS * BN * V;
+        fold_sum<V>(x, x + S::TOTAL, pr.sb);
+      }
+    }
+  };
+  const uint32_t ard = sbase + ty * ((BK + 1) * V * 16);
+  const uint32_t brd = sbase + 2 * A_STAGE_B + tx * (V * 16);
+
+  const int ktiles = l / BK;
+  load(0);
+  cp_async_commit();
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int st = kt & 1;
+    cp_async_wait<0>();
+    fold(st);
+    __syncthreads();
+    if (kt + 1 < ktiles) {
+      load(st ^ 1);
+      cp_async_commit();
+    }
+    uint32_t ap = ard + st * A_STAGE_B, bp = brd + st * B_STAGE_B;
+    const uint32_t aend = ap + BK * V * 16;
+#pragma unroll 1
+    do {
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        double2 a[TM][V], b[TN][V];
+#pragma unroll
+        for (int r = 0; r < TM; ++r)
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            a[r][v] = lds_double2(ap + ((r * NTY * (BK + 1) + u) * V + v) * 16);
+#pragma unroll
+        for (int c = 0; c < TN; ++c)
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            b[c][v] = lds_double2(bp + ((u * BN + c * NTX) * V + v) * 16);
+#pragma unroll
+        for (int r = 0; r < TM; ++r)
+#pragma unroll
+          for (int c = 0; c < TN; ++c) Ops::madd(acc[r][c], a[r], b[c]);
+      }
+      ap += UNROLL * V * 16;
+      bp += UNROLL * BN * V * 16;
+    } while (ap != aend);
+  }
+  __syncthreads();
+
+#pragma unroll
+  for (int r = 0; r < TM; ++r)
+#pragma unroll
+    for (int c = 0; c < TN; ++c) {
+      const int i = m0 + ty + r * NTY, j = n0 + tx + c * NTX;
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        pr.C[((int64_t)i * pr.ldc + j) * V + v] =
+            make_double2(acc[r][c][2 * v], acc[r][c][2 * v + 1]);
+        bad |= !finite2(acc[r][c][2 * v], acc[r][c][2 * v + 1]);
+      }
+    }
+}
+
+template <class Ops, int BM, int BN, int BK, int TM, int TN, int NT>
+__device__ __forceinline__ void gemm_tile_sum_any(const SumProb& pr, int m, int n, int l, int m0,
+                                                  int n0, double2* smem, bool& bad) {
+  if constexpr (SumInteriorOk<Ops, BM, BN, BK, NT>::value) {
+    if (m0 + BM <= m && n0 + BN <= n && l >= BK && l % BK == 0) {
+      gemm_tile_sum_interior<Ops, BM, BN, BK, TM, TN, NT>(pr, l, m0, n0, smem, bad);
+      return;
+    }
+  }
+  gemm_tile_sum<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, m0, n0, smem, bad);
+}
+
 template <class Ops, int BM, int BN, int BK, int TM, int TN, int MINB>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN), MINB)
 gemm_tiled_sum(const SumProblem* __restrict__ probs, int m, int n, int l,
@@ -693,7 +847,7 @@ gemm_tiled_sum(const SumProblem* __restrict__ probs, int m, int n, int l,
   bool bad = false;
   int tm, tn;
   grouped_tile(t, tiles_m, tiles_n, tm, tn);
-  gemm_tile_sum<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, tm * BM, tn * BN, dsmem, bad);
+  gemm_tile_sum_any<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, tm * BM, tn * BN, dsmem, bad);
   if (nonfinite != nullptr && bad) atomicOr(nonfinite, 1);
 }
 
@@ -753,7 +907,7 @@ gemm_persist(const GemmProblem* __restrict__ probs, const SumProblem* __restrict
     const int p = (int)(u / per), t = (int)(u % per);
     const int m0 = (t / tiles_n) * BM, n0 = (t % tiles_n) * BN;
     if constexpr (SUM) {
-      gemm_tile_sum<Ops, BM, BN, BK, TM, TN, NT>(get_sum_prob(sprobs[p]), m, n, l, m0, n0,
+      gemm_tile_sum_any<Ops, BM, BN, BK, TM, TN, NT>(get_sum_prob(sprobs[p]), m, n, l, m0, n0,
                                                 dsmem, bad);
     } else {
       gemm_tile<Ops, BM, BN, BK, TM, TN, NT>(get_prob(probs, single, p), m, n, l, accumulate,
