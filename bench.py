@@ -639,7 +639,12 @@ def run_extras(args, torch, _cuda, mp, inputs, DenseMatrix, A, B, dev, stream, b
         qd = mp.PrecisionSpec.qd()
         qn = n
         Aq, Bq = inputs.gemm_inputs_device("qd", qn, qn, qn, seed=args.seed, device=dev)
-        q_nmin = 64
+        # the block size from the same GPU predictor as the headline's
+        tq0 = time.perf_counter()
+        q_nmin, q_recs = mp.select_block_size(
+            DenseMatrix(qn, qn, qd, Aq), DenseMatrix(qn, qn, qd, Bq), [16, 32, 64, 128, 256],
+            policy=mp.TimingPolicy(warmup_runs=1, measured_runs=2, aggregator="min"))
+        q_phase = time.perf_counter() - tq0
         Cq = torch.empty((qn, qn, 4), dtype=torch.float64, device=dev)
 
         def qd_gemm(m):
@@ -651,7 +656,9 @@ def run_extras(args, torch, _cuda, mp, inputs, DenseMatrix, A, B, dev, stream, b
         tq = min(timed(torch, lambda: qd_gemm(qn), 1))
         out["qd"] = {"what": f"QD blocked mirror m=l=n={qn}, seed {args.seed}, n_min={q_nmin}",
                      "size": qn, "value": 2.0 * float(qn) ** 3 / tq, "unit": "2mnl/s",
-                     "ms": tq * 1e3, "kernel_s": tq, "flops_per_madd": F_QD}
+                     "ms": tq * 1e3, "kernel_s": tq, "flops_per_madd": F_QD, "n_min": q_nmin,
+                     "prediction_phase_wall_s": q_phase,
+                     "predicted_ms": {str(r.n_min): r.predicted_full_s * 1e3 for r in q_recs}}
         del Aq, Bq, Cq
 
     # (3) the opt-in exact tensor-core mode on the same operands (int8

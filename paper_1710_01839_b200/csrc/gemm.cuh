@@ -352,6 +352,17 @@ __device__ __forceinline__ void gemm_tile(const Prob& pr, int m, int n, int l, i
 #ifndef MPMM_INTERIOR_UNROLL
 #define MPMM_INTERIOR_UNROLL 4
 #endif
+#ifndef MPMM_INTERIOR_UNROLL_QD
+#define MPMM_INTERIOR_UNROLL_QD 1
+#endif
+
+// k-steps per trip of the inner loop: the body must stay inside the 32 KB
+// instruction cache (a DD multiply-add is ~0.8 KB of code per accumulator,
+// a QD one ~20 KB with its exact paths)
+template <class Ops>
+struct InteriorUnroll {
+  static constexpr int value = Ops::V == 1 ? MPMM_INTERIOR_UNROLL : MPMM_INTERIOR_UNROLL_QD;
+};
 
 __device__ __forceinline__ void cp_async16_at(uint32_t saddr, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem) : "memory");
@@ -369,7 +380,7 @@ struct InteriorOk {
   static constexpr int V = Ops::V;
   static constexpr bool value = MPMM_INTERIOR != 0 && NT % (BK * V) == 0 && NT % (BN * V) == 0 &&
                                 (BM * BK * V) % NT == 0 && (BK * BN * V) % NT == 0 &&
-                                BK % MPMM_INTERIOR_UNROLL == 0;
+                                BK % InteriorUnroll<Ops>::value == 0;
 };
 
 template <class Ops, int BM, int BN, int BK, int TM, int TN, int NT, bool STREAM = false>
@@ -378,7 +389,7 @@ __device__ __forceinline__ void gemm_tile_interior(const Prob& pr, int m, int n,
                                                    bool& bad, const KReady kr = KReady{nullptr, 0}) {
   constexpr int V = Ops::V;
   constexpr int NTX = BN / TN, NTY = BM / TM;
-  constexpr int UNROLL = MPMM_INTERIOR_UNROLL;
+  constexpr int UNROLL = InteriorUnroll<Ops>::value;
   static_assert(NTX * NTY == NT, "thread tile does not cover the CTA tile");
   using S = TileSmem<Ops, BM, BN, BK>;
   constexpr int AROWS = NT / (BK * V);          // A rows covered by one pass of the CTA's copies
@@ -686,7 +697,7 @@ template <class Ops, int BM, int BN, int BK, int NT>
 struct SumInteriorOk {
   static constexpr bool value = MPMM_INTERIOR != 0 && NT % BK == 0 && NT % BN == 0 &&
                                 (BM * BK) % NT == 0 && (BK * BN) % NT == 0 &&
-                                BK % MPMM_INTERIOR_UNROLL == 0;
+                                BK % InteriorUnroll<Ops>::value == 0;
 };
 
 template <class Ops, int BM, int BN, int BK, int TM, int TN, int NT>
@@ -694,7 +705,7 @@ __device__ __forceinline__ void gemm_tile_sum_interior(const SumProb& pr, int l,
                                                        double2* smem, bool& bad) {
   constexpr int V = Ops::V;
   constexpr int NTX = BN / TN, NTY = BM / TM;
-  constexpr int UNROLL = MPMM_INTERIOR_UNROLL;
+  constexpr int UNROLL = InteriorUnroll<Ops>::value;
   using S = TileSmem<Ops, BM, BN, BK>;
   constexpr int AROWS = NT / BK, BROWS = NT / BN;       // rows per pass of the CTA's copies
   constexpr int AEL = BM / AROWS, BEL = BK / BROWS;     // elements per thread and k-tile
