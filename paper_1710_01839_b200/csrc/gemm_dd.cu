@@ -5,14 +5,19 @@
 // ALGO_BLOCK_FAST runs the same tiles with the opt-in faithful sequence
 // dd_madd_fast (15 FP64 instructions, within the north_star bound, NOT
 // bit-identical to the reference).
-// Tile configurations (n_min -> tile: capi.cu tile_for):
+// Tile configurations (n_min -> tile: capi.cu tile_for; measured in
+// profiles/r02_interior_probe.log, all bitwise equal):
 //   TILE_16    16x16 CTA tile, 1x1 per thread, 256 threads, 4 CTAs/SM
-//   TILE_32    32x32, 2x2, 256 threads, 2 CTAs/SM, k-tiles of 16
+//   TILE_32    32x32, 2x4 per thread, 128 threads, 4 CTAs/SM, k-tiles of 16
+//              (the finest wave quantum: best at 1024^3; 0.2 % behind
+//              TILE_32x64 at 8192^3)
 //   TILE_LPT   persistent 64x64 (4x4) tiles in whole waves + 32x32 quarters
-//   TILE_32x64 32x64, 2x4, 256 threads, 2 CTAs/SM (0.6-0.8 % faster than
-//              TILE_32 in steady state -- fewer LDS per multiply-add --
-//              but a coarser wave quantum: profiles/r02_tile_variants2.log)
-//   TILE_64    64x64, 4x4, 256 threads, plain grid
+//   TILE_32x64 32x64, 2x4, 256 threads, 2 CTAs/SM, k-tiles of 16 (fastest in
+//              steady state: 0.512 of the FP64 roofline at 8192^3)
+//   TILE_64    64x64, 4x4, 256 threads, 1 CTA/SM, plain grid
+// 2x4 register tiles are the sweet spot: 0.75 operand fetches per
+// multiply-add at 16 warps per SM; 2x2 needs 1.0, and 4x4 / 2x8 (0.5 /
+// 0.625) only fit 8-12 warps per SM and lose more to latency than they save.
 #include "gemm.cuh"
 
 // Experiments select another set at build time (tools/exp/build_variant.py
@@ -21,6 +26,14 @@
 #define MPMM_DD32 32, 32, 32, 2, 2, 2
 #define MPMM_DD32x64 32, 64, 8, 2, 4, 2
 #define MPMM_DD64 64, 64, 16, 4, 4, 1
+#elif defined(MPMM_DDCFG) && MPMM_DDCFG == 3   // 128-thread CTAs, four per SM
+#define MPMM_DD32 32, 32, 16, 2, 4, 4
+#define MPMM_DD32x64 16, 64, 16, 2, 4, 4
+#define MPMM_DD64 32, 32, 32, 2, 4, 4
+#elif defined(MPMM_DDCFG) && MPMM_DDCFG == 4   // 2x8 / 4x4 register tiles, 128 threads
+#define MPMM_DD32 32, 64, 16, 2, 8, 3
+#define MPMM_DD32x64 64, 32, 16, 4, 4, 2
+#define MPMM_DD64 64, 32, 16, 4, 4, 3
 #elif defined(MPMM_DDCFG) && MPMM_DDCFG == 2
 #define MPMM_DD32 64, 32, 16, 4, 2, 2
 #define MPMM_DD32x64 32, 64, 32, 2, 4, 2
@@ -30,7 +43,7 @@
 #define MPMM_DD16 16, 16, 16, 1, 1, 4
 #endif
 #ifndef MPMM_DD32
-#define MPMM_DD32 32, 32, 16, 2, 2, 2
+#define MPMM_DD32 32, 32, 16, 2, 4, 4
 #endif
 #ifndef MPMM_DD64
 #define MPMM_DD64 64, 64, 8, 4, 4, 1
