@@ -545,7 +545,12 @@ def run_ours(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_s / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(workload_config(args, world), n_min=args.nmin),
+        # the workload only: identical in both arms (the block size is each
+        # implementation's own tuned knob -- ours is under "block_size")
+        "config": workload_config(args, world),
+        "block_size": {"n_min": args.nmin,
+                       "chosen_by": "GPU slice predictor (select_block_size)" if tuner
+                                    else "--nmin"},
         "e2e": {"value": e2e_value, "unit": "2mnl/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps, "api": api},
         "roofline": roofline,
