@@ -34,6 +34,10 @@
 #define MPMM_DD32 32, 64, 16, 2, 8, 3
 #define MPMM_DD32x64 64, 32, 16, 4, 4, 2
 #define MPMM_DD64 64, 32, 16, 4, 4, 3
+#elif defined(MPMM_DDCFG) && MPMM_DDCFG == 5   // more warps per SM at fewer registers
+#define MPMM_DD32 32, 32, 16, 2, 4, 5
+#define MPMM_DD32x64 32, 32, 16, 2, 4, 6
+#define MPMM_DD64 32, 32, 16, 2, 2, 6
 #elif defined(MPMM_DDCFG) && MPMM_DDCFG == 2
 #define MPMM_DD32 64, 32, 16, 4, 2, 2
 #define MPMM_DD32x64 32, 64, 32, 2, 4, 2
