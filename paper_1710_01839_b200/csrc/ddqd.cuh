@@ -199,6 +199,50 @@ __device__ __forceinline__ bool hi_nonzero(double x) {
   return __int_as_float(__double2hiint(x)) != 0.0f;
 }
 
+// ---- speculative dense path (gemm.cuh gemm_tile_interior, QDSpecOps) ------
+// The gates above decide, per multiply-add, whether the register-only dense
+// sequences apply: 23 + 8 + 3 + 3 high-word tests, their predicate combines
+// and four branches -- ~70 non-FP64 instructions per multiply-add, 3 % of
+// the QD GEMM's time (profiles/r02_qd_variants.log).  The speculative path
+// runs the dense sequences unconditionally and only RECORDS the tests: a
+// running minimum of |high word| (read as float32) over every tested value,
+// one three-input FMNMX3 per two values, no branch.  The CTA looks at the
+// minimum once per k-tile (__syncthreads_or at the barrier it has anyway);
+// if any tested value may have been zero, the tile is abandoned and
+// recomputed from the start by the gated, exact kernel.  A tile that
+// completes therefore executed exactly the operations the gates would have
+// selected -- the same bits -- and a tile that does not is never stored.
+
+// min(|a|, |b|, |c|) of three float32 bit patterns: FMNMX3 |a|,|b|,|c|
+// (sm_100).  A NaN pattern (a high word of |x| >= 2^1017: never zero) is
+// skipped by min; a subnormal pattern stays nonzero (no .ftz).
+__device__ __forceinline__ float min3_abs(float a, float b, float c) {
+  float d;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(fabsf(a)), "f"(fabsf(b)), "f"(fabsf(c)));
+  return d;
+}
+
+__device__ __forceinline__ float hi_as_float(double x) {
+  return __int_as_float(__double2hiint(x));
+}
+
+// fold the high words of t[0..N) into the running minimum m: two values
+// per FMNMX3 (a chain through m -- off the arithmetic's critical path)
+template <int N>
+__device__ __forceinline__ void fold_min_hi(float& m, const double (&t)[N]) {
+#ifdef MPMM_SPEC_NO_TESTS   // experiment only: the cost of the recorded tests
+  return;
+#endif
+#pragma unroll
+  for (int i = 0; i < N; i += 2)
+    m = min3_abs(m, hi_as_float(t[i]), hi_as_float(t[i + 1 < N ? i + 1 : i]));
+}
+
+// true when some folded value had a zero high word (sign ignored)
+__device__ __forceinline__ bool min_hi_is_zero(float m) {
+  return (__float_as_int(m) & 0x7fffffff) == 0;
+}
+
 // ddqd.py:140-172 _renorm5 == _kernels.pyx:237-271: the general case,
 // branch-free: the data-dependent "if e != 0" emission becomes predicated
 // selects.  In the reference's k == 3 case "acc += v" equals the s
@@ -262,6 +306,29 @@ __device__ __forceinline__ void renorm5(double x0, double x1, double x2, double 
   }
 }
 
+// renorm5's fast path taken unconditionally, its gate (e1, e2, e3 nonzero)
+// recorded in m: valid only if the caller later finds m nonzero.
+__device__ __forceinline__ void renorm5_spec(double x0, double x1, double x2, double x3,
+                                             double x4, double out[4], float& m, double extra) {
+  double s, t;
+  s = quick_two_sum(x3, x4, x4);
+  t = quick_two_sum(x2, s, x3);
+  s = quick_two_sum(x1, t, x2);
+  t = quick_two_sum(x0, s, x1);
+  const double sn1 = t + x1;
+  const double e1 = x1 - (sn1 - t);
+  const double sn2 = e1 + x2;
+  const double e2 = x2 - (sn2 - e1);
+  const double sn3 = e2 + x3;
+  const double e3 = x3 - (sn3 - e2);
+  const double tested[4] = {extra, e1, e2, e3};   // `extra`: a value of the caller's to test
+  fold_min_hi(m, tested);
+  out[0] = sn1;
+  out[1] = sn2;
+  out[2] = sn3;
+  out[3] = e3 + x4;
+}
+
 // ddqd.py:175-193 _compress4 for N terms that are ALL nonzero (the zero
 // filter is then the identity).  Fully unrolled: registers only.
 //
@@ -278,8 +345,9 @@ __device__ __forceinline__ void renorm5(double x0, double x1, double x2, double 
 // DADDs, the order test on the FP32/ALU pipes): a knob to balance the FP64
 // pipe against the ALU pipe, which the QD multiply-add loads with its zero
 // tests and selects.
-template <int N, int ORDMASK = 0>
-__device__ __forceinline__ void compress4_dense(double (&v)[N], double out[4]) {
+template <int N, int ORDMASK = 0, bool SPEC = false>
+__device__ __forceinline__ void compress4_dense(double (&v)[N], double out[4],
+                                                float* m = nullptr, double extra = 1.0) {
   double s[4];
 #pragma unroll
   for (int d = 1; d <= (N - 1) + 6; ++d) {
@@ -297,6 +365,7 @@ __device__ __forceinline__ void compress4_dense(double (&v)[N], double out[4]) {
     }
   }
   if constexpr (N <= 4) {
+    static_assert(!SPEC, "the speculative path compresses 23 and 8 terms only");
     double w[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
     for (int i = 0; i < N; ++i) w[4 - N + i] = v[i];
@@ -305,7 +374,10 @@ __device__ __forceinline__ void compress4_dense(double (&v)[N], double out[4]) {
     double tail = 0.0;
 #pragma unroll
     for (int i = 0; i < N - 4; ++i) tail += v[i];
-    renorm5(v[N - 1], v[N - 2], v[N - 3], v[N - 4], tail, out);
+    if constexpr (SPEC)
+      renorm5_spec(v[N - 1], v[N - 2], v[N - 3], v[N - 4], tail, out, *m, extra);
+    else
+      renorm5(v[N - 1], v[N - 2], v[N - 3], v[N - 4], tail, out);
   }
 }
 
@@ -398,6 +470,61 @@ __device__ __forceinline__ void qd_mul_add(double cc[4], const double x[4], cons
   } else {
     compress4_slow<8>(add, cc);
   }
+}
+
+// _qd_mul_add with every gate of qd_mul_add assumed to pass -- the all-dense
+// 23-term and 8-term compressions and both renorm5 fast paths -- and the
+// gates' tests folded into m instead of branched on (see above).  The
+// result is the reference's exactly when m stays nonzero.
+//
+// Which values are folded (18 per multiply-add instead of the gates' 37):
+//  * NOT the 13 products: a launch of the DFMA kernels runs inside the EFT
+//    domain (domain.cuh: exponents of nonzero operand components sum to
+//    >= -900), where two limbs with nonzero high words have a normal
+//    product -- and the operand limbs are folded once per staged k-tile
+//    element by the thread that copied it (qd_spec_stage), not once per use;
+//  * the 10 TwoProd errors;
+//  * of the 8-term gate's cc[0..3], prod[0..3] only cc[3] and prod[3]: the
+//    other six are the sums sn1..sn3 of a renorm5 fast path, and sn_i with a
+//    zero high word is zero or subnormal, hence an exact sum, hence e_i = 0
+//    -- already folded by that renorm5_spec.  (The caller folds all of
+//    cc[0..3] once after its gated first step: qd_spec_seed.)
+//  * both renorm5 gates (e1, e2, e3).
+__device__ __forceinline__ void qd_mul_add_spec(double cc[4], const double x[4],
+                                                const double y[4], float& m) {
+  double t[23];
+  t[0] = two_prod(x[0], y[0], t[1]);
+  t[2] = two_prod(x[0], y[1], t[3]);
+  t[4] = two_prod(x[1], y[0], t[5]);
+  t[6] = two_prod(x[0], y[2], t[7]);
+  t[8] = two_prod(x[1], y[1], t[9]);
+  t[10] = two_prod(x[2], y[0], t[11]);
+  t[12] = two_prod(x[0], y[3], t[13]);
+  t[14] = two_prod(x[1], y[2], t[15]);
+  t[16] = two_prod(x[2], y[1], t[17]);
+  t[18] = two_prod(x[3], y[0], t[19]);
+  t[20] = x[1] * y[3];
+  t[21] = x[2] * y[2];
+  t[22] = x[3] * y[1];
+  const double tested[10] = {t[1], t[3], t[5], t[7], t[9], t[11], t[13], t[15], t[17], t[19]};
+  fold_min_hi(m, tested);
+  double prod[4];
+  const double c3 = cc[3];
+  compress4_dense<23, 0, true>(t, prod, &m, c3);       // + the incoming cc[3]
+  double add[8] = {cc[0], prod[0], cc[1], prod[1], cc[2], prod[2], cc[3], prod[3]};
+  const double p3 = prod[3];
+  compress4_dense<8, 0, true>(add, cc, &m, p3);        // + this step's prod[3]
+}
+
+// one staged 16-byte chunk (two operand limbs), by the thread that copied it
+__device__ __forceinline__ void qd_spec_stage(double2 v, float& m) {
+  m = min3_abs(m, hi_as_float(v.x), hi_as_float(v.y));
+}
+
+// all four accumulator limbs, once, after a gated step (see above)
+__device__ __forceinline__ void qd_spec_seed(const double cc[4], float& m) {
+  const double c[4] = {cc[0], cc[1], cc[2], cc[3]};
+  fold_min_hi(m, c);
 }
 
 // qd_ewise_add / qd_ewise_sub body (_kernels.pyx:407-452)

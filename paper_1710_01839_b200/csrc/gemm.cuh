@@ -25,6 +25,7 @@
 #pragma once
 
 #include <mutex>
+#include <type_traits>
 #include <unordered_map>
 
 #include "common.cuh"
@@ -59,6 +60,50 @@ struct QDOps {
     qd_mul_add(acc, x, y);
   }
 };
+
+// QD with the speculative dense multiply-add on interior tiles (ddqd.cuh
+// qd_mul_add_spec): `madd_spec` records its gates in a per-thread float
+// instead of branching on them; gemm_tile_interior checks it once per
+// k-tile and, when a gate may have failed, recomputes the tile with `Exact`.
+// Everywhere else (edge tiles, the first k-step of a tile, whose
+// accumulator is zero) it is QDOps.
+struct QDSpecOps : QDOps {
+  using Exact = QDOps;
+  __device__ __forceinline__ static void madd_spec(double* acc, const double2* a,
+                                                   const double2* b, float& m) {
+    const double x[4] = {a[0].x, a[0].y, a[1].x, a[1].y};
+    const double y[4] = {b[0].x, b[0].y, b[1].x, b[1].y};
+    qd_mul_add_spec(acc, x, y, m);
+  }
+  // after a gated step: the accumulator's own tests, which madd_spec takes
+  // as folded from then on
+  __device__ __forceinline__ static void spec_seed(const double* acc, float& m) {
+    qd_spec_seed(acc, m);
+  }
+  // a staged operand chunk: the products' share of the 23-term gate
+  __device__ __forceinline__ static void spec_stage(double2 v, float& m) { qd_spec_stage(v, m); }
+};
+
+// Ops::madd, or Ops::madd_spec recording its gates in m
+template <class Ops, bool SPEC>
+struct Madd {
+  __device__ __forceinline__ static void run(double* acc, const double2* a, const double2* b,
+                                             float&) {
+    Ops::madd(acc, a, b);
+  }
+};
+template <class Ops>
+struct Madd<Ops, true> {
+  __device__ __forceinline__ static void run(double* acc, const double2* a, const double2* b,
+                                             float& m) {
+    Ops::madd_spec(acc, a, b, m);
+  }
+};
+
+template <class Ops, class = void>
+struct IsSpec : std::false_type {};
+template <class Ops>
+struct IsSpec<Ops, std::void_t<typename Ops::Exact>> : std::true_type {};
 
 // The reference's sequences with its Dekker TwoProd (_kernels.pyx:19-29),
 // for operands outside the DFMA-exact domain (domain.cuh).
@@ -383,11 +428,15 @@ struct InteriorOk {
                                 BK % InteriorUnroll<Ops>::value == 0;
 };
 
+// Returns false when a speculative tile (IsSpec<Ops>) was abandoned: nothing
+// was stored, the buffers are free, and the caller recomputes the tile with
+// Ops::Exact.  Always true otherwise.
 template <class Ops, int BM, int BN, int BK, int TM, int TN, int NT, bool STREAM = false>
-__device__ __forceinline__ void gemm_tile_interior(const Prob& pr, int m, int n, int l,
+__device__ __forceinline__ bool gemm_tile_interior(const Prob& pr, int m, int n, int l,
                                                    int accumulate, int m0, int n0, double2* smem,
                                                    bool& bad, const KReady kr = KReady{nullptr, 0}) {
   constexpr int V = Ops::V;
+  constexpr bool SPEC = IsSpec<Ops>::value;
   constexpr int NTX = BN / TN, NTY = BM / TM;
   constexpr int UNROLL = InteriorUnroll<Ops>::value;
   static_assert(NTX * NTY == NT, "thread tile does not cover the CTA tile");
@@ -447,10 +496,30 @@ __device__ __forceinline__ void gemm_tile_interior(const Prob& pr, int m, int n,
   }
   load(0);
   cp_async_commit();
+  float gate_min = 1.0f;   // SPEC: min |high word| over every gate test so far
   for (int kt = 0; kt < ktiles; ++kt) {
     const int st = kt & 1;
     cp_async_wait<0>();
-    __syncthreads();
+    if constexpr (SPEC) {
+      // this thread's own copies of k-tile kt have landed: their limbs'
+      // tests, before the vote, so a tile with a zero limb is never started
+#pragma unroll
+      for (int i = 0; i < ACH; ++i)
+        Ops::spec_stage(lds_double2(adst + st * A_STAGE_B + i * (AROWS * (BK + 1) * V * 16)),
+                        gate_min);
+#pragma unroll
+      for (int i = 0; i < BCH; ++i)
+        Ops::spec_stage(lds_double2(bdst + st * B_STAGE_B + i * (BROWS * BN * V * 16)),
+                        gate_min);
+      // the barrier doubles as the vote on the k-tiles computed so far
+#ifdef MPMM_SPEC_IGNORE_VOTE   // experiment only: never fall back (wrong on zero terms)
+      __syncthreads();
+#else
+      if (__syncthreads_or(min_hi_is_zero(gate_min))) return false;
+#endif
+    } else {
+      __syncthreads();
+    }
     if (kt + 1 < ktiles) {
       if constexpr (STREAM) wait_k_panel(kr, (kt + 1) * BK, seen);
       load(st ^ 1);
@@ -458,31 +527,53 @@ __device__ __forceinline__ void gemm_tile_interior(const Prob& pr, int m, int n,
     }
     uint32_t ap = ard + st * A_STAGE_B, bp = brd + st * B_STAGE_B;
     const uint32_t aend = ap + BK * V * 16;
+    // one k-step at offset u of the current addresses
+    auto step = [&](int u, auto spec) {
+      double2 a[TM][V], b[TN][V];
+#pragma unroll
+      for (int r = 0; r < TM; ++r)
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+          a[r][v] = lds_double2(ap + ((r * NTY * (BK + 1) + u) * V + v) * 16);
+#pragma unroll
+      for (int c = 0; c < TN; ++c)
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+          b[c][v] = lds_double2(bp + ((u * BN + c * NTX) * V + v) * 16);
+#pragma unroll
+      for (int r = 0; r < TM; ++r)
+#pragma unroll
+        for (int c = 0; c < TN; ++c)
+          Madd<Ops, decltype(spec)::value>::run(acc[r][c], a[r], b[c], gate_min);
+    };
+    if constexpr (SPEC) {
+      static_assert(UNROLL == 1 && BK > 1, "the speculative loop peels one k-step");
+      if (kt == 0) {
+        // the tile's first k-step meets a zero accumulator (or C's values):
+        // that is the gated sequence's business
+        step(0, std::false_type{});
+#pragma unroll
+        for (int r = 0; r < TM; ++r)
+#pragma unroll
+          for (int c = 0; c < TN; ++c) Ops::spec_seed(acc[r][c], gate_min);
+        ap += V * 16;
+        bp += BN * V * 16;
+      }
+    }
 #pragma unroll 1
     do {
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
-        double2 a[TM][V], b[TN][V];
-#pragma unroll
-        for (int r = 0; r < TM; ++r)
-#pragma unroll
-          for (int v = 0; v < V; ++v)
-            a[r][v] = lds_double2(ap + ((r * NTY * (BK + 1) + u) * V + v) * 16);
-#pragma unroll
-        for (int c = 0; c < TN; ++c)
-#pragma unroll
-          for (int v = 0; v < V; ++v)
-            b[c][v] = lds_double2(bp + ((u * BN + c * NTX) * V + v) * 16);
-#pragma unroll
-        for (int r = 0; r < TM; ++r)
-#pragma unroll
-          for (int c = 0; c < TN; ++c) Ops::madd(acc[r][c], a[r], b[c]);
-      }
+      for (int u = 0; u < UNROLL; ++u) step(u, std::integral_constant<bool, SPEC>{});
       ap += UNROLL * V * 16;
       bp += UNROLL * BN * V * 16;
     } while (ap != aend);
   }
-  __syncthreads();   // the buffers are free for the CTA's next tile
+  // the buffers are free for the CTA's next tile; SPEC: the last vote
+  if constexpr (SPEC) {
+    if (__syncthreads_or(min_hi_is_zero(gate_min))) return false;
+  } else {
+    __syncthreads();
+  }
 
 #pragma unroll
   for (int r = 0; r < TM; ++r)
@@ -496,6 +587,7 @@ __device__ __forceinline__ void gemm_tile_interior(const Prob& pr, int m, int n,
         bad |= !finite2(acc[r][c][2 * v], acc[r][c][2 * v + 1]);
       }
     }
+  return true;
 }
 
 // gemm_tile, through the interior path when the tile qualifies (uniform per
@@ -506,12 +598,24 @@ __device__ __forceinline__ void gemm_tile_any(const Prob& pr, int m, int n, int 
                                               const KReady kr = KReady{nullptr, 0}) {
   if constexpr (InteriorOk<Ops, BM, BN, BK, NT>::value) {
     if (m0 + BM <= m && n0 + BN <= n && l >= BK && l % BK == 0) {
-      gemm_tile_interior<Ops, BM, BN, BK, TM, TN, NT, STREAM>(pr, m, n, l, accumulate, m0, n0,
-                                                              smem, bad, kr);
+      if (gemm_tile_interior<Ops, BM, BN, BK, TM, TN, NT, STREAM>(pr, m, n, l, accumulate, m0,
+                                                                  n0, smem, bad, kr))
+        return;
+      if constexpr (IsSpec<Ops>::value) {
+        // a gate of the speculative sequence may have failed somewhere in
+        // the tile: the exact sequence, from the start (the operands have
+        // landed, so no panel waits)
+        gemm_tile_interior<typename Ops::Exact, BM, BN, BK, TM, TN, NT, false>(
+            pr, m, n, l, accumulate, m0, n0, smem, bad);
+      }
       return;
     }
   }
-  gemm_tile<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, m0, n0, smem, bad, kr);
+  if constexpr (IsSpec<Ops>::value)
+    gemm_tile<typename Ops::Exact, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, m0, n0, smem,
+                                                           bad, kr);
+  else
+    gemm_tile<Ops, BM, BN, BK, TM, TN, NT>(pr, m, n, l, accumulate, m0, n0, smem, bad, kr);
 }
 
 // ---------------------------------------------------------------------------

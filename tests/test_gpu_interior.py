@@ -111,3 +111,58 @@ def test_strassen_fused_leaves_interior(gpu, n, cutoff, monkeypatch):
         monkeypatch.setenv("MPMM_STRASSEN_FUSE", fuse)
         got = mp.matmul_strassen(A, B, cutoff, 32).host_array()
         assert np.array_equal(got, want), f"fuse={fuse}"
+
+
+# --- the speculative dense QD path (ddqd.cuh qd_mul_add_spec) -----------------
+# Interior QD tiles run every gate of the multiply-add as "passed" and vote
+# once per k-tile on whether one may have failed; a failed vote recomputes the
+# tile with the gated sequence.  These operands make gates fail at chosen
+# places of an all-interior product: from a later k-tile on, in one tile
+# only, in every multiply-add (exact products: zero error terms), and through
+# zero limbs; the result must be the oracle's bits every time.
+
+def _qd_product(a, b, n_min):
+    m, l, n = a.shape[0], a.shape[1], b.shape[1]
+    C = torch.full((m, n, 4), float("nan"), dtype=torch.float64, device="cuda")
+    _gemm(4, n_min, _dev(a), _dev(b), C, m, l, n, l, n, n)
+    return C.cpu().numpy()
+
+
+@pytest.mark.parametrize("n_min", [16, 32, 64, 128, 256])
+@pytest.mark.parametrize("case", ["late_zeros", "one_tile", "exact_products", "zero_limbs",
+                                  "cancel"])
+def test_qd_speculation_falls_back(gpu, n_min, case):
+    m, l, n = 64, 64, 64
+    a, b = inputs.gemm_inputs("qd", m, l, n, seed=21)
+    rng = np.random.default_rng(22)
+    if case == "late_zeros":          # whole elements vanish from the third k-tile on
+        a[:, 40:, :] *= (rng.random((m, l - 40, 1)) < 0.7)
+    elif case == "one_tile":          # one element of B: only the tiles of column 5 fail
+        b[50, 5, :] = 0.0
+    elif case == "exact_products":    # powers of two: every TwoProd error is zero
+        a = np.ldexp(np.where(rng.random(a.shape) < 0.5, 1.0, -1.0),
+                     rng.integers(-8, 8, a.shape) - 55 * np.arange(4))
+        b = np.ldexp(np.where(rng.random(b.shape) < 0.5, 1.0, -1.0),
+                     rng.integers(-8, 8, b.shape) - 55 * np.arange(4))
+    elif case == "zero_limbs":        # double-precision values stored as QD
+        a[..., 1:] = 0.0
+        b[..., 2:] = 0.0
+    elif case == "cancel":            # second half of k cancels the first: the sum passes 0
+        a[:, 32:, :] = a[:, :32, :]
+        b[32:, :, :] = -b[:32, :, :]
+    want = oracle.matmul_simple(np.ascontiguousarray(a), np.ascontiguousarray(b))
+    got = _qd_product(np.ascontiguousarray(a), np.ascontiguousarray(b), n_min)
+    assert np.array_equal(got, want)
+
+
+def test_qd_speculation_accumulate_from_zero_and_nonzero(gpu):
+    # C += A B with C zero (the first step's gate fails -> gated first step)
+    # and with C random (speculative from the second step on)
+    m, l, n = 32, 32, 48
+    a, b = inputs.gemm_inputs("qd", m, 2 * l, n, seed=23)
+    want = oracle.matmul_simple(a, b)
+    A, B = _dev(a), _dev(b)
+    C = torch.zeros((m, n, 4), dtype=torch.float64, device="cuda")
+    _gemm(4, 64, A, B, C, m, l, n, 2 * l, n, n, accumulate=True)
+    _gemm(4, 64, A[:, l:], B[l:], C, m, l, n, 2 * l, n, n, accumulate=True)
+    assert np.array_equal(C.cpu().numpy(), want)
