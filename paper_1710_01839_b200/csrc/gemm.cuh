@@ -547,17 +547,21 @@ __device__ __forceinline__ bool gemm_tile_interior(const Prob& pr, int m, int n,
           Madd<Ops, decltype(spec)::value>::run(acc[r][c], a[r], b[c], gate_min);
     };
     if constexpr (SPEC) {
-      static_assert(UNROLL == 1 && BK > 1, "the speculative loop peels one k-step");
+      static_assert(BK > UNROLL, "the speculative loop peels its first trip");
       if (kt == 0) {
         // the tile's first k-step meets a zero accumulator (or C's values):
-        // that is the gated sequence's business
-        step(0, std::false_type{});
+        // that is the gated sequence's business (the whole first trip, so the
+        // loop below keeps its trip length)
+#pragma unroll 1
+        for (int u = 0; u < UNROLL; ++u) {
+          step(0, std::false_type{});
+          ap += V * 16;
+          bp += BN * V * 16;
+        }
 #pragma unroll
         for (int r = 0; r < TM; ++r)
 #pragma unroll
           for (int c = 0; c < TN; ++c) Ops::spec_seed(acc[r][c], gate_min);
-        ap += V * 16;
-        bp += BN * V * 16;
       }
     }
 #pragma unroll 1
