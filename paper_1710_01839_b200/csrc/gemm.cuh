@@ -607,10 +607,10 @@ __device__ __forceinline__ void gemm_tile_any(const Prob& pr, int m, int n, int 
         return;
       if constexpr (IsSpec<Ops>::value) {
         // a gate of the speculative sequence may have failed somewhere in
-        // the tile: the exact sequence, from the start (the operands have
-        // landed, so no panel waits)
-        gemm_tile_interior<typename Ops::Exact, BM, BN, BK, TM, TN, NT, false>(
-            pr, m, n, l, accumulate, m0, n0, smem, bad);
+        // the tile: the exact sequence, from the start (streamed operands:
+        // with the same panel waits -- later k-panels may not have landed)
+        gemm_tile_interior<typename Ops::Exact, BM, BN, BK, TM, TN, NT, STREAM>(
+            pr, m, n, l, accumulate, m0, n0, smem, bad, kr);
       }
       return;
     }

@@ -166,3 +166,20 @@ def test_qd_speculation_accumulate_from_zero_and_nonzero(gpu):
     _gemm(4, 64, A, B, C, m, l, n, 2 * l, n, n, accumulate=True)
     _gemm(4, 64, A[:, l:], B[l:], C, m, l, n, 2 * l, n, n, accumulate=True)
     assert np.array_equal(C.cpu().numpy(), want)
+
+
+def test_qd_speculation_falls_back_under_streamed_operands(gpu):
+    # host operands, k-panel streaming (64-column panels): interior QD tiles
+    # whose gates first fail in the LAST k-panel -- the abandoned tile's exact
+    # recomputation must wait for the panels like the first attempt did
+    from paper_1710_01839_b200.matrix import DenseMatrix
+    m, l, n = 64, 512, 64
+    a, b = inputs.gemm_inputs("qd", m, l, n, seed=24)
+    a[:, 480:, 1:] = 0.0                       # zero limbs from k = 480 on
+    want = oracle.matmul_simple(a, b)
+    qd = mp.PrecisionSpec.qd()
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
+    for n_min in (16, 64):
+        A, B = DenseMatrix(m, l, qd, pin(a)), DenseMatrix(l, n, qd, pin(b))
+        for _ in range(2):
+            assert np.array_equal(mp.matmul_block(A, B, n_min).host_array(), want)
