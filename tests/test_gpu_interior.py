@@ -130,7 +130,7 @@ def _qd_product(a, b, n_min):
 
 @pytest.mark.parametrize("n_min", [16, 32, 64, 128, 256])
 @pytest.mark.parametrize("case", ["late_zeros", "one_tile", "exact_products", "zero_limbs",
-                                  "cancel"])
+                                  "cancel", "bits28", "bits27", "bits26_53"])
 def test_qd_speculation_falls_back(gpu, n_min, case):
     m, l, n = 64, 64, 64
     a, b = inputs.gemm_inputs("qd", m, l, n, seed=21)
@@ -147,6 +147,22 @@ def test_qd_speculation_falls_back(gpu, n_min, case):
     elif case == "zero_limbs":        # double-precision values stored as QD
         a[..., 1:] = 0.0
         b[..., 2:] = 0.0
+    elif case in ("bits28", "bits27", "bits26_53"):
+        # limbs with exactly 28 significant bits pass the staging test (their
+        # products have 55-56 bits: inexact, the speculation must be exact);
+        # 27 bits fail it; 26-bit limbs of A against full 53-bit limbs of B
+        # fail it although every product is inexact (the test is sufficient,
+        # not necessary)
+        def limbs(shape, bits):
+            mant = rng.integers(1 << (bits - 1), 1 << bits, shape) | 1   # odd, `bits` long
+            sign = np.where(rng.random(shape) < 0.5, 1.0, -1.0)
+            return np.ldexp(sign * mant.astype(np.float64),
+                            rng.integers(-3, 3, shape) - bits - 53 * np.arange(4))
+        if case == "bits26_53":
+            a = limbs(a.shape, 26)
+        else:
+            nb = 28 if case == "bits28" else 27
+            a, b = limbs(a.shape, nb), limbs(b.shape, nb)
     elif case == "cancel":            # second half of k cancels the first: the sum passes 0
         a[:, 32:, :] = a[:, :32, :]
         b[32:, :, :] = -b[:32, :, :]
