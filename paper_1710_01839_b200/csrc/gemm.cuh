@@ -15,6 +15,14 @@
 // Kernels are bound by the FP64 pipe (DD: 50 FP64 instructions per
 // multiply-add; QD: ~786).  Operand tiles are staged in shared memory with
 // cp.async double buffering; each thread owns a TM x TN register tile.
+// Two code paths compute a tile, bit for bit the same: gemm_tile (any shape:
+// bounds predicates, zero fill) and gemm_tile_interior (the whole tile
+// inside C, l a multiple of the k-tile: no predicates, one barrier per
+// k-tile, advanced addresses -- every instruction that is not FP64
+// arithmetic costs the FP64 pipe an issue cycle).  On interior QD tiles the
+// reference's data-dependent zero-term gates are run speculatively
+// (QDSpecOps): recorded, voted once per k-tile, the tile recomputed by the
+// gated sequence if a vote fails.
 //
 // Load balance.  At moderate sizes the tile count is a few waves of 148
 // SMs, and the last partial wave costs up to half a wave of idle FP64
