@@ -199,3 +199,16 @@ def test_qd_speculation_falls_back_under_streamed_operands(gpu):
         A, B = DenseMatrix(m, l, qd, pin(a)), DenseMatrix(l, n, qd, pin(b))
         for _ in range(2):
             assert np.array_equal(mp.matmul_block(A, B, n_min).host_array(), want)
+
+
+def test_randomised_blocked_parity(gpu):
+    # tools/fuzz_gemm.py: random shapes around the tile boundaries, every
+    # block size, DD/QD, accumulate, strided views, zero-sprinkled QD operands
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz_gemm.py"), "120", "5"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "0 mismatches" in r.stdout
