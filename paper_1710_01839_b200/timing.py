@@ -18,11 +18,13 @@ from dataclasses import dataclass, field
 
 from .errors import MeasurementError
 
-_AGGREGATORS = {
-    "median": statistics.median,
-    "min": min,
-    "mean": statistics.fmean,
-}
+def _reduce(samples, how):
+    if how == "median":
+        return statistics.median(samples)
+    return min(samples) if how == "min" else statistics.fmean(samples)
+
+
+_AGGREGATORS = ("median", "min", "mean")
 
 
 def device_clock():
@@ -38,39 +40,54 @@ def device_clock():
 
 @dataclass
 class TimingPolicy:
+    """The reference's fields and defaults (timing.py:22-35); only the
+    default clock differs (device_clock)."""
     warmup_runs: int = 0
     measured_runs: int = 1
     aggregator: str = "median"
     clock: object = field(default=device_clock, repr=False)
 
     def __post_init__(self):
-        if self.measured_runs < 1:
-            raise ValueError("measured_runs must be >= 1")
-        if self.warmup_runs < 0:
-            raise ValueError("warmup_runs must be >= 0")
-        if self.aggregator not in _AGGREGATORS:
-            raise ValueError(f"unknown aggregator {self.aggregator!r}")
+        problems = {
+            "measured_runs must be >= 1": self.measured_runs < 1,
+            "warmup_runs must be >= 0": self.warmup_runs < 0,
+            f"unknown aggregator {self.aggregator!r}": self.aggregator not in _AGGREGATORS,
+        }
+        for message, wrong in problems.items():
+            if wrong:
+                raise ValueError(message)
+
+
+def _collect(fn, policy, setup, interval):
+    """Warm-up runs, then ``measured_runs`` samples of ``interval(fn)`` --
+    one timed call each, ``setup`` before every call and never timed --
+    aggregated as the policy says."""
+    def one(timed):
+        if setup is not None:
+            setup()
+        if not timed:
+            fn()
+            return None
+        elapsed = interval(fn)
+        if elapsed <= 0.0:
+            raise MeasurementError(f"non-positive elapsed time {elapsed!r}")
+        return elapsed
+
+    for _ in range(policy.warmup_runs):
+        one(False)
+    return _reduce([one(True) for _ in range(policy.measured_runs)], policy.aggregator)
 
 
 def measure(fn, policy, setup=None):
-    """Elapsed seconds for ``fn()`` under ``policy`` (reference
-    timing.py:38-59); ``setup`` runs before every sample, untimed."""
+    """Elapsed seconds for ``fn()`` under ``policy`` by the policy's clock
+    (reference timing.py:38-59); ``setup`` runs before every sample, untimed."""
     clock = policy.clock
-    for _ in range(policy.warmup_runs):
-        if setup is not None:
-            setup()
-        fn()
-    samples = []
-    for _ in range(policy.measured_runs):
-        if setup is not None:
-            setup()
+
+    def interval(f):
         t0 = clock()
-        fn()
-        elapsed = clock() - t0
-        if elapsed <= 0.0:
-            raise MeasurementError(f"non-positive elapsed time {elapsed!r}")
-        samples.append(elapsed)
-    return _AGGREGATORS[policy.aggregator](samples)
+        f()
+        return clock() - t0
+    return _collect(fn, policy, setup, interval)
 
 
 class EventTimer:
@@ -103,18 +120,8 @@ class EventTimer:
 def measure_events(fn, policy, setup=None, stream=None):
     """Like :func:`measure` but each sample is a CUDA-event interval on
     ``stream`` around the device work ``fn`` enqueues."""
-    for _ in range(policy.warmup_runs):
-        if setup is not None:
-            setup()
-        fn()
-    samples = []
-    for _ in range(policy.measured_runs):
-        if setup is not None:
-            setup()
+    def interval(f):
         with EventTimer(stream) as t:
-            fn()
-        elapsed = t.seconds
-        if elapsed <= 0.0:
-            raise MeasurementError(f"non-positive elapsed time {elapsed!r}")
-        samples.append(elapsed)
-    return _AGGREGATORS[policy.aggregator](samples)
+            f()
+        return t.seconds
+    return _collect(fn, policy, setup, interval)
