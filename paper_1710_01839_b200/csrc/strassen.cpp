@@ -68,12 +68,48 @@ class Driver {
   }
 
   // scratch allocations of the current scope, freed stream-ordered
+  // One stream-ordered allocation for all the scratch matrices a level's
+  // nodes are about to ask for (`bytes`, an upper bound; alloc() carves it
+  // and falls back to its own allocation when the slab runs out).  A level
+  // of 7^5 nodes otherwise makes ~50 000 cudaMallocAsync / cudaFreeAsync
+  // calls -- ~0.1 s of host time during which the GPU, already through the
+  // few launches of the level above, waits for the leaf launches.
+  cudaError_t begin_slab(size_t bytes) {
+    slab_ = nullptr;
+    slab_left_ = 0;
+    if (bytes == 0) return cudaSuccess;
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, bytes, s_);
+    if (e == cudaErrorMemoryAllocation) {
+      // no contiguous block of that size: the nodes allocate one by one
+      (void)cudaGetLastError();
+      return cudaSuccess;
+    }
+    if (e != cudaSuccess) return e;
+    scope_.push_back(p);
+    slab_ = static_cast<char*>(p);
+    slab_left_ = bytes;
+    return cudaSuccess;
+  }
+  void end_slab() { slab_ = nullptr, slab_left_ = 0; }
+  static size_t slab_round(size_t bytes) { return (bytes + 255) & ~static_cast<size_t>(255); }
+  size_t matrix_bytes(int64_t rows, int64_t cols) const {
+    return slab_round(static_cast<size_t>(rows * cols * comps_) * sizeof(double));
+  }
+
   cudaError_t alloc(int64_t rows, int64_t cols, bool zero, View* v) {
     size_t bytes = static_cast<size_t>(rows * cols * comps_) * sizeof(double);
     void* p = nullptr;
-    cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : sizeof(double), s_);
-    if (e != cudaSuccess) return e;
-    scope_.push_back(p);
+    cudaError_t e = cudaSuccess;
+    if (bytes && slab_round(bytes) <= slab_left_) {
+      p = slab_;
+      slab_ += slab_round(bytes);
+      slab_left_ -= slab_round(bytes);
+    } else {
+      e = cudaMallocAsync(&p, bytes ? bytes : sizeof(double), s_);
+      if (e != cudaSuccess) return e;
+      scope_.push_back(p);
+    }
     if (zero && bytes) {
       if ((e = cudaMemsetAsync(p, 0, bytes, s_)) != cudaSuccess) return e;
     }
@@ -202,7 +238,16 @@ class Driver {
     const int64_t me = m + (m & 1), le = l + (l & 1), ne = n + (n & 1);
     const int64_t hm = me / 2, hl = le / 2, hn = ne / 2;
     std::vector<EwiseProblem> sa, sb;
-    cudaError_t e = cudaSuccess;
+    // the level's scratch in one allocation: per node the seven products and
+    // (unless the sums are folded into the leaves) the ten operand sums,
+    // plus the padded copies of odd-sized operands and results
+    size_t per = matrix_bytes(7 * hm, hn);
+    if (!fuse) per += matrix_bytes(5 * hm, hl) + matrix_bytes(5 * hl, hn);
+    if (me != m || le != l) per += matrix_bytes(me, le);
+    if (le != l || ne != n) per += matrix_bytes(le, ne);
+    if (me != m || ne != n) per += matrix_bytes(me, ne);
+    cudaError_t e = begin_slab(per * nodes.size());
+    if (e != cudaSuccess) return e;
     for (Node& nd : nodes) {
       View Ap, Bp, ta, tb, pt;
       if ((e = padded(nd.A, me, le, &Ap)) != cudaSuccess) return e;
@@ -276,6 +321,7 @@ class Driver {
         stats_[1] += 18;
       }
     }
+    end_slab();
     if ((e = ewise(sa, hm, hl)) != cudaSuccess) return e;
     return ewise(sb, hl, hn);
   }
@@ -399,6 +445,8 @@ class Driver {
   std::vector<void*> scope_;
   const int* words_ = nullptr;
   int depth_ = 0;
+  char* slab_ = nullptr;       // the current level's scratch slab (begin_slab)
+  size_t slab_left_ = 0;
 
  public:
   // fold the last level's operand sums into the leaf launch: 1 always,
