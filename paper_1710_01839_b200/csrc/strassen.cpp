@@ -32,6 +32,7 @@ namespace mpmm {
 namespace {
 
 constexpr int64_t kMaxBatch = 65535;
+constexpr size_t kFusedChunk = 1024;   // parents per expand + leaf launch of the fused last level
 
 struct View {
   double* p;
@@ -379,7 +380,26 @@ class Driver {
       // when the leaves are small enough for that to pay
       fused = std::min(hm, std::min(hl, hn)) <= cutoff_ &&
               (fuse_ == 1 || (fuse_ < 0 && std::max(hm, std::max(hl, hn)) <= kFuseLeafMax));
-      if ((e = expand(nodes, m, l, n, &children, fused)) != cudaSuccess) return e;
+      if (fused) {
+        // The last expansion launches nothing itself (its sums are folded
+        // into the leaves), and planning 7^d leaves takes the host tens of
+        // milliseconds: expand and launch the parents in chunks, so the GPU
+        // starts on the first leaves while the host plans the rest.
+        for (size_t lo = 0; lo < nodes.size(); lo += kFusedChunk) {
+          const size_t hi = std::min(nodes.size(), lo + kFusedChunk);
+          std::vector<Node> part(nodes.begin() + lo, nodes.begin() + hi), kids;
+          kids.reserve(7 * part.size());
+          if ((e = expand(part, m, l, n, &kids, true)) != cudaSuccess) return e;
+          std::copy(part.begin(), part.end(), nodes.begin() + lo);   // P, C, crop
+          if ((e = leaves_fused(kids, hm, hl, hn)) != cudaSuccess) return e;
+        }
+        levels.push_back(std::move(nodes));
+        lm.push_back(m);
+        ln.push_back(n);
+        nodes.clear();
+        break;   // the children were leaves
+      }
+      if ((e = expand(nodes, m, l, n, &children, false)) != cudaSuccess) return e;
       levels.push_back(std::move(nodes));
       lm.push_back(m);
       ln.push_back(n);
@@ -388,9 +408,7 @@ class Driver {
       l = (l + (l & 1)) / 2;
       n = (n + (n & 1)) / 2;
     }
-    if (fused) {
-      if ((e = leaves_fused(nodes, m, l, n)) != cudaSuccess) return e;
-    } else {
+    if (!fused) {
       std::vector<GemmProblem> probs;
       probs.reserve(nodes.size());
       for (const Node& nd : nodes)
