@@ -665,6 +665,18 @@ def run_extras(args, torch, _cuda, mp, inputs, DenseMatrix, A, B, dev, stream, b
                      "ms": tq * 1e3, "kernel_s": tq, "flops_per_madd": F_QD, "n_min": q_nmin,
                      "prediction_phase_wall_s": q_phase,
                      "predicted_ms": {str(r.n_min): r.predicted_full_s * 1e3 for r in q_recs}}
+        # the tuner's QD pick at this size (profiles/r02_cfg4_qd.tbl): Strassen
+        # at cutoff 32, bit-identical to the reference's Strassen
+        if os.environ.get("BENCH_SKIP_QD_STRASSEN") != "1":
+            Aqd, Bqd = DenseMatrix(qn, qn, qd, Aq), DenseMatrix(qn, qn, qd, Bq)
+            q_cut = 32
+            mp.matmul_strassen(Aqd, Bqd, q_cut, q_nmin)
+            torch.cuda.synchronize()
+            tqs = min(timed(torch, lambda: mp.matmul_strassen(Aqd, Bqd, q_cut, q_nmin), 1))
+            out["qd"]["tuner_pick"] = {"choice": f"strassen:{q_cut}/{q_nmin}", "ms": tqs * 1e3,
+                                       "value": 2.0 * float(qn) ** 3 / tqs,
+                                       "unit": "effective 2mnl/s", "bit_identical": True}
+            del Aqd, Bqd
         del Aq, Bq, Cq
 
     # (3) the opt-in exact tensor-core mode on the same operands (int8
