@@ -32,6 +32,7 @@ namespace mpmm {
 namespace {
 
 constexpr int64_t kMaxBatch = 65535;
+constexpr size_t kEwiseChunk = 16384;  // elementwise problems per upload + launch (as they are planned)
 constexpr size_t kFusedChunk = 1024;   // parents per expand + leaf launch of the fused last level
 
 struct View {
@@ -308,6 +309,13 @@ class Driver {
       sb.push_back(ew(SB[2], b21, b11, -1));
       sb.push_back(ew(SB[3], b11, b12, 1));
       sb.push_back(ew(SB[4], b21, b22, 1));
+      // launch the sums planned so far (the GPU works while the host plans on)
+      if (sa.size() >= kEwiseChunk) {
+        if ((e = ewise(sa, hm, hl)) != cudaSuccess) return e;
+        if ((e = ewise(sb, hl, hn)) != cudaSuccess) return e;
+        sa.clear();
+        sb.clear();
+      }
       const View xs[7] = {SA[0], SA[1], a11, a22, SA[2], SA[3], SA[4]};
       const View ys[7] = {SB[0], b11, SB[1], SB[2], b22, SB[3], SB[4]};
       for (int q = 0; q < 7; ++q) {
@@ -337,6 +345,10 @@ class Driver {
       items.push_back(ew(sub(nd.C, 0, hn, hm, hn), P[2], P[4], 1));
       items.push_back(ew(sub(nd.C, hm, 0, hm, hn), P[1], P[3], 1));
       items.push_back(ew3(sub(nd.C, hm, hn, hm, hn), P[0], P[2], 1, P[1], -1, P[5], 1));
+      if (items.size() >= kEwiseChunk) {
+        if (cudaError_t ce = ewise(items, hm, hn); ce != cudaSuccess) return ce;
+        items.clear();
+      }
     }
     cudaError_t e = ewise(items, hm, hn);
     for (const Node& nd : nodes)
