@@ -383,6 +383,7 @@ def run_ours(args, rank, world, local_rank):
         tuner = {"chosen_n_min": best, "prediction_phase_wall_s": phase, "records": [
             {"n_min": r.n_min, "slice_rows": r.slice_rows, "slice_ms": r.slice_time_s * 1e3,
              "slice2_rows": r.slice2_rows, "slice2_ms": (r.slice2_time_s or 0.0) * 1e3,
+             "superseded_slices_ms": r.extra_time_s * 1e3,
              "predicted_ms": r.predicted_full_s * 1e3} for r in recs]}
     if rank != 0 and world > 1:
         del A_full

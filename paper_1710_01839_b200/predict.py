@@ -39,6 +39,12 @@ class PredictionRecord:
     predicted_full_s: float
     slice2_rows: int = 0          # wave-aware mode: the second (smaller) slice
     slice2_time_s: float = 0.0
+    extra_time_s: float = 0.0     # slices timed and then superseded by a refinement
+
+    @property
+    def phase_time_s(self):
+        """Everything timed for this candidate (what the prediction cost)."""
+        return self.slice_time_s + (self.slice2_time_s or 0.0) + self.extra_time_s
 
     @property
     def scale_factor(self):
@@ -175,12 +181,13 @@ def choose_best(records):
 
 
 def select_block_size(a, b, candidates, threads=1, policy=None,
-                      slice_multiplier=DEFAULT_SLICE_MULTIPLIER, wave_aware=None):
+                      slice_multiplier=DEFAULT_SLICE_MULTIPLIER, wave_aware=None, refine=True):
     """Predict the full-size time of each candidate; returns
     ``(best_n_min, records)`` (reference predict.py:83-104).
 
     ``wave_aware`` (default: on for the cuda backend) switches from the
-    reference's row ratio to the wave model above."""
+    reference's row ratio to the wave model above; ``refine`` re-measures
+    candidates predicted within 1 % of the best on a larger slice."""
     if not candidates:
         raise ValueError("need at least one block-size candidate")
     if list(candidates) != sorted(candidates):
@@ -209,4 +216,37 @@ def select_block_size(a, b, candidates, threads=1, policy=None,
             records.append(PredictionRecord(n_min=n_min, slice_rows=rows, full_rows=a.rows,
                                             slice_time_s=elapsed,
                                             predicted_full_s=elapsed * (a.rows / rows)))
+    if wave_aware and refine:
+        records = _refine_close_candidates(a, b, records, threads, policy, slice_multiplier)
     return choose_best(records), records
+
+
+def _refine_close_candidates(a, b, records, threads, policy, slice_multiplier,
+                             within=0.01, growth=4):
+    """A second look at candidates whose predictions are within ``within`` of
+    the best: the two-slice fit extrapolates from ~1-3 waves of CTAs to
+    hundreds and is good to a few tenths of a percent, which is also how far
+    apart the best tile configurations are at large sizes.  Each close
+    candidate gets one ``growth`` times larger slice (at most half the
+    product), and the fit is redone through its two largest slices; the
+    superseded slice's time stays charged (``extra_time_s``)."""
+    best = min(r.predicted_full_s for r in records)
+    close = [i for i, r in enumerate(records)
+             if r.predicted_full_s <= best * (1.0 + within) and r.slice2_rows
+             and r.slice_rows < a.rows]
+    if len(close) < 2:
+        return records
+    out = list(records)
+    for i in close:
+        r = records[i]
+        model = wave_model(a.prec.comps, r.n_min)
+        r3 = min(a.rows // 2, growth * r.slice_rows)
+        r3 = (r3 // model.tile_m) * model.tile_m
+        if r3 <= r.slice_rows:
+            continue
+        t3, _ = time_slice(a, b, r.n_min, threads, policy, slice_multiplier, r3)
+        predicted = fit_two_slices(model, r.slice_rows, r.slice_time_s, r3, t3, a.rows, b.cols)
+        out[i] = PredictionRecord(r.n_min, r3, a.rows, t3, predicted,
+                                  slice2_rows=r.slice_rows, slice2_time_s=r.slice_time_s,
+                                  extra_time_s=r.extra_time_s + (r.slice2_time_s or 0.0))
+    return out

@@ -137,7 +137,7 @@ def test_acceptance_criteria_6_7_on_the_gpu(gpu, tok, n):
     cands = [16, 32, 64, 128, 256]
     best, recs = mp.select_block_size(A, B, cands, policy=pol)
     full = {c: _measure_block(A, B, c, 1, pol) for c in cands}
-    phase = sum(r.slice_time_s + r.slice2_time_s for r in recs)
+    phase = sum(r.phase_time_s for r in recs)
     for r in recs:
         err = mp.rel_diff(r.predicted_full_s, full[r.n_min])
         print(f"{tok} n={n} n_min={r.n_min} predicted={r.predicted_full_s * 1e3:.2f} ms "
