@@ -25,6 +25,10 @@
 #define MPMM_QD64 16, 16, 8, 1, 1, 3
 #define MPMM_QD32x64 8, 32, 16, 1, 1, 2
 #define MPMM_QDLPT 16, 16, 16, 1, 1, 2
+#ifndef MPMM_QDSUM_BK
+#define MPMM_QDSUM_BK 8
+#endif
+#define MPMM_QDSUM 16, 16, MPMM_QDSUM_BK, 1, 1, 2   // Strassen leaves with folded operand sums
 
 namespace mpmm {
 
@@ -38,7 +42,7 @@ using QDBlockOps = QDOps;
 
 cudaError_t qd_gemm_launch(const GemmArgs& g) {
   if (g.m <= 0 || g.n <= 0 || g.batch <= 0) return cudaSuccess;
-  if (g.sprobs != nullptr) return launch_tiled_sum<QDOps, 16, 16, 8, 1, 1, 2>(g);
+  if (g.sprobs != nullptr) return launch_tiled_sum<QDOps, MPMM_QDSUM>(g);
   if (g.algo == ALGO_SIMPLE) return launch_simple<QDOps>(g);
   if (g.algo != ALGO_BLOCK) return cudaErrorNotSupported;
   switch (g.tile) {
