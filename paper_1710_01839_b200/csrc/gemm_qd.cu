@@ -25,10 +25,7 @@
 #define MPMM_QD64 16, 16, 8, 1, 1, 3
 #define MPMM_QD32x64 8, 32, 16, 1, 1, 2
 #define MPMM_QDLPT 16, 16, 16, 1, 1, 2
-#ifndef MPMM_QDSUM_BK
-#define MPMM_QDSUM_BK 8
-#endif
-#define MPMM_QDSUM 16, 16, MPMM_QDSUM_BK, 1, 1, 2   // Strassen leaves with folded operand sums
+#define MPMM_QDSUM 16, 16, 8, 1, 1, 2   // Strassen leaves with folded operand sums (16-deep k-tiles: no gain)
 
 namespace mpmm {
 
