@@ -212,3 +212,20 @@ def test_randomised_blocked_parity(gpu):
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "0 mismatches" in r.stdout
+
+
+def test_strassen_driver_regimes(gpu):
+    # tools/exp/strassen_fuzz_deep.py: deep recursions with padded levels,
+    # fused and materialised last levels, chunked launches (> 1024 parents,
+    # > 16384 elementwise problems per level), and the depth-first mode
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("MPMM_STRASSEN_FUSE", None)
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "exp",
+                                                     "strassen_fuzz_deep.py"), "5"],
+                       capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "0 mismatches" in r.stdout
